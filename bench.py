@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark: QTT apply y = A x in fp64 on B200 (Alg. 2).
+
+Workload (BASELINE.json metric): config c4, N = 2^24 (256^3 volume grid), tapered
+rank profile r_k = min(2^k, 2^(24-k), 48), one RHS x ~ U[-1,1), seed 0.
+A "step" is one full apply (all d = 24 levels) over one input vector that is
+resident in HBM.  Every buffer exceeds L2 (x 128 MiB; intermediates up to
+6.4 GB), so no L2 flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
+
+Multi-GPU (--gpus N, launched by torchrun): N independent replicas (weak
+scaling, no data-path collective).  Rank 0 prints ONE
+JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "QTT apply fp64 GFLOP/s, ms/apply and % of per-stage roofline at N=2^24 on 1 B200"
+UNIT = "GFLOP/s"
+HBM_FALLBACK_GBS = 6650.0        # B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json is absent)
+FP64_NOMINAL_TFLOPS = 37.2       # 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
+
+
+# --------------------------------------------------------------------------- peaks
+def load_peaks():
+    hbm, hbm_src = HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            hbm = float(json.load(f)["hbm_gbs"])
+        hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    fp64, fp64_src = FP64_NOMINAL_TFLOPS, "nominal"
+    q = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+    if os.path.exists(q):
+        with open(q) as f:
+            d = json.load(f)
+        vals = [v for k, v in d.items() if k.startswith("dmma_")]
+        if vals:
+            fp64, fp64_src = max(vals), "measured (profiles/r01_fp64_peaks.json, DMMA burst)"
+    return hbm, hbm_src, fp64, fp64_src
+
+
+def load_traffic(config):
+    """dram read+write bytes per launch of the dominant kernel from the committed
+    ncu --set full capture summary (profiles/*_ncu_full_summary.json), or None."""
+    import glob
+    best = None
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full_summary.json"))):
+        try:
+            with open(p) as f:
+                d = json.load(f)
+            if d.get("config") == config and d.get("dram_bytes_per_launch"):
+                best = (float(d["dram_bytes_per_launch"]), os.path.basename(p))
+        except Exception:
+            pass
+    return best
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.05)
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 8:
+                self.rows.append(parts)
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        # "under load": samples within 25% of the busiest clock seen
+        load = [s for s in sm if s >= 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None,
+                "samples": len(rows), "reasons": reasons}
+
+
+# --------------------------------------------------------------------------- distributed plumbing
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = os.environ.get("QTT_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def dist_max(value: float, world: int, device=None) -> float:
+    """Max over ranks (device-timed numbers are reduced, never wall clock)."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# --------------------------------------------------------------------------- helpers
+def config_desc(cfg, nrhs):
+    prof = "tapered r_k=min(2^k,2^(d-k),48)" if cfg.name == "c4" else f"r={max(cfg.ranks)}"
+    return {"workload": f"{cfg.name}: QTT apply d={cfg.d} N=2^{cfg.d} {prof}, nrhs={nrhs}, seed {cfg.seed}",
+            "d": cfg.d, "N": cfg.N, "nrhs": nrhs, "max_rank": max(cfg.ranks),
+            "x_dist": cfg.x_dist, "stands_for": cfg.stands_for,
+            "l2": "no flush: inputs larger than L2 (x %d MiB, intermediates up to %.1f GB)"
+                  % (cfg.N * nrhs * 8 >> 20, max(cfg.ranks[1:-1] or [1]) * cfg.N * nrhs * 8 / 1e9),
+            "parallelism": "replicas"}
+
+
+def oracle_sample(cores, x, cfg, s_bits: int):
+    """Bounded CPU sample of the same workload: Alg. 2 levels 1..d-s on the first
+    of 2^s top-bit blocks of x (these levels never mix blocks)."""
+    import oracle
+    d = cfg.d
+    n = cfg.N >> s_bits
+    sub = cores[: d - s_bits]
+    ranks = cfg.ranks
+    flops = 4 * sum(ranks[k] * ranks[k + 1] for k in range(d - s_bits)) * n
+    t0 = time.perf_counter()
+    oracle.alg2_sweep(sub, x[0, :n])
+    dt = time.perf_counter() - t0
+    return flops, dt
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max((i.get("num_threads", 1) for i in info), default=1), [i.get("internal_api") for i in info]
+    except Exception:
+        return os.cpu_count() or 1, []
+
+
+def run_cpu_baseline(cfg, cores, x, budget_s=20.0):
+    """Time the oracle (as it stands) on a bounded sample; returns a dict."""
+    s_bits = 3
+    flops, dt = oracle_sample(cores, x, cfg, s_bits)
+    # grow the sample toward ~budget_s of CPU work
+    while dt * 2 < budget_s and s_bits > 1:
+        s_bits -= 1
+        flops, dt = oracle_sample(cores, x, cfg, s_bits)
+    threads, apis = blas_threads()
+    return {"value": flops / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"oracle.alg2_sweep (Alg. 2, numpy/BLAS) over levels 1..{cfg.d - s_bits} on 1 of "
+                      f"2^{s_bits} top-bit blocks of x ({flops / 1e9:.1f} GFLOP, {dt:.1f} s)",
+            "seconds": dt, "blas": apis, "host_cpus": os.cpu_count()}
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from qtt_workload import generate
+    cfg, cores, x = generate(args.config)
+    nrhs = cfg.nrhs
+    vals = []
+    cb = None
+    for it in range(args.warmup + args.steps):
+        c = run_cpu_baseline(cfg, cores, x, budget_s=args.ref_budget)
+        if it >= args.warmup:
+            vals.append(c["value"])
+            cb = c
+    v = statistics.median(vals)
+    total_flops = 4 * sum(cfg.ranks[k] * cfg.ranks[k + 1] for k in range(cfg.d)) * cfg.N * nrhs
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_flops / (v * 1e9) * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded; random cores with the config's rank profile)",
+           "config": config_desc(cfg, nrhs),
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
+                            "sample": cb["sample"]},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "note": "ms_per_step extrapolates the sampled rate to one full apply"}
+    print(json.dumps(out))
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=20.0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world, rank, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    import paper_1511_06029_b200 as q
+    from qtt_workload import generate
+
+    cfg, cores, x_np = generate(args.config)
+    nrhs = cfg.nrhs
+    op = q.QttOperator(cores)
+    x = torch.from_numpy(x_np).to(dev)
+    y = torch.empty_like(x)
+    ws = torch.empty(max(op.workspace_size(nrhs), 8) // 8 + 64, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flops_step = op.flops_per_rhs * nrhs
+
+    for _ in range(args.warmup):
+        op.apply(x, out=y, workspace=ws, stream=stream)
+    torch.cuda.synchronize(dev)
+
+    op.set_stage_timing(True)
+    op.stage_times()                      # reset accumulators
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        dist_barrier(world)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            op.apply(x, out=y, workspace=ws, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        dist_barrier(world)
+    op.set_stage_timing(False)
+    ms_local = e0.elapsed_time(e1)
+    stage_ms, n_timed = op.stage_times()
+    ms_total = dist_max(ms_local, world, dev)
+    ms_step = ms_total / args.steps
+    value = flops_step * world * args.steps / (ms_total * 1e-3) / 1e9
+
+    # ---- end-to-end through the public API with host buffers (H2D + apply + D2H)
+    xh = torch.from_numpy(x_np).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    op.apply_host(xh.numpy(), out=yh.numpy())          # warm the staging buffers
+    torch.cuda.synchronize(dev)
+    dist_barrier(world)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.e2e_steps):
+        op.apply_host(xh.numpy(), out=yh.numpy(), stream=stream)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = dist_max(t0.elapsed_time(t1), world, dev) / args.e2e_steps
+    e2e_value = flops_step * world / (e2e_ms * 1e-3) / 1e9
+
+    # ---- per-stage roofline
+    hbm, hbm_src, fp64, fp64_src = load_peaks()
+    P = fp64 * 1e12
+    BW = hbm * 1e9
+    stages = op.stages()
+    r = cfg.ranks
+    N = cfg.N
+    stage_rows = []
+    sum_T, sum_t = 0.0, 0.0
+    for s, st in enumerate(stages):
+        k0, k1 = st["k_first"], st["k_last"]
+        F = sum(4 * r[k - 1] * r[k] for k in range(k0, k1 + 1)) * N * nrhs
+        B = 8 * N * nrhs * (r[k0 - 1] + r[k1]) + 32 * sum(r[k - 1] * r[k] for k in range(k0, k1 + 1))
+        t = stage_ms[s] / max(n_timed, 1) * 1e-3
+        T = max(F / P, B / BW)
+        sum_T += T
+        sum_t += t
+        stage_rows.append({"levels": [k0, k1], "ranks": [r[k0 - 1], r[k1]], "variant": st["variant"],
+                           "ms": t * 1e3, "gflops": F / t / 1e9 if t else None,
+                           "gbs": B / t / 1e9 if t else None, "roofline_frac": T / t if t else None})
+    # dominant kernel: the DMMA instance with the largest share of the step
+    by_kernel = {}
+    for s, row in enumerate(stage_rows):
+        key = (row["variant"], row["ranks"][0], row["ranks"][1])
+        by_kernel.setdefault(key, []).append(row)
+    dom_key = max(by_kernel, key=lambda k: sum(rr["ms"] for rr in by_kernel[k]))
+    dom = by_kernel[dom_key]
+    dom_ms = sum(rr["ms"] for rr in dom) / len(dom)
+    rin, rout = dom_key[1], dom_key[2]
+    dom_flops = 4 * rin * rout * N * nrhs
+    achieved = dom_flops / (dom_ms * 1e-3) / 1e12
+    tr = load_traffic(args.config)
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                "frac": achieved / fp64, "traffic": tr[0] if tr else None,
+                "kernel": f"level_dmma_kernel r_in={rin} r_out={rout} ({dom_key[0]}; {len(dom)} launches/step)",
+                "share_of_step": sum(rr["ms"] for rr in dom) / (ms_step if world == 1 else ms_local / args.steps),
+                "peak_source": fp64_src + "; MEASURED_PEAKS.json has no FP64 figure",
+                "algorithmic_flops_per_launch": dom_flops,
+                "traffic_source": tr[1] if tr else None}
+    per_stage = {"frac": sum_T / sum_t if sum_t else None, "sum_T_ms": sum_T * 1e3, "sum_t_ms": sum_t * 1e3,
+                 "fp64_peak_tflops": fp64, "hbm_gbs": hbm, "hbm_source": hbm_src,
+                 "frac_vs_nominal_fp64": None, "stages": stage_rows}
+    # algorithmic roofline T_alg = max(F/P, (x+y+cores bytes)/BW)
+    alg_bytes = 16 * N * nrhs + 32 * sum(r[k] * r[k + 1] for k in range(cfg.d))
+    T_alg = max(flops_step / P, alg_bytes / BW)
+    per_stage["algorithmic_frac"] = T_alg / (ms_step * 1e-3)
+    per_stage["frac_vs_nominal_fp64"] = sum(
+        max(4 * sum(r[k - 1] * r[k] for k in range(st["levels"][0], st["levels"][1] + 1)) * N * nrhs
+            / (FP64_NOMINAL_TFLOPS * 1e12),
+            (8 * N * nrhs * (r[st["levels"][0] - 1] + r[st["levels"][1]])) / BW)
+        for st in stage_rows) / sum_t if sum_t else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline(cfg, cores, x_np, budget_s=20.0)
+        cpu.pop("seconds", None)
+
+    clocks = clk.summary()
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded; random cores with the config's rank profile stand in for the paper's inverse cores)",
+        "config": config_desc(cfg, nrhs),
+        "gbs": (16 * N * nrhs) / (ms_step * 1e-3) / 1e9,
+        "per_stage_roofline": per_stage,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(x_np.nbytes), "d2h_bytes_per_step": int(x_np.nbytes)},
+        "gpu_launches": op.launches_per_apply * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(out))
+    op.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

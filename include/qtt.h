@@ -1,0 +1,138 @@
+/*
+ * qtt.h -- C ABI of the B200-native QTT apply library (libqtt_b200.so).
+ *
+ * The one operation: y = A x, where A is an N x N matrix (N = 2^d) stored in
+ * Quantized Tensor-Train form and x, y are dense N x nrhs fp64 matrices.
+ *
+ *   Definition (PAPER.md Eq. (TTdeccores), with the product-tree
+ *   tensorization of a matrix):
+ *     A(overline{i_1..i_d}, overline{j_1..j_d})
+ *         = G_1(:, i_1 j_1, :) G_2(:, i_2 j_2, :) ... G_d(:, i_d j_d, :)
+ *   Method (Alg. 2 "QTT matrix by uncompressed vector product",
+ *   P:1441-1532): contract one core per level, k = 1..d, an upward pass that
+ *   costs 4 r_{k-1} r_k N flops per level per right-hand side.
+ *
+ * Conventions (readings R1, R2, R8):
+ *   - cores[k-1] holds G_k as ranks[k-1] * 2 * 2 * ranks[k] doubles, row-major
+ *     [alpha_{k-1}][i_k][j_k][alpha_k]; i_k is the ROW (target/output) digit,
+ *     j_k the COLUMN (source/input) digit.
+ *   - Digits are least-significant first: row index i = sum_k i_k 2^{k-1}
+ *     (core 1 acts on bit 0, the finest level).  Vectors are in
+ *     this hierarchical (Morton) order already.
+ *   - x and y are column-major N x nrhs with leading dimension N.
+ *
+ * Semantics: y = A x up to fp64 rounding (IEEE binary64, FMA contraction,
+ * no reduced precision).  NaN/Inf propagate per IEEE; nothing is checked.
+ * Results are bitwise deterministic for a fixed (handle, nrhs): no atomics,
+ * no split-K.  No exceptions cross this boundary; every entry point returns
+ * a qtt_status_t.
+ */
+#ifndef QTT_B200_H
+#define QTT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Opaque plan: packed cores in device memory + per-level kernel schedule. */
+typedef struct qtt_plan* qtt_handle_t;
+
+/* A CUDA stream; layout-compatible with cudaStream_t / CUstream (NULL = the
+ * legacy default stream).  Declared here so this header needs no CUDA include. */
+typedef struct CUstream_st* qtt_stream_t;
+
+typedef enum {
+  QTT_SUCCESS = 0,
+  QTT_ERROR_INVALID_VALUE = 1,  /* null pointer, bad d / ranks, nrhs < 1, x/y overlap, short workspace */
+  QTT_ERROR_NOT_SUPPORTED = 2,  /* misaligned pointer, host pointer where device memory is required,
+                                   no sm_100 device */
+  QTT_ERROR_OUT_OF_MEMORY = 3,  /* device allocation failed */
+  QTT_ERROR_CUDA = 4            /* a CUDA runtime call or kernel launch failed */
+} qtt_status_t;
+
+/* Human-readable name of a status code (static storage; never NULL). */
+const char* qtt_status_string(qtt_status_t s);
+
+/*
+ * qtt_create -- build a plan from a core list and rank profile.
+ *   out    : receives the handle (set to NULL on failure).
+ *   d      : number of cores, 1 <= d <= 30 (N = 2^d).
+ *   ranks  : host array of d+1 TT ranks; ranks[0] == ranks[d] == 1 and
+ *            1 <= ranks[k] <= 4096 (PAPER P:531-534 dummy bonds r_0 = r_d = 1).
+ *   cores  : host array of d HOST pointers; cores[k-1] points to
+ *            ranks[k-1]*4*ranks[k] doubles in [a][i][j][b] order.
+ * The library COPIES and repacks the cores into device memory it owns (on
+ * the current CUDA device), so the caller may free its arrays on return.
+ * Synchronous.  Plans the per-level kernels (ranks <= 64 run on the FP64
+ * tensor-core path, larger ranks on a generic kernel) and uploads.
+ */
+qtt_status_t qtt_create(qtt_handle_t* out, int d, const int64_t* ranks,
+                        const double* const* cores);
+
+/*
+ * qtt_apply -- y = A x on `stream` (asynchronous, stream-ordered).
+ *   x, y  : DEVICE pointers owned by the caller, column-major N x nrhs,
+ *           16-byte aligned; the ranges [x, x+N*nrhs) and [y, y+N*nrhs)
+ *           must not overlap (in-place is impossible, reading R13).
+ *   nrhs  : number of right-hand sides, >= 1.
+ * Argument errors return synchronously and enqueue nothing.  The handle
+ * keeps a cached workspace of qtt_workspace_size() bytes, allocated on first
+ * use with cudaMallocAsync on `stream`; concurrent applies on one handle
+ * from different streams must use qtt_apply_ws instead.  No host sync.
+ */
+qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
+                       qtt_stream_t stream);
+
+/* Bytes of device workspace one apply with `nrhs` right-hand sides needs
+ * (two ping-pong buffers of max interior rank * N * nrhs doubles; 0 if d==1). */
+qtt_status_t qtt_workspace_size(qtt_handle_t h, int64_t nrhs, size_t* bytes);
+
+/* qtt_apply with caller-owned DEVICE workspace `ws` of `ws_bytes` >= the
+ * qtt_workspace_size(h, nrhs) (256-byte aligned).  Otherwise as qtt_apply. */
+qtt_status_t qtt_apply_ws(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
+                          void* ws, size_t ws_bytes, qtt_stream_t stream);
+
+/*
+ * qtt_apply_host -- end-to-end convenience: x_host, y_host are HOST arrays
+ * (pinned or pageable) of N*nrhs doubles.  Copies x to the device on
+ * `stream`, applies, copies y back, and synchronizes `stream` before
+ * returning.  Device staging buffers are cached in the handle.
+ */
+qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host,
+                            int64_t nrhs, qtt_stream_t stream);
+
+/* Plan facts: d, N, max rank, algorithmic flops per right-hand side
+ * (4 * sum_k r_{k-1} r_k * N) and the number of kernel
+ * launches one apply enqueues.  Any output pointer may be NULL. */
+qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank,
+                          double* flops_per_rhs, int* launches_per_apply);
+
+/*
+ * Per-stage description: stage s covers levels [*k_first, *k_last] (1-based)
+ * and runs kernel variant *variant (0 = generic, 1 = fp64 tensor-core DMMA,
+ * 2 = fused small-rank stage).
+ */
+qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int* variant);
+
+/*
+ * Stage timing (for the bench's roofline): when enabled, each apply records
+ * a CUDA event pair around every stage launch on the apply stream.
+ * qtt_stage_times synchronizes those events, writes the summed milliseconds
+ * per stage into ms[0..n_stages-1] and the number of timed applies into
+ * *n_applies, and resets the accumulators.
+ */
+qtt_status_t qtt_set_stage_timing(qtt_handle_t h, int enable);
+qtt_status_t qtt_stage_times(qtt_handle_t h, float* ms, int n_stages, int* n_applies);
+
+/* Waits for the handle's last apply (event recorded on its stream), then
+ * frees device memory.  NULL is a no-op. */
+qtt_status_t qtt_destroy(qtt_handle_t h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QTT_B200_H */

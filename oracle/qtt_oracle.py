@@ -208,6 +208,18 @@ def compressed_matvec(A_cores, b_cores):
     return out
 
 
+def tt_vector_entries(cores, idx, dtype=np.float64):
+    """Entries v[i] = H_1(:, i_1, :) ... H_d(:, i_d, :) of a TT vector (Eq. TTdeccores)."""
+    idx = np.asarray(idx, dtype=np.int64)
+    out = np.empty(idx.size, dtype=dtype)
+    for t, i in enumerate(idx):
+        v = np.ones((1, 1), dtype=dtype)
+        for k, H in enumerate(cores):
+            v = v @ H[:, (int(i) >> k) & 1, :].astype(dtype)
+        out[t] = v[0, 0]
+    return out
+
+
 def tt_vector_dense(cores, dtype=np.float64):
     """Dense N-vector of a TT vector with cores H_k (r_{k-1}, 2, r_k), LSB-first digits:
     v[overline{i_1..i_d}] = H_1(:, i_1, :) ... H_d(:, i_d, :)."""

@@ -1,0 +1,214 @@
+"""B200-native QTT apply: y = A x for a matrix A in Quantized Tensor-Train form.
+
+Thin Python binding over the C ABI in ``include/qtt.h`` (``libqtt_b200.so``):
+argument marshalling only -- every step of PAPER.md Alg. 2 runs
+in the library's CUDA kernels.  PyTorch provides device memory and streams.
+There is no CPU fallback: without the built library, or without an sm_100
+device, calls raise.
+
+Layout (readings R1, R2, R8): ``cores[k]`` has shape
+``(r_k, 2, 2, r_{k+1})`` = ``[alpha_{k-1}][i_k][j_k][alpha_k]`` with i_k the row
+digit; digits are LSB-first.  A batch of right-hand sides is a tensor of
+shape ``(nrhs, N)`` (row s = RHS s), whose memory image is the column-major
+``N x nrhs`` matrix of the ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import QttError, SYMBOLS
+
+__all__ = [
+    "QttOperator", "QttError", "qtt_create", "qtt_apply", "qtt_apply_ws", "qtt_apply_host",
+    "qtt_workspace_size", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
+    "qtt_stage_times", "qtt_destroy", "qtt_status_string", "library_path", "SYMBOLS",
+]
+
+VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "fused"}
+
+
+def library_path() -> str:
+    return _lib.LIB_PATH
+
+
+def _ptr(t) -> int:
+    return int(t.data_ptr())
+
+
+def _stream_handle(stream) -> int | None:
+    if stream is None:
+        import torch
+        return int(torch.cuda.current_stream().cuda_stream) or None
+    if isinstance(stream, int):
+        return stream or None
+    return int(stream.cuda_stream) or None
+
+
+# ----------------------------------------------------------------- C names
+def qtt_status_string(code: int) -> str:
+    return _lib.load().qtt_status_string(code).decode()
+
+
+def qtt_create(cores, ranks=None) -> int:
+    """cores: list of d float64 arrays (r_{k-1}, 2, 2, r_k). Returns a handle (int)."""
+    lib = _lib.load()
+    d = len(cores)
+    if d < 1:
+        raise ValueError("need at least one core")
+    arrs = [np.ascontiguousarray(np.asarray(G, dtype=np.float64)) for G in cores]
+    if ranks is None:
+        ranks = [arrs[0].shape[0]] + [a.shape[3] for a in arrs]
+    ranks = [int(r) for r in ranks]
+    if len(ranks) != d + 1:
+        raise ValueError("ranks must have d+1 entries")
+    for k, a in enumerate(arrs):
+        if a.shape != (ranks[k], 2, 2, ranks[k + 1]):
+            raise ValueError(f"core {k + 1} has shape {a.shape}, expected {(ranks[k], 2, 2, ranks[k + 1])}")
+    r_arr = (C.c_int64 * (d + 1))(*ranks)
+    p_arr = (C.c_void_p * d)(*[a.ctypes.data for a in arrs])
+    h = C.c_void_p()
+    _lib.check("qtt_create", lib.qtt_create(C.byref(h), d, r_arr, p_arr))
+    return int(h.value)
+
+
+def qtt_apply(h: int, x, y, nrhs: int, stream=None) -> None:
+    _lib.check("qtt_apply", _lib.load().qtt_apply(h, _ptr(x), _ptr(y), int(nrhs), _stream_handle(stream)))
+
+
+def qtt_apply_ws(h: int, x, y, nrhs: int, ws, ws_bytes: int, stream=None) -> None:
+    _lib.check("qtt_apply_ws", _lib.load().qtt_apply_ws(
+        h, _ptr(x), _ptr(y), int(nrhs), _ptr(ws) if ws is not None else None, int(ws_bytes),
+        _stream_handle(stream)))
+
+
+def qtt_apply_host(h: int, x: np.ndarray, y: np.ndarray, nrhs: int, stream=None) -> None:
+    _lib.check("qtt_apply_host", _lib.load().qtt_apply_host(
+        h, x.ctypes.data, y.ctypes.data, int(nrhs), _stream_handle(stream)))
+
+
+def qtt_workspace_size(h: int, nrhs: int) -> int:
+    b = C.c_size_t()
+    _lib.check("qtt_workspace_size", _lib.load().qtt_workspace_size(h, int(nrhs), C.byref(b)))
+    return int(b.value)
+
+
+def qtt_get_info(h: int) -> dict:
+    d, N, mr, fl, nl = C.c_int(), C.c_int64(), C.c_int64(), C.c_double(), C.c_int()
+    _lib.check("qtt_get_info", _lib.load().qtt_get_info(
+        h, C.byref(d), C.byref(N), C.byref(mr), C.byref(fl), C.byref(nl)))
+    return dict(d=d.value, N=N.value, max_rank=mr.value, flops_per_rhs=fl.value, launches_per_apply=nl.value)
+
+
+def qtt_get_stage(h: int, s: int) -> dict:
+    a, b, v = C.c_int(), C.c_int(), C.c_int()
+    _lib.check("qtt_get_stage", _lib.load().qtt_get_stage(h, int(s), C.byref(a), C.byref(b), C.byref(v)))
+    return dict(k_first=a.value, k_last=b.value, variant=VARIANT_NAMES.get(v.value, str(v.value)))
+
+
+def qtt_set_stage_timing(h: int, enable: bool) -> None:
+    _lib.check("qtt_set_stage_timing", _lib.load().qtt_set_stage_timing(h, int(bool(enable))))
+
+
+def qtt_stage_times(h: int, n_stages: int):
+    ms = (C.c_float * n_stages)()
+    n = C.c_int()
+    _lib.check("qtt_stage_times", _lib.load().qtt_stage_times(h, ms, int(n_stages), C.byref(n)))
+    return [float(v) for v in ms], int(n.value)
+
+
+def qtt_destroy(h: int) -> None:
+    _lib.check("qtt_destroy", _lib.load().qtt_destroy(h))
+
+
+# ----------------------------------------------------------------- object API
+class QttOperator:
+    """A QTT matrix resident on the current CUDA device; ``apply`` computes y = A x."""
+
+    def __init__(self, cores, ranks=None):
+        self._h = None
+        self._h = qtt_create(cores, ranks)
+        info = qtt_get_info(self._h)
+        self.d = info["d"]
+        self.N = info["N"]
+        self.max_rank = info["max_rank"]
+        self.flops_per_rhs = info["flops_per_rhs"]
+        self.launches_per_apply = info["launches_per_apply"]
+        self.ranks = [int(np.shape(cores[0])[0])] + [int(np.shape(G)[3]) for G in cores]
+
+    @property
+    def handle(self) -> int:
+        if self._h is None:
+            raise ValueError("operator is closed")
+        return self._h
+
+    def _check_x(self, x):
+        import torch
+        if not isinstance(x, torch.Tensor):
+            raise ValueError("x must be a torch.Tensor on a CUDA device")
+        if x.dtype != torch.float64:
+            raise ValueError(f"x must be float64, got {x.dtype}")
+        if not x.is_cuda:
+            raise ValueError("x must be on a CUDA device")
+        if x.dim() not in (1, 2) or x.shape[-1] != self.N:
+            raise ValueError(f"x must have shape (N,) or (nrhs, N) with N={self.N}, got {tuple(x.shape)}")
+        if not x.is_contiguous():
+            raise ValueError("x must be contiguous")
+        return 1 if x.dim() == 1 else int(x.shape[0])
+
+    def apply(self, x, out=None, stream=None, workspace=None):
+        import torch
+        nrhs = self._check_x(x)
+        if nrhs < 1:
+            raise ValueError("nrhs must be >= 1")
+        y = torch.empty_like(x) if out is None else out
+        if out is not None:
+            if out.shape != x.shape or out.dtype != torch.float64 or not out.is_contiguous() or not out.is_cuda:
+                raise ValueError("out must be a contiguous float64 CUDA tensor shaped like x")
+        if workspace is None:
+            qtt_apply(self.handle, x, y, nrhs, stream)
+        else:
+            qtt_apply_ws(self.handle, x, y, nrhs, workspace, workspace.numel() * workspace.element_size(), stream)
+        return y
+
+    __matmul__ = apply
+
+    def apply_host(self, x: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
+        x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+        if x.ndim not in (1, 2) or x.shape[-1] != self.N:
+            raise ValueError(f"x must have shape (N,) or (nrhs, N) with N={self.N}")
+        nrhs = 1 if x.ndim == 1 else x.shape[0]
+        y = np.empty_like(x) if out is None else out
+        qtt_apply_host(self.handle, x, y, nrhs, stream)
+        return y
+
+    def workspace_size(self, nrhs: int = 1) -> int:
+        return qtt_workspace_size(self.handle, nrhs)
+
+    def stages(self):
+        return [qtt_get_stage(self.handle, s) for s in range(self.launches_per_apply)]
+
+    def set_stage_timing(self, enable: bool = True):
+        qtt_set_stage_timing(self.handle, enable)
+
+    def stage_times(self):
+        return qtt_stage_times(self.handle, self.launches_per_apply)
+
+    def close(self):
+        if self._h is not None:
+            h, self._h = self._h, None
+            qtt_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -1,0 +1,78 @@
+"""ctypes declarations for include/qtt.h (argument marshalling only).
+
+Loads the in-tree ``libqtt_b200.so``; there is no fallback -- if the library
+is missing or fails to load, import raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqtt_b200.so")
+
+QTT_SUCCESS = 0
+QTT_ERROR_INVALID_VALUE = 1
+QTT_ERROR_NOT_SUPPORTED = 2
+QTT_ERROR_OUT_OF_MEMORY = 3
+QTT_ERROR_CUDA = 4
+
+# every symbol include/qtt.h declares
+SYMBOLS = (
+    "qtt_status_string", "qtt_create", "qtt_apply", "qtt_workspace_size", "qtt_apply_ws",
+    "qtt_apply_host", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
+    "qtt_stage_times", "qtt_destroy",
+)
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_1511_06029_b200.build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    h = C.c_void_p
+    st = C.c_int
+    i64 = C.c_int64
+    dp = C.c_void_p
+    lib.qtt_status_string.restype = C.c_char_p
+    lib.qtt_status_string.argtypes = [st]
+    lib.qtt_create.restype = st
+    lib.qtt_create.argtypes = [C.POINTER(h), C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p)]
+    lib.qtt_apply.restype = st
+    lib.qtt_apply.argtypes = [h, dp, dp, i64, C.c_void_p]
+    lib.qtt_workspace_size.restype = st
+    lib.qtt_workspace_size.argtypes = [h, i64, C.POINTER(C.c_size_t)]
+    lib.qtt_apply_ws.restype = st
+    lib.qtt_apply_ws.argtypes = [h, dp, dp, i64, dp, C.c_size_t, C.c_void_p]
+    lib.qtt_apply_host.restype = st
+    lib.qtt_apply_host.argtypes = [h, dp, dp, i64, C.c_void_p]
+    lib.qtt_get_info.restype = st
+    lib.qtt_get_info.argtypes = [h, C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(i64),
+                                 C.POINTER(C.c_double), C.POINTER(C.c_int)]
+    lib.qtt_get_stage.restype = st
+    lib.qtt_get_stage.argtypes = [h, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    lib.qtt_set_stage_timing.restype = st
+    lib.qtt_set_stage_timing.argtypes = [h, C.c_int]
+    lib.qtt_stage_times.restype = st
+    lib.qtt_stage_times.argtypes = [h, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]
+    lib.qtt_destroy.restype = st
+    lib.qtt_destroy.argtypes = [h]
+    _lib = lib
+    return lib
+
+
+class QttError(RuntimeError):
+    def __init__(self, fn, code):
+        self.code = code
+        name = load().qtt_status_string(code).decode()
+        super().__init__(f"{fn} failed: {name} ({code})")
+
+
+def check(fn, code):
+    if code != QTT_SUCCESS:
+        raise QttError(fn, code)

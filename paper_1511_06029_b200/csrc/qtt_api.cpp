@@ -1,0 +1,468 @@
+// C ABI of libqtt_b200.so (declared and documented in include/qtt.h).
+//
+// Host side of the QTT apply: argument validation, core packing,
+// the per-level stage plan (B4), workspace management and launches.  The
+// arithmetic of PAPER.md Alg. 2 runs entirely in the kernels
+// (qtt_level_dmma.cu); nothing here touches vector data.
+#include "../../include/qtt.h"
+#include "qtt_internal.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <vector>
+
+namespace {
+
+using qtt::LevelArgs;
+
+struct Level {
+  int r_in = 0, r_out = 0;
+  int variant = qtt::kGeneric;
+  int KB = 0, NB = 0, RP = 0, rep = 1, stages = 2, ctas_per_sm = 1;
+  size_t smem = 0;
+  double* d_bpack = nullptr;   // DMMA fragment-packed core
+  double* d_core = nullptr;    // raw core (generic kernel)
+};
+
+struct StageEvents {
+  cudaEvent_t start, stop;
+  int stage;
+};
+
+}  // namespace
+
+struct qtt_plan {
+  int device = 0;
+  int num_sms = 0;
+  size_t smem_optin = 0;
+  int d = 0;
+  int64_t N = 0;
+  std::vector<int64_t> ranks;
+  std::vector<Level> levels;
+  int64_t max_interior_rank = 0;
+  // cached workspace (qtt_apply)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaStream_t ws_stream = nullptr;
+  // cached staging buffers (qtt_apply_host)
+  double* hx = nullptr;
+  double* hy = nullptr;
+  size_t h_elems = 0;
+  cudaEvent_t last = nullptr;
+  bool timing = false;
+  std::vector<StageEvents> pending;
+  std::vector<double> stage_ms;
+  int timed_applies = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+qtt_status_t from_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return QTT_SUCCESS;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return QTT_ERROR_OUT_OF_MEMORY;
+  }
+  return QTT_ERROR_CUDA;
+}
+
+// B operand of level k in MMA-fragment order (see qtt_level_dmma.cu):
+//   Bmat[kk][n], kk = j*r_in + a (the column-merged index of Alg. 2 line 6),
+//   n = i*RP + b (the row-separated output, Alg. 2 line 8), value G[a,i,j,b];
+//   pack[kb][nb][lane][v] = Bmat[kb*16 + 4*(lane%4) + v][nb*8 + lane/4].
+std::vector<double> pack_dmma(const double* G, int r_in, int r_out, int KB, int NB, int RP) {
+  std::vector<double> out(size_t(KB) * NB * 32 * 4, 0.0);
+  const int K = 2 * r_in;
+  for (int kb = 0; kb < KB; ++kb)
+    for (int nb = 0; nb < NB; ++nb)
+      for (int lane = 0; lane < 32; ++lane)
+        for (int v = 0; v < 4; ++v) {
+          const int kk = kb * 16 + 4 * (lane % 4) + v;
+          const int n = nb * 8 + lane / 4;
+          double val = 0.0;
+          if (kk < K) {
+            const int j = kk / r_in, a = kk % r_in;
+            const int i = n / RP, b = n % RP;
+            if (i < 2 && b < r_out) val = G[((size_t(a) * 2 + i) * 2 + j) * r_out + b];
+          }
+          out[((size_t(kb) * NB + nb) * 32 + lane) * 4 + v] = val;
+        }
+  return out;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs) {
+  if (h->d <= 1) return 0;
+  const size_t one = size_t(h->max_interior_rank) * size_t(h->N) * size_t(nrhs) * sizeof(double);
+  const size_t aligned = (one + 255) / 256 * 256;
+  return 2 * aligned;
+}
+
+void free_plan(qtt_plan* h) {
+  for (auto& L : h->levels) {
+    if (L.d_bpack) cudaFree(L.d_bpack);
+    if (L.d_core) cudaFree(L.d_core);
+  }
+  if (h->ws) cudaFree(h->ws);
+  if (h->hx) cudaFree(h->hx);
+  if (h->hy) cudaFree(h->hy);
+  for (auto& e : h->pending) {
+    cudaEventDestroy(e.start);
+    cudaEventDestroy(e.stop);
+  }
+  if (h->last) cudaEventDestroy(h->last);
+  delete h;
+}
+
+qtt_status_t plan_level(qtt_plan* h, Level& L, const double* G) {
+  const int r_in = L.r_in, r_out = L.r_out;
+  const size_t core_elems = size_t(r_in) * 4 * r_out;
+  cudaError_t e = cudaMalloc(&L.d_core, core_elems * sizeof(double));
+  if (e != cudaSuccess) return from_cuda(e);
+  e = cudaMemcpy(L.d_core, G, core_elems * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return from_cuda(e);
+
+  const int K = 2 * r_in;
+  const int RP = (r_out + 1) / 2 * 2;
+  const int KB = (K + 15) / 16;
+  const int NB = (2 * RP + 7) / 8;
+  L.RP = RP;
+  if (KB > qtt::kMaxKB || NB > qtt::kMaxNB) {
+    L.variant = qtt::kGeneric;
+    return QTT_SUCCESS;
+  }
+  // TMA stage: >= 16 KiB per stage (HBM bytes in flight), <= 64 KiB.
+  const size_t sub_bytes = size_t(qtt::kDmmaRowsPerSubtile) * K * 8;
+  int rep = int(std::max<size_t>(1, (16384 + sub_bytes - 1) / sub_bytes));
+  while (rep > 1 && sub_bytes * rep > 65536) --rep;
+  int stages = qtt::kMaxStages;
+  size_t smem = 0;
+  for (; stages >= 2; --stages) {
+    smem = qtt::dmma_smem_bytes(KB, NB, K, rep, stages);
+    if (smem <= h->smem_optin) break;
+  }
+  if (stages < 2) {
+    L.variant = qtt::kGeneric;
+    return QTT_SUCCESS;
+  }
+  // Prefer 4 stages + 2 CTAs/SM when small stages allow it.
+  e = qtt::dmma_prepare(KB, NB, smem);
+  if (e != cudaSuccess) return from_cuda(e);
+  int occ = 0;
+  e = qtt::dmma_occupancy(KB, NB, smem, &occ);
+  if (e != cudaSuccess) return from_cuda(e);
+  L.variant = qtt::kDmma;
+  L.KB = KB;
+  L.NB = NB;
+  L.rep = rep;
+  L.stages = stages;
+  L.smem = smem;
+  L.ctas_per_sm = std::max(1, occ);
+  std::vector<double> pk = pack_dmma(G, r_in, r_out, KB, NB, RP);
+  e = cudaMalloc(&L.d_bpack, pk.size() * sizeof(double));
+  if (e != cudaSuccess) return from_cuda(e);
+  e = cudaMemcpy(L.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice);
+  return from_cuda(e);
+}
+
+qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st) {
+  const int64_t half = h->N / 2;
+  const size_t buf_elems = ws ? (ws_bytes_for(h, nrhs) / 2) / sizeof(double) : 0;
+  double* buf[2] = {static_cast<double*>(ws), ws ? static_cast<double*>(ws) + buf_elems : nullptr};
+  const double* in = x;
+  for (int k = 0; k < h->d; ++k) {
+    const Level& L = h->levels[k];
+    double* out = (k == h->d - 1) ? y : buf[k & 1];
+    LevelArgs a;
+    a.in = in;
+    a.out = out;
+    a.bpack = L.d_bpack;
+    a.core = L.d_core;
+    a.M = nrhs * half;
+    a.half = half;
+    a.r_in = L.r_in;
+    a.r_out = L.r_out;
+    a.RP = L.RP;
+    a.K = 2 * L.r_in;
+    a.KB = L.KB;
+    a.NB = L.NB;
+    a.rep = L.rep;
+    a.stages = L.stages;
+    a.smem = L.smem;
+    StageEvents ev{};
+    if (h->timing) {
+      ev.stage = k;
+      if (cudaEventCreate(&ev.start) != cudaSuccess || cudaEventCreate(&ev.stop) != cudaSuccess)
+        return QTT_ERROR_CUDA;
+      cudaEventRecord(ev.start, st);
+    }
+    cudaError_t e;
+    if (L.variant == qtt::kDmma) {
+      const int64_t rows_per_stage = int64_t(qtt::kDmmaRowsPerSubtile) * L.rep;
+      const int64_t tiles = (a.M + rows_per_stage - 1) / rows_per_stage;
+      a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms) * L.ctas_per_sm));
+      e = qtt::launch_level_dmma(a, st);
+    } else {
+      e = qtt::launch_level_generic(a, st, h->num_sms);
+    }
+    if (e != cudaSuccess) return from_cuda(e);
+    if (h->timing) {
+      cudaEventRecord(ev.stop, st);
+      h->pending.push_back(ev);
+    }
+    in = out;
+  }
+  if (h->timing) h->timed_applies++;
+  cudaEventRecord(h->last, st);
+  return QTT_SUCCESS;
+}
+
+qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs) {
+  if (!h || !x || !y || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  if (nrhs > (int64_t(1) << 40) / h->N) return QTT_ERROR_INVALID_VALUE;
+  const uintptr_t xs = reinterpret_cast<uintptr_t>(x), ys = reinterpret_cast<uintptr_t>(y);
+  const uintptr_t bytes = uintptr_t(h->N) * uintptr_t(nrhs) * sizeof(double);
+  if (xs < ys + bytes && ys < xs + bytes) return QTT_ERROR_INVALID_VALUE;
+  if ((xs % 16) || (ys % 16)) return QTT_ERROR_NOT_SUPPORTED;
+  if (!is_device_ptr(x) || !is_device_ptr(y)) return QTT_ERROR_NOT_SUPPORTED;
+  return QTT_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* qtt_status_string(qtt_status_t s) {
+  switch (s) {
+    case QTT_SUCCESS: return "QTT_SUCCESS";
+    case QTT_ERROR_INVALID_VALUE: return "QTT_ERROR_INVALID_VALUE";
+    case QTT_ERROR_NOT_SUPPORTED: return "QTT_ERROR_NOT_SUPPORTED";
+    case QTT_ERROR_OUT_OF_MEMORY: return "QTT_ERROR_OUT_OF_MEMORY";
+    case QTT_ERROR_CUDA: return "QTT_ERROR_CUDA";
+  }
+  return "QTT_ERROR_UNKNOWN";
+}
+
+qtt_status_t qtt_create(qtt_handle_t* out, int d, const int64_t* ranks, const double* const* cores) {
+  if (!out) return QTT_ERROR_INVALID_VALUE;
+  *out = nullptr;
+  if (d < 1 || d > 30 || !ranks || !cores) return QTT_ERROR_INVALID_VALUE;
+  if (ranks[0] != 1 || ranks[d] != 1) return QTT_ERROR_INVALID_VALUE;
+  for (int k = 0; k <= d; ++k)
+    if (ranks[k] < 1 || ranks[k] > 4096) return QTT_ERROR_INVALID_VALUE;
+  for (int k = 0; k < d; ++k)
+    if (!cores[k]) return QTT_ERROR_INVALID_VALUE;
+  qtt_plan* h = nullptr;
+  try {
+    h = new qtt_plan();
+  } catch (const std::bad_alloc&) {
+    return QTT_ERROR_OUT_OF_MEMORY;
+  }
+  if (cudaGetDevice(&h->device) != cudaSuccess) {
+    cudaGetLastError();
+    delete h;
+    return QTT_ERROR_NOT_SUPPORTED;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, h->device) != cudaSuccess) {
+    delete h;
+    return QTT_ERROR_CUDA;
+  }
+  if (prop.major != 10 || prop.minor != 0) {
+    delete h;
+    return QTT_ERROR_NOT_SUPPORTED;   // built for sm_100a only
+  }
+  h->num_sms = prop.multiProcessorCount;
+  h->smem_optin = prop.sharedMemPerBlockOptin;
+  h->d = d;
+  h->N = int64_t(1) << d;
+  h->ranks.assign(ranks, ranks + d + 1);
+  for (int k = 1; k < d; ++k) h->max_interior_rank = std::max<int64_t>(h->max_interior_rank, ranks[k]);
+  qtt_status_t st = QTT_SUCCESS;
+  try {
+    h->levels.resize(d);
+    for (int k = 0; k < d && st == QTT_SUCCESS; ++k) {
+      h->levels[k].r_in = int(ranks[k]);
+      h->levels[k].r_out = int(ranks[k + 1]);
+      st = plan_level(h, h->levels[k], cores[k]);
+    }
+  } catch (const std::bad_alloc&) {
+    st = QTT_ERROR_OUT_OF_MEMORY;
+  }
+  if (st == QTT_SUCCESS && cudaEventCreateWithFlags(&h->last, cudaEventDisableTiming) != cudaSuccess)
+    st = QTT_ERROR_CUDA;
+  if (st == QTT_SUCCESS && cudaDeviceSynchronize() != cudaSuccess) st = QTT_ERROR_CUDA;
+  if (st != QTT_SUCCESS) {
+    free_plan(h);
+    return st;
+  }
+  h->stage_ms.assign(d, 0.0);
+  *out = h;
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_workspace_size(qtt_handle_t h, int64_t nrhs, size_t* bytes) {
+  if (!h || !bytes || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  *bytes = ws_bytes_for(h, nrhs);
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_apply_ws(qtt_handle_t h, const double* x, double* y, int64_t nrhs, void* ws,
+                          size_t ws_bytes, qtt_stream_t stream) {
+  qtt_status_t s = check_apply_args(h, x, y, nrhs);
+  if (s != QTT_SUCCESS) return s;
+  const size_t need = ws_bytes_for(h, nrhs);
+  if (need > 0) {
+    if (!ws || ws_bytes < need) return QTT_ERROR_INVALID_VALUE;
+    if (reinterpret_cast<uintptr_t>(ws) % 256) return QTT_ERROR_NOT_SUPPORTED;
+    if (!is_device_ptr(ws)) return QTT_ERROR_NOT_SUPPORTED;
+  }
+  try {
+    DeviceGuard g(h->device);
+    return enqueue(h, x, y, nrhs, need ? ws : nullptr, reinterpret_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs, qtt_stream_t stream) {
+  qtt_status_t s = check_apply_args(h, x, y, nrhs);
+  if (s != QTT_SUCCESS) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  try {
+    DeviceGuard g(h->device);
+    const size_t need = ws_bytes_for(h, nrhs);
+    if (need > h->ws_bytes) {
+      if (h->ws) {
+        // the old buffer may still be in use by work on its stream
+        cudaFreeAsync(h->ws, h->ws_stream);
+        h->ws = nullptr;
+        h->ws_bytes = 0;
+      }
+      cudaError_t e = cudaMallocAsync(&h->ws, need, st);
+      if (e != cudaSuccess) {
+        h->ws = nullptr;
+        return from_cuda(e);
+      }
+      h->ws_bytes = need;
+      h->ws_stream = st;
+    }
+    return enqueue(h, x, y, nrhs, need ? h->ws : nullptr, st);
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host, int64_t nrhs,
+                            qtt_stream_t stream) {
+  if (!h || !x_host || !y_host || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  try {
+    DeviceGuard g(h->device);
+    const size_t elems = size_t(h->N) * size_t(nrhs);
+    if (elems > h->h_elems) {
+      if (h->hx) cudaFree(h->hx);
+      if (h->hy) cudaFree(h->hy);
+      h->hx = h->hy = nullptr;
+      h->h_elems = 0;
+      cudaError_t e = cudaMalloc(&h->hx, elems * sizeof(double));
+      if (e == cudaSuccess) e = cudaMalloc(&h->hy, elems * sizeof(double));
+      if (e != cudaSuccess) return from_cuda(e);
+      h->h_elems = elems;
+    }
+    cudaError_t e = cudaMemcpyAsync(h->hx, x_host, elems * sizeof(double), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return from_cuda(e);
+    qtt_status_t s = qtt_apply(h, h->hx, h->hy, nrhs, stream);
+    if (s != QTT_SUCCESS) return s;
+    e = cudaMemcpyAsync(y_host, h->hy, elems * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return from_cuda(e);
+    return from_cuda(cudaStreamSynchronize(st));
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank, double* flops_per_rhs,
+                          int* launches_per_apply) {
+  if (!h) return QTT_ERROR_INVALID_VALUE;
+  if (d) *d = h->d;
+  if (N) *N = h->N;
+  if (max_rank) *max_rank = *std::max_element(h->ranks.begin(), h->ranks.end());
+  if (flops_per_rhs) {
+    double s = 0;
+    for (int k = 0; k < h->d; ++k) s += double(h->ranks[k]) * double(h->ranks[k + 1]);
+    *flops_per_rhs = 4.0 * s * double(h->N);
+  }
+  if (launches_per_apply) *launches_per_apply = h->d;
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int* variant) {
+  if (!h || s < 0 || s >= h->d) return QTT_ERROR_INVALID_VALUE;
+  if (k_first) *k_first = s + 1;
+  if (k_last) *k_last = s + 1;
+  if (variant) *variant = h->levels[s].variant;
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_set_stage_timing(qtt_handle_t h, int enable) {
+  if (!h) return QTT_ERROR_INVALID_VALUE;
+  h->timing = enable != 0;
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_stage_times(qtt_handle_t h, float* ms, int n_stages, int* n_applies) {
+  if (!h) return QTT_ERROR_INVALID_VALUE;
+  DeviceGuard g(h->device);
+  qtt_status_t st = QTT_SUCCESS;
+  for (auto& e : h->pending) {
+    float t = 0;
+    if (cudaEventSynchronize(e.stop) != cudaSuccess || cudaEventElapsedTime(&t, e.start, e.stop) != cudaSuccess)
+      st = QTT_ERROR_CUDA;
+    h->stage_ms[e.stage] += t;
+    cudaEventDestroy(e.start);
+    cudaEventDestroy(e.stop);
+  }
+  h->pending.clear();
+  if (ms)
+    for (int s = 0; s < n_stages && s < h->d; ++s) ms[s] = float(h->stage_ms[s]);
+  if (n_applies) *n_applies = h->timed_applies;
+  std::fill(h->stage_ms.begin(), h->stage_ms.end(), 0.0);
+  h->timed_applies = 0;
+  return st;
+}
+
+qtt_status_t qtt_destroy(qtt_handle_t h) {
+  if (!h) return QTT_SUCCESS;
+  DeviceGuard g(h->device);
+  if (h->last) cudaEventSynchronize(h->last);
+  if (h->ws && h->ws_stream) cudaStreamSynchronize(h->ws_stream);
+  free_plan(h);
+  return QTT_SUCCESS;
+}
+
+}  // extern "C"

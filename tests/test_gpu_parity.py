@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star; reading R11): relative l2
+<= 1e-12 per RHS column and elementwise relative error with an RMS floor
+<= 1e-10; closed forms (identity, shift) bitwise.  Inputs come only from
+``qtt_workload``; expected values only from ``oracle`` or library routines.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from qtt_workload import closed_forms as CF
+from qtt_workload import generate, random_case
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def qtt():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    import paper_1511_06029_b200 as q
+    q._lib.load()
+    return q
+
+
+def gpu_apply(q, cores, x, **kw):
+    op = q.QttOperator(cores)
+    try:
+        xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        y = op.apply(xt, **kw)
+        torch.cuda.synchronize()
+        return y.cpu().numpy(), op.stages()
+    finally:
+        op.close()
+
+
+# ------------------------------------------------------------------ closed forms
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 12, 20])
+def test_identity_bitwise(qtt, d):
+    x = np.random.default_rng(d).standard_normal((2, 1 << d))
+    y, _ = gpu_apply(qtt, CF.identity_cores(d), x)
+    np.testing.assert_array_equal(y, x)
+
+
+@pytest.mark.parametrize("d,s", [(1, 1), (2, 3), (6, 1), (13, 1), (13, 4097), (21, 12345)])
+def test_shift_bitwise(qtt, d, s):
+    x = np.random.default_rng(s).standard_normal((1, 1 << d))
+    y, _ = gpu_apply(qtt, CF.shift_cores(d, s), x)
+    np.testing.assert_array_equal(y[0], np.roll(x[0], s))
+
+
+def test_transposed_shift_bitwise(qtt):
+    d = 16
+    x = np.random.default_rng(0).standard_normal((1, 1 << d))
+    y, _ = gpu_apply(qtt, oracle.transpose(CF.shift_cores(d, 1)), x)
+    np.testing.assert_array_equal(y[0], np.roll(x[0], -1))
+
+
+def test_kronecker_np_kron(qtt):
+    d = 11
+    rng = np.random.default_rng(3)
+    F = [rng.standard_normal((2, 2)) for _ in range(d)]
+    A = np.ones((1, 1))
+    for Fk in F:
+        A = np.kron(Fk, A)
+    x = rng.standard_normal((2, 1 << d))
+    y, _ = gpu_apply(qtt, CF.kron_cores(F), x)
+    oracle.assert_close(y, x @ A.T)
+
+
+# ------------------------------------------------------------------ random profiles
+RANDOM_CASES = [
+    # seed, d, max_rank, nrhs  (odd / non-multiple-of-8 ranks, ragged tails, tiny N)
+    (1, 1, 1, 1), (2, 2, 2, 5), (3, 3, 4, 37), (4, 6, 7, 3), (5, 9, 13, 2), (6, 10, 24, 1),
+    (7, 12, 33, 1), (8, 13, 48, 2), (9, 14, 5, 4), (10, 16, 17, 1), (11, 17, 31, 1), (12, 18, 3, 2),
+    (13, 11, 64, 1), (14, 9, 100, 1),
+]
+
+
+@pytest.mark.parametrize("seed,d,maxr,nrhs", RANDOM_CASES)
+def test_random_profiles(qtt, seed, d, maxr, nrhs):
+    ranks, cores, x = random_case(seed, d, maxr, nrhs)
+    y, _ = gpu_apply(qtt, cores, x)
+    ref = oracle.apply_alg2(cores, x)
+    oracle.assert_close(y, ref)
+
+
+@pytest.mark.parametrize("r", [1, 2, 3, 8, 9, 16, 23, 32, 47, 48])
+def test_constant_rank_sweep(qtt, r):
+    ranks = [1] + [r] * 9 + [1]
+    _, cores, x = random_case(100 + r, 10, r, 2, ranks=ranks)
+    y, stages = gpu_apply(qtt, cores, x)
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
+    assert all(s["variant"] != "generic" for s in stages), stages
+
+
+def test_generic_path_large_rank(qtt):
+    ranks = [1, 2, 4, 70, 70, 4, 2, 1]
+    _, cores, x = random_case(77, 7, 70, 1, ranks=ranks)
+    y, stages = gpu_apply(qtt, cores, x)
+    assert any(s["variant"] == "generic" for s in stages)
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
+
+
+# ------------------------------------------------------------------ BASELINE configs
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_config_full_vector(qtt, name):
+    cfg, cores, x = generate(name)
+    y, _ = gpu_apply(qtt, cores, x)
+    ref = oracle.apply_alg2(cores, x)
+    oracle.assert_close(y, ref)
+    if name == "c1":
+        oracle.assert_close(y, oracle.apply_dense(cores, x))
+
+
+def test_c3x16_columns(qtt):
+    cfg, cores, x = generate("c3x16")
+    y, _ = gpu_apply(qtt, cores, x)
+    # column 0 bitwise equal to the single-RHS run (deterministic, batch-invariant)
+    _, cores1, x1 = generate("c3")
+    y1, _ = gpu_apply(qtt, cores1, x1)
+    np.testing.assert_array_equal(y[0], y1[0])
+    for s in (0, 7, 15):
+        oracle.assert_close(y[s:s + 1], oracle.apply_alg2(cores, x[s:s + 1]))
+
+
+def _sampled_rows(N, n, seed):
+    rng = np.random.default_rng(seed)
+    rows = set(rng.integers(0, N, n).tolist()) | {0, 1, N // 2, N - 1}
+    return np.array(sorted(rows))
+
+
+@pytest.mark.parametrize("name,nrows", [("c4", 24), ("c5", 6)])
+def test_full_size_sampled_rows(qtt, name, nrows):
+    """Full BASELINE size, same launch configuration as bench.py; the oracle
+    computes sampled outputs one by one (apply_rows)."""
+    cfg, cores, x = generate(name)
+    y, _ = gpu_apply(qtt, cores, x)
+    assert np.all(np.isfinite(y))
+    rows = _sampled_rows(cfg.N, nrows, 1)
+    ref = oracle.apply_rows(cores, x, rows)
+    rms = float(np.sqrt(np.mean(ref[0] ** 2)))
+    oracle.assert_close(y[:, rows], ref, rms=rms, check_l2=False)
+    m = oracle.compare(y[:, rows], ref, rms=rms)[0]
+    assert m["rel_l2"] <= 1e-12, m
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_full_size_kronecker_vector(qtt, name):
+    """x = v_d (x) ... (x) v_1: y = A x has exact TT cores from the compressed
+    matvec; its entries are checked at sampled positions."""
+    cfg, cores, _ = generate(name, with_x=False)
+    rng = np.random.default_rng(5)
+    vs = [rng.uniform(0.5, 1.5, 2) * rng.choice([-1, 1], 2) for _ in range(cfg.d)]
+    xk = oracle.tt_vector_dense(oracle.kron_vector_cores(vs))[None, :]
+    y, _ = gpu_apply(qtt, cores, xk)
+    yc_cores = oracle.compressed_matvec(cores, oracle.kron_vector_cores(vs))
+    rows = _sampled_rows(cfg.N, 2000, 2)
+    ref = oracle.tt_vector_entries(yc_cores, rows)[None, :]
+    rms = float(np.sqrt(np.mean(ref ** 2)))
+    oracle.assert_close(y[:, rows], ref, rms=rms)
+
+
+# ------------------------------------------------------------------ determinism, streams, ABI
+def test_determinism_and_stream(qtt):
+    _, cores, x = generate("c2")
+    op = qtt.QttOperator(cores)
+    xt = torch.from_numpy(x).cuda()
+    y1 = op.apply(xt)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        y2 = op.apply(xt, stream=s)
+    s.synchronize()
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    # caller-owned workspace
+    ws = torch.empty(op.workspace_size(1) // 8 + 32, dtype=torch.float64, device="cuda")
+    y3 = op.apply(xt, workspace=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y3)
+    # host end-to-end entry point
+    yh = op.apply_host(x)
+    np.testing.assert_array_equal(yh, y1.cpu().numpy())
+    op.close()
+
+
+def test_abi_errors(qtt):
+    lib = qtt._lib.load()
+    import ctypes as C
+    _, cores, x = generate("c1")
+    op = qtt.QttOperator(cores)
+    h = op.handle
+    N = op.N
+    xt = torch.from_numpy(x).cuda()
+    big = torch.zeros(2 * N + 2, dtype=torch.float64, device="cuda")
+    yt = torch.empty_like(xt)
+    E = qtt._lib
+    # nrhs < 1
+    assert lib.qtt_apply(h, xt.data_ptr(), yt.data_ptr(), 0, None) == E.QTT_ERROR_INVALID_VALUE
+    # overlap
+    assert lib.qtt_apply(h, big.data_ptr(), big.data_ptr() + 8 * 8, 1, None) == E.QTT_ERROR_INVALID_VALUE
+    # misaligned (8-byte offset)
+    assert lib.qtt_apply(h, big.data_ptr() + 8, yt.data_ptr(), 1, None) == E.QTT_ERROR_NOT_SUPPORTED
+    # host pointer
+    assert lib.qtt_apply(h, x.ctypes.data, yt.data_ptr(), 1, None) == E.QTT_ERROR_NOT_SUPPORTED
+    # null
+    assert lib.qtt_apply(h, None, yt.data_ptr(), 1, None) == E.QTT_ERROR_INVALID_VALUE
+    # short workspace
+    ws = torch.empty(16, dtype=torch.float64, device="cuda")
+    assert lib.qtt_apply_ws(h, xt.data_ptr(), yt.data_ptr(), 1, ws.data_ptr(), 128, None) == E.QTT_ERROR_INVALID_VALUE
+    # python-side validation
+    with pytest.raises(ValueError):
+        op.apply(xt.float())
+    with pytest.raises(ValueError):
+        op.apply(torch.zeros(N + 1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        op.apply(torch.zeros(N, dtype=torch.float64))
+    # bad ranks at create
+    with pytest.raises(qtt.QttError):
+        qtt.qtt_create([np.zeros((2, 2, 2, 1))], ranks=[2, 1])
+    op.close()
+    assert lib.qtt_destroy(None) == E.QTT_SUCCESS
+
+
+def test_nan_inf_propagate(qtt):
+    d = 8
+    _, cores, x = random_case(9, d, 6)
+    x = x.copy()
+    x[0, 5] = np.nan
+    y, _ = gpu_apply(qtt, cores, x)
+    ref = oracle.apply_alg2(cores, x)
+    np.testing.assert_array_equal(np.isnan(y), np.isnan(ref))

@@ -179,8 +179,12 @@ def test_kron_vector_compressed_path(d, maxr):
     for v in vs:
         ref_x = np.kron(v, ref_x)
     np.testing.assert_allclose(xk, ref_x, rtol=1e-14)
-    yc = oracle.tt_vector_dense(oracle.compressed_matvec(cores, oracle.kron_vector_cores(vs)))
+    cc = oracle.compressed_matvec(cores, oracle.kron_vector_cores(vs))
+    yc = oracle.tt_vector_dense(cc)
     oracle.assert_close(oracle.apply_alg2(cores, xk), yc[None, :], l2_tol=1e-13)
+    idx = rng.integers(0, 1 << d, 20)
+    np.testing.assert_allclose(oracle.tt_vector_entries(cc, idx), yc[idx], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(oracle.tt_vector_entries(oracle.kron_vector_cores(vs), idx), ref_x[idx], rtol=1e-14)
 
 
 # --- c1: oracle against the dense 4096 x 4096 matvec (BASELINE.json configs[0]) ---
