@@ -169,8 +169,9 @@ qtt_status_t plan_level(qtt_plan* h, Level& L, const double* G) {
     L.variant = qtt::kGeneric;
     return QTT_SUCCESS;
   }
-  // Prefer 4 stages + 2 CTAs/SM when small stages allow it.
-  e = qtt::dmma_prepare(KB, NB, smem);
+  // The attribute is per kernel instance and shared by every level (and plan)
+  // that uses it, so raise it to the device maximum rather than this level's need.
+  e = qtt::dmma_prepare(KB, NB, h->smem_optin);
   if (e != cudaSuccess) return from_cuda(e);
   int occ = 0;
   e = qtt::dmma_occupancy(KB, NB, smem, &occ);

@@ -14,8 +14,8 @@ enum Variant : int { kGeneric = 0, kDmma = 1, kFused = 2 };
 // 2 * roundup(r_out, 2) <= 8*kMaxNB.
 constexpr int kMaxKB = 6;
 constexpr int kMaxNB = 12;
-constexpr int kDmmaConsumerWarps = 4;            // 16 rows each -> 64-row sub-tile
-constexpr int kDmmaRowsPerSubtile = 16 * kDmmaConsumerWarps;
+constexpr int kDmmaConsumerWarps = 8;            // 4 row groups (16 rows) x 2 column groups
+constexpr int kDmmaRowsPerSubtile = 64;
 constexpr int kMaxStages = 8;
 
 // One level (= one core, PAPER Alg. 2 lines 5-8) as a GEMM over the rotating

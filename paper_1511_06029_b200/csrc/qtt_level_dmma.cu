@@ -62,24 +62,143 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// D(16x8) += A(16x16) . B(16x8), fp64, fragments per the PTX ISA m16n8k16 layout.
-__device__ __forceinline__ void mma_16816(double (&d)[4], const double (&a)[8], const double4& b) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 "
-      "{%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
-      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
-      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
-        "d"(b.x), "d"(b.y), "d"(b.z), "d"(b.w));
-}
-
 constexpr int kBarBytes = 256;   // full[8] + empty[8] mbarriers, padded
 
 __host__ __device__ constexpr uint32_t round_up_u32(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
+// One 8x8x4 fp64 MMA (the native DMMA shape): d(8x8) += a(8x4) . b(4x8).
+// Fragments: a = A[g][t0], b = B[t0][g], d = {D[g][2 t0], D[g][2 t0 + 1]}
+// with g = lane / 4, t0 = lane % 4.
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// A fragments of one 16-row x 16-k block for this lane: a[2q + h] is the
+// value of k4-step q for row half h (rows g and g + 8), i.e. physical
+// column 4*t0 + q of rows r0 (h = 0) and r1 (h = 1).
+template <bool FULL>
+__device__ __forceinline__ void load_a16(double (&a)[8], const double* r0, const double* r1, int kbase, int K) {
+  if (FULL) {
+    const double2 x0 = *reinterpret_cast<const double2*>(r0 + kbase);
+    const double2 x1 = *reinterpret_cast<const double2*>(r0 + kbase + 2);
+    const double2 y0 = *reinterpret_cast<const double2*>(r1 + kbase);
+    const double2 y1 = *reinterpret_cast<const double2*>(r1 + kbase + 2);
+    a[0] = x0.x; a[2] = x0.y; a[4] = x1.x; a[6] = x1.y;
+    a[1] = y0.x; a[3] = y0.y; a[5] = y1.x; a[7] = y1.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool ok = (kbase + q) < K;
+      a[2 * q] = ok ? r0[kbase + q] : 0.0;
+      a[2 * q + 1] = ok ? r1[kbase + q] : 0.0;
+    }
+  }
+}
+
+// 16 rows x NBC n8-blocks (starting at n-block nb0) of one sub-tile:
+// c[nb][2h + v] = D[row g + 8h][col (nb0+nb)*8 + 2 t0 + v].
+// Issue order: k4-step outermost, then n-block, then row half, so that two
+// DMMAs into the same accumulator are 2*NBC instructions apart.
+template <int KB, int NB, int NBC>
+__device__ __forceinline__ void subtile_mma(double (&c)[NBC > 0 ? NBC : 1][4], const double* r0, const double* r1,
+                                            const double4* sB, int nb0, int lane, int K, bool kfull) {
+  const int t0 = lane & 3;
+#pragma unroll
+  for (int nb = 0; nb < NBC; ++nb) c[nb][0] = c[nb][1] = c[nb][2] = c[nb][3] = 0.0;
+#pragma unroll
+  for (int kb = 0; kb < KB; ++kb) {
+    double a[8];
+    const int kbase = kb * 16 + 4 * t0;
+    if (kfull || kb < KB - 1) load_a16<true>(a, r0, r1, kbase, K);
+    else load_a16<false>(a, r0, r1, kbase, K);
+    double4 b[NBC > 0 ? NBC : 1];
+#pragma unroll
+    for (int nb = 0; nb < NBC; ++nb) b[nb] = sB[(kb * NB + nb0 + nb) * 32 + lane];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int nb = 0; nb < NBC; ++nb) {
+        const double bq = q == 0 ? b[nb].x : q == 1 ? b[nb].y : q == 2 ? b[nb].z : b[nb].w;
+        dmma_884(c[nb][0], c[nb][1], a[2 * q], bq);
+        dmma_884(c[nb][2], c[nb][3], a[2 * q + 1], bq);
+      }
+    }
+  }
+}
+
+// Alg. 2 line 8 (row separation): column n = i*RP + b of GEMM row m goes to
+// out row m + half*(s + i), s = m / half (the RHS index).
+template <int NBC>
+__device__ __forceinline__ void subtile_store(const double (&c)[NBC > 0 ? NBC : 1][4], const LevelArgs& p,
+                                              int64_t m_first, int nb0, int lane) {
+  const int g = lane >> 2, t0 = lane & 3;
+  const bool vec_out = (p.r_out % 2) == 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t m = m_first + g + 8 * h;
+    if (m >= p.M) continue;
+    const int64_t sr = m / p.half;
+#pragma unroll
+    for (int nb = 0; nb < NBC; ++nb) {
+      const int n = (nb0 + nb) * 8 + 2 * t0;
+      const int i = n / p.RP;
+      const int b = n - i * p.RP;
+      if (i > 1 || b >= p.r_out) continue;
+      double* dst = p.out + (m + p.half * (sr + i)) * p.r_out + b;
+      const double v0 = c[nb][2 * h], v1 = c[nb][2 * h + 1];
+      if (vec_out) {
+        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+      } else {
+        dst[0] = v0;
+        if (b + 1 < p.r_out) dst[1] = v1;
+      }
+    }
+  }
+}
+
+// Consumer loop of one warp: row group rg (16 rows of each 64-row sub-tile),
+// n-blocks [nb0, nb0 + NBC).
+template <int KB, int NB, int NBC>
+__device__ __forceinline__ void consumer_loop(const LevelArgs& p, uint64_t* full, uint64_t* empty,
+                                              const double4* sB, const unsigned char* sA, uint32_t stage_stride,
+                                              int rg, int nb0, int lane) {
+  const int K = p.K;
+  const int S = p.stages;
+  const int rows_per_stage = kDmmaRowsPerSubtile * p.rep;
+  const int64_t nstage_tiles = (p.M + rows_per_stage - 1) / rows_per_stage;
+  const bool kfull = (K == 16 * KB);
+  const int g = lane >> 2;
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < nstage_tiles; t += gridDim.x, ++it) {
+    const int s = it % S;
+    const uint32_t ph = uint32_t(it / S) & 1u;
+    mbar_wait(&full[s], ph);
+    const double* stage = reinterpret_cast<const double*>(sA + size_t(s) * stage_stride);
+    const int64_t m_stage = t * rows_per_stage;
+    for (int u = 0; u < p.rep; ++u) {
+      const int lrow0 = u * kDmmaRowsPerSubtile + rg * 16;
+      const double* r0 = stage + size_t(lrow0 + g) * K;
+      const double* r1 = r0 + size_t(8) * K;
+      double c[NBC > 0 ? NBC : 1][4];
+      if (NBC > 0) subtile_mma<KB, NB, NBC>(c, r0, r1, sB, nb0, lane, K, kfull);
+      if (u == p.rep - 1) {
+        // every smem read of this stage has been consumed by the MMAs above
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      if (NBC > 0) subtile_store<NBC>(c, p, m_stage + lrow0, nb0, lane);
+    }
+  }
+}
+
 template <int KB, int NB>
 __global__ void __launch_bounds__((kDmmaConsumerWarps + 1) * 32, 1)
 level_dmma_kernel(const LevelArgs p) {
-  constexpr int CW = kDmmaConsumerWarps;
+  constexpr int CW = kDmmaConsumerWarps;          // 8 = 4 row groups x 2 column groups
+  constexpr int NB0 = (NB + 1) / 2;               // n-blocks of column group 0
+  constexpr int NB1 = NB - NB0;                   // n-blocks of column group 1
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
@@ -107,12 +226,11 @@ level_dmma_kernel(const LevelArgs p) {
   }
   __syncthreads();
 
-  const int64_t M = p.M;
-  const int64_t nstage_tiles = (M + rows_per_stage - 1) / rows_per_stage;
-
   if (warp == CW) {
     // ---------------- TMA producer (one lane) ----------------
     if (lane == 0) {
+      const int64_t M = p.M;
+      const int64_t nstage_tiles = (M + rows_per_stage - 1) / rows_per_stage;
       int it = 0;
       for (int64_t t = blockIdx.x; t < nstage_tiles; t += gridDim.x, ++it) {
         const int s = it % S;
@@ -127,85 +245,9 @@ level_dmma_kernel(const LevelArgs p) {
     }
     return;
   }
-
-  // ---------------- consumers: 4 warps x 16 rows per sub-tile ----------------
-  const int g = lane >> 2;
-  const int t0 = lane & 3;
-  const bool kfull = (K == 16 * KB);
-  const bool vec_out = (p.r_out % 2) == 0;
-  const int RP = p.RP;
-  const int r_out = p.r_out;
-  const int64_t half = p.half;
-
-  int it = 0;
-  for (int64_t t = blockIdx.x; t < nstage_tiles; t += gridDim.x, ++it) {
-    const int s = it % S;
-    const uint32_t ph = uint32_t(it / S) & 1u;
-    mbar_wait(&full[s], ph);
-    const double* stage = reinterpret_cast<const double*>(sA + size_t(s) * stage_stride);
-    const int64_t m_stage = t * rows_per_stage;
-
-    for (int u = 0; u < p.rep; ++u) {
-      const int lrow = u * kDmmaRowsPerSubtile + warp * 16 + g;     // local row of this lane (h = 0)
-      const double* r0 = stage + size_t(lrow) * K;
-      const double* r1 = r0 + size_t(8) * K;
-      double c[NB][4];
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb) c[nb][0] = c[nb][1] = c[nb][2] = c[nb][3] = 0.0;
-#pragma unroll
-      for (int kb = 0; kb < KB; ++kb) {
-        double a[8];
-        const int kbase = kb * 16 + 4 * t0;
-        if (kfull || kb < KB - 1) {
-          const double2 x0 = *reinterpret_cast<const double2*>(r0 + kbase);
-          const double2 x1 = *reinterpret_cast<const double2*>(r0 + kbase + 2);
-          const double2 y0 = *reinterpret_cast<const double2*>(r1 + kbase);
-          const double2 y1 = *reinterpret_cast<const double2*>(r1 + kbase + 2);
-          a[0] = x0.x; a[2] = x0.y; a[4] = x1.x; a[6] = x1.y;
-          a[1] = y0.x; a[3] = y0.y; a[5] = y1.x; a[7] = y1.y;
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const bool ok = (kbase + q) < K;
-            a[2 * q] = ok ? r0[kbase + q] : 0.0;
-            a[2 * q + 1] = ok ? r1[kbase + q] : 0.0;
-          }
-        }
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          const double4 b = sB[(kb * NB + nb) * 32 + lane];
-          mma_16816(c[nb], a, b);
-        }
-      }
-      if (u == p.rep - 1) {
-        // all smem reads of this stage are complete (their values were consumed above)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-      }
-      // ---- epilogue: row separation (Alg. 2 line 8) ----
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t m = m_stage + lrow + 8 * h;
-        if (m >= M) continue;
-        const int64_t sr = m / half;
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          const int n = nb * 8 + 2 * t0;
-          const int i = n / RP;
-          const int b = n - i * RP;
-          if (i > 1 || b >= r_out) continue;
-          double* dst = p.out + (m + half * (sr + i)) * r_out + b;
-          const double v0 = c[nb][2 * h], v1 = c[nb][2 * h + 1];
-          if (vec_out) {
-            *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-          } else {
-            dst[0] = v0;
-            if (b + 1 < r_out) dst[1] = v1;
-          }
-        }
-      }
-    }
-  }
+  const int rg = warp & 3;
+  if (warp < 4) consumer_loop<KB, NB, NB0>(p, full, empty, sB, sA, stage_stride, rg, 0, lane);
+  else consumer_loop<KB, NB, NB1>(p, full, empty, sB, sA, stage_stride, rg, NB0, lane);
 }
 
 using KernelFn = void (*)(const LevelArgs);

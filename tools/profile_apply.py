@@ -1,0 +1,34 @@
+"""Run a few QTT applies of one BASELINE config (for ncu / compute-sanitizer).
+
+    python tools/profile_apply.py --config c4 --reps 2
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--reps", type=int, default=2)
+    args = ap.parse_args()
+    import torch
+    import paper_1511_06029_b200 as q
+    from qtt_workload import generate
+    cfg, cores, x = generate(args.config)
+    op = q.QttOperator(cores)
+    xt = torch.from_numpy(x).cuda()
+    y = torch.empty_like(xt)
+    for _ in range(args.reps):
+        op.apply(xt, out=y)
+    torch.cuda.synchronize()
+    print("stages:", [(s["k_first"], s["k_last"], s["variant"]) for s in op.stages()])
+    print("ok", float(y.abs().sum()))
+    op.close()
+
+
+if __name__ == "__main__":
+    main()
