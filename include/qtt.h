@@ -23,8 +23,9 @@
  *
  * Semantics: y = A x up to fp64 rounding (IEEE binary64, FMA contraction,
  * no reduced precision).  NaN/Inf propagate per IEEE; nothing is checked.
- * Results are bitwise deterministic for a fixed (handle, nrhs): no atomics,
- * no split-K.  No exceptions cross this boundary; every entry point returns
+ * Results are bitwise deterministic for a fixed (handle, nrhs): no split-K
+ * and no atomic accumulation (the one atomic, the dynamic tile scheduler,
+ * decides only which SM computes a tile, never the order of its arithmetic).  No exceptions cross this boundary; every entry point returns
  * a qtt_status_t.
  */
 #ifndef QTT_B200_H
@@ -87,7 +88,8 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
                        qtt_stream_t stream);
 
 /* Bytes of device workspace one apply with `nrhs` right-hand sides needs
- * (two ping-pong buffers of max interior rank * N * nrhs doubles; 0 if d==1). */
+ * (256 bytes of scheduler counters plus two ping-pong buffers of max interior
+ * rank * N * nrhs doubles; the buffers are absent when d == 1). */
 qtt_status_t qtt_workspace_size(qtt_handle_t h, int64_t nrhs, size_t* bytes);
 
 /* qtt_apply with caller-owned DEVICE workspace `ws` of `ws_bytes` >= the

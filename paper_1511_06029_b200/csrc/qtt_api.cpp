@@ -115,12 +115,18 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs) {
+// Workspace layout: [256 B: per-level tile counters of the dynamic scheduler]
+// [buffer 0][buffer 1], each buffer max interior rank * N * nrhs doubles (the
+// ping-pong intermediate y_k of Alg. 2).
+constexpr size_t kWsHeader = 256;
+
+size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs) {
   if (h->d <= 1) return 0;
   const size_t one = size_t(h->max_interior_rank) * size_t(h->N) * size_t(nrhs) * sizeof(double);
-  const size_t aligned = (one + 255) / 256 * 256;
-  return 2 * aligned;
+  return (one + 255) / 256 * 256;
 }
+
+size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs) { return kWsHeader + 2 * ws_buf_bytes(h, nrhs); }
 
 void free_plan(qtt_plan* h) {
   for (auto& L : h->levels) {
@@ -192,8 +198,12 @@ qtt_status_t plan_level(qtt_plan* h, Level& L, const double* G) {
 
 qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st) {
   const int64_t half = h->N / 2;
-  const size_t buf_elems = ws ? (ws_bytes_for(h, nrhs) / 2) / sizeof(double) : 0;
-  double* buf[2] = {static_cast<double*>(ws), ws ? static_cast<double*>(ws) + buf_elems : nullptr};
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  int* counters = reinterpret_cast<int*>(base);
+  const size_t bb = ws_buf_bytes(h, nrhs);
+  double* buf[2] = {reinterpret_cast<double*>(base + kWsHeader), reinterpret_cast<double*>(base + kWsHeader + bb)};
+  cudaError_t me = cudaMemsetAsync(counters, 0, kWsHeader, st);
+  if (me != cudaSuccess) return from_cuda(me);
   const double* in = x;
   for (int k = 0; k < h->d; ++k) {
     const Level& L = h->levels[k];
@@ -205,6 +215,8 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
     a.core = L.d_core;
     a.M = nrhs * half;
     a.half = half;
+    a.log2_half = h->d - 1;
+    a.tile_counter = counters + k;
     a.r_in = L.r_in;
     a.r_out = L.r_out;
     a.RP = L.RP;
@@ -337,14 +349,12 @@ qtt_status_t qtt_apply_ws(qtt_handle_t h, const double* x, double* y, int64_t nr
   qtt_status_t s = check_apply_args(h, x, y, nrhs);
   if (s != QTT_SUCCESS) return s;
   const size_t need = ws_bytes_for(h, nrhs);
-  if (need > 0) {
-    if (!ws || ws_bytes < need) return QTT_ERROR_INVALID_VALUE;
-    if (reinterpret_cast<uintptr_t>(ws) % 256) return QTT_ERROR_NOT_SUPPORTED;
-    if (!is_device_ptr(ws)) return QTT_ERROR_NOT_SUPPORTED;
-  }
+  if (!ws || ws_bytes < need) return QTT_ERROR_INVALID_VALUE;
+  if (reinterpret_cast<uintptr_t>(ws) % 256) return QTT_ERROR_NOT_SUPPORTED;
+  if (!is_device_ptr(ws)) return QTT_ERROR_NOT_SUPPORTED;
   try {
     DeviceGuard g(h->device);
-    return enqueue(h, x, y, nrhs, need ? ws : nullptr, reinterpret_cast<cudaStream_t>(stream));
+    return enqueue(h, x, y, nrhs, ws, reinterpret_cast<cudaStream_t>(stream));
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
@@ -372,7 +382,7 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
       h->ws_bytes = need;
       h->ws_stream = st;
     }
-    return enqueue(h, x, y, nrhs, need ? h->ws : nullptr, st);
+    return enqueue(h, x, y, nrhs, h->ws, st);
   } catch (...) {
     return QTT_ERROR_CUDA;
   }

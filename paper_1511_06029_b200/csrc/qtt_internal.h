@@ -14,8 +14,12 @@ enum Variant : int { kGeneric = 0, kDmma = 1, kFused = 2 };
 // 2 * roundup(r_out, 2) <= 8*kMaxNB.
 constexpr int kMaxKB = 6;
 constexpr int kMaxNB = 12;
-constexpr int kDmmaConsumerWarps = 8;            // 4 row groups (16 rows) x 2 column groups
-constexpr int kDmmaRowsPerSubtile = 64;
+constexpr int kDmmaRowGroups = 4;                // 4 x 16 rows = one 64-row sub-tile
+constexpr int kDmmaRowsPerSubtile = 16 * kDmmaRowGroups;
+// Column groups of consumer warps for a level with NB n8-blocks: 2-3 warps per
+// SM sub-partition for the wide levels, fewer for narrow (memory-bound) ones.
+__host__ __device__ constexpr int dmma_col_groups(int NB) { return NB >= 9 ? 3 : (NB >= 2 ? 2 : 1); }
+__host__ __device__ constexpr int dmma_threads(int NB) { return (kDmmaRowGroups * dmma_col_groups(NB) + 1) * 32; }
 constexpr int kMaxStages = 8;
 
 // One level (= one core, PAPER Alg. 2 lines 5-8) as a GEMM over the rotating
@@ -28,6 +32,8 @@ struct LevelArgs {
   const double* core = nullptr;    // generic: raw core [a][i][j][b]
   int64_t M = 0;                   // GEMM rows: nrhs * N / 2
   int64_t half = 0;                // N / 2
+  int log2_half = 0;               // half = 2^log2_half
+  int* tile_counter = nullptr;     // zeroed before the launch; dynamic tile scheduler
   int r_in = 0, r_out = 0;
   int RP = 0;                      // r_out rounded up to even (column padding per half)
   int K = 0;                       // 2 * r_in

@@ -62,7 +62,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-constexpr int kBarBytes = 256;   // full[8] + empty[8] mbarriers, padded
+constexpr int kBarBytes = 256;   // full[8] + empty[8] mbarriers + tile_id[8]
 
 __host__ __device__ constexpr uint32_t round_up_u32(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
@@ -129,52 +129,61 @@ __device__ __forceinline__ void subtile_mma(double (&c)[NBC > 0 ? NBC : 1][4], c
 }
 
 // Alg. 2 line 8 (row separation): column n = i*RP + b of GEMM row m goes to
-// out row m + half*(s + i), s = m / half (the RHS index).
+// out row m + half*(s + i), s = m / half (the RHS index; half = N/2 is a power of 2).
+// coff[nb] = half*i*r_out + b for this lane's column pair, or -1 if padding.
 template <int NBC>
 __device__ __forceinline__ void subtile_store(const double (&c)[NBC > 0 ? NBC : 1][4], const LevelArgs& p,
-                                              int64_t m_first, int nb0, int lane) {
-  const int g = lane >> 2, t0 = lane & 3;
-  const bool vec_out = (p.r_out % 2) == 0;
+                                              const int64_t (&coff)[NBC > 0 ? NBC : 1], bool vec_out,
+                                              int64_t m_first, int lane) {
+  const int g = lane >> 2;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int64_t m = m_first + g + 8 * h;
     if (m >= p.M) continue;
-    const int64_t sr = m / p.half;
+    double* rowp = p.out + (m + ((m >> p.log2_half) << p.log2_half)) * p.r_out;
 #pragma unroll
     for (int nb = 0; nb < NBC; ++nb) {
-      const int n = (nb0 + nb) * 8 + 2 * t0;
-      const int i = n / p.RP;
-      const int b = n - i * p.RP;
-      if (i > 1 || b >= p.r_out) continue;
-      double* dst = p.out + (m + p.half * (sr + i)) * p.r_out + b;
+      if (coff[nb] < 0) continue;
+      double* dst = rowp + coff[nb];
       const double v0 = c[nb][2 * h], v1 = c[nb][2 * h + 1];
       if (vec_out) {
         *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
       } else {
         dst[0] = v0;
-        if (b + 1 < p.r_out) dst[1] = v1;
+        if (((coff[nb] % p.r_out) + 1) < p.r_out) dst[1] = v1;
       }
     }
   }
 }
 
 // Consumer loop of one warp: row group rg (16 rows of each 64-row sub-tile),
-// n-blocks [nb0, nb0 + NBC).
+// n-blocks [nb0, nb0 + NBC).  Tiles arrive from the producer through the
+// smem ring; tile index -1 ends the loop.
 template <int KB, int NB, int NBC>
 __device__ __forceinline__ void consumer_loop(const LevelArgs& p, uint64_t* full, uint64_t* empty,
-                                              const double4* sB, const unsigned char* sA, uint32_t stage_stride,
-                                              int rg, int nb0, int lane) {
+                                              const int64_t* tile_id, const double4* sB,
+                                              const unsigned char* sA, uint32_t stage_stride, int rg, int nb0,
+                                              int lane) {
   const int K = p.K;
   const int S = p.stages;
   const int rows_per_stage = kDmmaRowsPerSubtile * p.rep;
-  const int64_t nstage_tiles = (p.M + rows_per_stage - 1) / rows_per_stage;
   const bool kfull = (K == 16 * KB);
-  const int g = lane >> 2;
-  int it = 0;
-  for (int64_t t = blockIdx.x; t < nstage_tiles; t += gridDim.x, ++it) {
+  const bool vec_out = (p.r_out % 2) == 0;
+  const int g = lane >> 2, t0 = lane & 3;
+  int64_t coff[NBC > 0 ? NBC : 1];
+#pragma unroll
+  for (int nb = 0; nb < NBC; ++nb) {
+    const int n = (nb0 + nb) * 8 + 2 * t0;
+    const int i = n / p.RP;
+    const int b = n - i * p.RP;
+    coff[nb] = (i > 1 || b >= p.r_out) ? int64_t(-1) : (p.half * i * p.r_out + b);
+  }
+  for (int it = 0;; ++it) {
     const int s = it % S;
     const uint32_t ph = uint32_t(it / S) & 1u;
     mbar_wait(&full[s], ph);
+    const int64_t t = tile_id[s];
+    if (t < 0) break;
     const double* stage = reinterpret_cast<const double*>(sA + size_t(s) * stage_stride);
     const int64_t m_stage = t * rows_per_stage;
     for (int u = 0; u < p.rep; ++u) {
@@ -188,20 +197,23 @@ __device__ __forceinline__ void consumer_loop(const LevelArgs& p, uint64_t* full
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
-      if (NBC > 0) subtile_store<NBC>(c, p, m_stage + lrow0, nb0, lane);
+      if (NBC > 0) subtile_store<NBC>(c, p, coff, vec_out, m_stage + lrow0, lane);
     }
   }
 }
 
 template <int KB, int NB>
-__global__ void __launch_bounds__((kDmmaConsumerWarps + 1) * 32, 1)
+__global__ void __launch_bounds__(dmma_threads(NB), 1)
 level_dmma_kernel(const LevelArgs p) {
-  constexpr int CW = kDmmaConsumerWarps;          // 8 = 4 row groups x 2 column groups
-  constexpr int NB0 = (NB + 1) / 2;               // n-blocks of column group 0
-  constexpr int NB1 = NB - NB0;                   // n-blocks of column group 1
+  constexpr int CG = dmma_col_groups(NB);
+  constexpr int CW = kDmmaRowGroups * CG;         // consumer warps
+  constexpr int NBW = (NB + CG - 1) / CG;         // n-blocks per column group
+  constexpr int NB_1 = (NB - NBW) < NBW ? (NB - NBW) : NBW;
+  constexpr int NB_2 = NB - NBW - NB_1;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
+  int64_t* tile_id = reinterpret_cast<int64_t*>(empty + kMaxStages);
   double4* sB = reinterpret_cast<double4*>(smem + kBarBytes);
   unsigned char* sA = smem + kBarBytes + KB * NB * 32 * sizeof(double4);
 
@@ -227,15 +239,21 @@ level_dmma_kernel(const LevelArgs p) {
   __syncthreads();
 
   if (warp == CW) {
-    // ---------------- TMA producer (one lane) ----------------
+    // ---------------- producer: dynamic tile scheduler + TMA bulk loads ----------------
     if (lane == 0) {
       const int64_t M = p.M;
       const int64_t nstage_tiles = (M + rows_per_stage - 1) / rows_per_stage;
-      int it = 0;
-      for (int64_t t = blockIdx.x; t < nstage_tiles; t += gridDim.x, ++it) {
+      for (int it = 0;; ++it) {
         const int s = it % S;
         const uint32_t ph = uint32_t(it / S) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
+        const int64_t t = atomicAdd(p.tile_counter, 1);
+        if (t >= nstage_tiles) {
+          tile_id[s] = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        tile_id[s] = t;
         const int64_t m0 = t * rows_per_stage;
         const int64_t rows = (M - m0) < rows_per_stage ? (M - m0) : rows_per_stage;
         const uint32_t bytes = uint32_t(rows) * uint32_t(K) * 8u;
@@ -245,9 +263,11 @@ level_dmma_kernel(const LevelArgs p) {
     }
     return;
   }
-  const int rg = warp & 3;
-  if (warp < 4) consumer_loop<KB, NB, NB0>(p, full, empty, sB, sA, stage_stride, rg, 0, lane);
-  else consumer_loop<KB, NB, NB1>(p, full, empty, sB, sA, stage_stride, rg, NB0, lane);
+  const int rg = warp % kDmmaRowGroups;
+  const int cg = warp / kDmmaRowGroups;
+  if (cg == 0) consumer_loop<KB, NB, NBW>(p, full, empty, tile_id, sB, sA, stage_stride, rg, 0, lane);
+  else if (cg == 1) consumer_loop<KB, NB, NB_1>(p, full, empty, tile_id, sB, sA, stage_stride, rg, NBW, lane);
+  else consumer_loop<KB, NB, NB_2>(p, full, empty, tile_id, sB, sA, stage_stride, rg, NBW + NB_1, lane);
 }
 
 using KernelFn = void (*)(const LevelArgs);
@@ -285,7 +305,7 @@ __global__ void level_generic_kernel(const LevelArgs p) {
       const double* g = p.core + (size_t(i) * 2 + j) * r_out + b;   // G[a][i][j][b], a stride 4 r_out
       for (int a = 0; a < r_in; ++a) acc = fma(g[size_t(a) * 4 * r_out], in[a], acc);
     }
-    const int64_t sr = m / p.half;
+    const int64_t sr = m >> p.log2_half;
     p.out[(m + p.half * (sr + i)) * r_out + b] = acc;
   }
 }
@@ -308,13 +328,13 @@ cudaError_t dmma_occupancy(int KB, int NB, size_t smem, int* ctas_per_sm) {
   KernelFn f = lookup(KB, NB);
   if (!f) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, reinterpret_cast<const void*>(f),
-                                                       (kDmmaConsumerWarps + 1) * 32, smem);
+                                                       dmma_threads(NB), smem);
 }
 
 cudaError_t launch_level_dmma(const LevelArgs& a, cudaStream_t st) {
   KernelFn f = lookup(a.KB, a.NB);
   if (!f) return cudaErrorInvalidValue;
-  f<<<a.grid, (kDmmaConsumerWarps + 1) * 32, a.smem, st>>>(a);
+  f<<<a.grid, dmma_threads(a.NB), a.smem, st>>>(a);
   return cudaGetLastError();
 }
 
