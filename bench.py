@@ -247,6 +247,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=20.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--max-stage-levels", type=int, default=None,
+                    help="cap on levels per launch (1 = Alg. 2 level by level); default: the library's")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
@@ -263,7 +265,7 @@ def main(argv=None):
 
     cfg, cores, x_np = generate(args.config)
     nrhs = cfg.nrhs
-    op = q.QttOperator(cores)
+    op = q.QttOperator(cores, max_stage_levels=args.max_stage_levels)
     x = torch.from_numpy(x_np).to(dev)
     y = torch.empty_like(x)
     ws = torch.empty(max(op.workspace_size(nrhs), 8) // 8 + 64, dtype=torch.float64, device=dev)
@@ -323,28 +325,34 @@ def main(argv=None):
         k0, k1 = st["k_first"], st["k_last"]
         F = sum(4 * r[k - 1] * r[k] for k in range(k0, k1 + 1)) * N * nrhs
         B = 8 * N * nrhs * (r[k0 - 1] + r[k1]) + 32 * sum(r[k - 1] * r[k] for k in range(k0, k1 + 1))
+        # flops the kernel actually executes (unpadded): a merged stage of L levels
+        # applies the 2^L r_in x 2^L r_out super-core, 2^(L+1) r_in r_out per element
+        F_exec = (2 ** (k1 - k0 + 2)) * r[k0 - 1] * r[k1] * N * nrhs if k1 > k0 else F
         t = stage_ms[s] / max(n_timed, 1) * 1e-3
         T = max(F / P, B / BW)
         sum_T += T
         sum_t += t
         stage_rows.append({"levels": [k0, k1], "ranks": [r[k0 - 1], r[k1]], "variant": st["variant"],
                            "ms": t * 1e3, "gflops": F / t / 1e9 if t else None,
-                           "gbs": B / t / 1e9 if t else None, "roofline_frac": T / t if t else None})
-    # dominant kernel: the DMMA instance with the largest share of the step
+                           "gbs": B / t / 1e9 if t else None, "roofline_frac": T / t if t else None,
+                           "flops_alg2": F, "flops_executed": F_exec,
+                           "roofline_frac_executed": max(F_exec / P, B / BW) / t if t else None})
+    # dominant kernel: the stage shape with the largest share of the step
     by_kernel = {}
     for s, row in enumerate(stage_rows):
-        key = (row["variant"], row["ranks"][0], row["ranks"][1])
+        key = (row["variant"], row["ranks"][0], row["ranks"][1], row["levels"][1] - row["levels"][0] + 1)
         by_kernel.setdefault(key, []).append(row)
     dom_key = max(by_kernel, key=lambda k: sum(rr["ms"] for rr in by_kernel[k]))
     dom = by_kernel[dom_key]
     dom_ms = sum(rr["ms"] for rr in dom) / len(dom)
     rin, rout = dom_key[1], dom_key[2]
-    dom_flops = 4 * rin * rout * N * nrhs
+    dom_flops = dom[0]["flops_executed"]
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12
     tr = load_traffic(args.config)
     roofline = {"bound": "tensor", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
                 "frac": achieved / fp64, "traffic": tr[0] if tr else None,
-                "kernel": f"level_dmma_kernel r_in={rin} r_out={rout} ({dom_key[0]}; {len(dom)} launches/step)",
+                "kernel": f"level_dmma_kernel r_in={rin} r_out={rout} levels/launch={dom_key[3]} "
+                          f"({dom_key[0]}; {len(dom)} launches/step)",
                 "share_of_step": sum(rr["ms"] for rr in dom) / (ms_step if world == 1 else ms_local / args.steps),
                 "peak_source": fp64_src + "; MEASURED_PEAKS.json has no FP64 figure",
                 "algorithmic_flops_per_launch": dom_flops,
@@ -373,7 +381,8 @@ def main(argv=None):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; random cores with the config's rank profile stand in for the paper's inverse cores)",
-        "config": config_desc(cfg, nrhs),
+        "config": dict(config_desc(cfg, nrhs), launches_per_apply=op.launches_per_apply,
+                       stages=[[st["k_first"], st["k_last"]] for st in stages]),
         "gbs": (16 * N * nrhs) / (ms_step * 1e-3) / 1e9,
         "per_stage_roofline": per_stage,
         "roofline": roofline,

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-/* Opaque plan: packed cores in device memory + per-level kernel schedule. */
+/* Opaque plan: packed (super-)cores in device memory + the stage schedule. */
 typedef struct qtt_plan* qtt_handle_t;
 
 /* A CUDA stream; layout-compatible with cudaStream_t / CUstream (NULL = the
@@ -67,11 +67,40 @@ const char* qtt_status_string(qtt_status_t s);
  *            ranks[k-1]*4*ranks[k] doubles in [a][i][j][b] order.
  * The library COPIES and repacks the cores into device memory it owns (on
  * the current CUDA device), so the caller may free its arrays on return.
- * Synchronous.  Plans the per-level kernels (ranks <= 64 run on the FP64
- * tensor-core path, larger ranks on a generic kernel) and uploads.
+ * Synchronous.  Plans the stages (see qtt_plan_stages) and uploads.
  */
 qtt_status_t qtt_create(qtt_handle_t* out, int d, const int64_t* ranks,
                         const double* const* cores);
+
+/*
+ * qtt_create_ex -- qtt_create with the longest merged stage capped at
+ * `max_stage_levels` levels (>= 1; 1 = one launch per level, i.e. PAPER
+ * Alg. 2 executed level by level; qtt_create uses 6).  Otherwise identical.
+ */
+qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks,
+                           const double* const* cores, int max_stage_levels);
+
+/*
+ * qtt_plan_stages -- the stage schedule qtt_create_ex would choose, computed
+ * on the host without touching a GPU (pure function of the rank profile).
+ * A stage is a run of consecutive levels [k_first, k_last] applied by one
+ * kernel launch.  Alg. 2 applies one core per level; a stage of
+ * L >= 2 levels applies instead the product of its L cores contracted over
+ * the inner bonds (the super-core W[a][ii][jj][b], the QTT definition
+ * P:519-523 restricted to the stage's L digits, built once at create time),
+ * which is the same linear map, so the level intermediates never exist.  The
+ * schedule minimises a cost model of FP64 tensor-core time, HBM bytes and
+ * launch latency by dynamic programming over the levels.
+ *   d, ranks          : as for qtt_create (validated the same way).
+ *   smem_optin        : max dynamic shared memory per block (0 = B200's 232448).
+ *   max_stage_levels  : >= 1, as for qtt_create_ex.
+ *   n_stages          : receives the number of stages (<= d).
+ *   k_first, k_last, variant : arrays of >= d ints (any may be NULL) receiving
+ *                       per stage the 1-based level range and the variant
+ *                       (0 generic, 1 DMMA one level, 2 DMMA merged stage).
+ */
+qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
+                             int* n_stages, int* k_first, int* k_last, int* variant);
 
 /*
  * qtt_apply -- y = A x on `stream` (asynchronous, stream-ordered).
@@ -88,8 +117,8 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
                        qtt_stream_t stream);
 
 /* Bytes of device workspace one apply with `nrhs` right-hand sides needs
- * (256 bytes of scheduler counters plus two ping-pong buffers of max interior
- * rank * N * nrhs doubles; the buffers are absent when d == 1). */
+ * (256 bytes of scheduler counters plus two ping-pong buffers of max
+ * stage-boundary rank * N * nrhs doubles; absent for a one-stage plan). */
 qtt_status_t qtt_workspace_size(qtt_handle_t h, int64_t nrhs, size_t* bytes);
 
 /* qtt_apply with caller-owned DEVICE workspace `ws` of `ws_bytes` >= the
@@ -113,9 +142,10 @@ qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank,
                           double* flops_per_rhs, int* launches_per_apply);
 
 /*
- * Per-stage description: stage s covers levels [*k_first, *k_last] (1-based)
- * and runs kernel variant *variant (0 = generic, 1 = fp64 tensor-core DMMA,
- * 2 = fused small-rank stage).
+ * Per-stage description: stage s (0 <= s < launches_per_apply) covers levels
+ * [*k_first, *k_last] (1-based) and runs kernel variant *variant (0 = generic,
+ * 1 = fp64 tensor-core DMMA, one level; 2 = DMMA merged stage of several
+ * levels, see qtt_plan_stages).
  */
 qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int* variant);
 

@@ -22,12 +22,13 @@ from . import _lib
 from ._lib import QttError, SYMBOLS
 
 __all__ = [
-    "QttOperator", "QttError", "qtt_create", "qtt_apply", "qtt_apply_ws", "qtt_apply_host",
+    "QttOperator", "QttError", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "plan_stages", "qtt_apply", "qtt_apply_ws", "qtt_apply_host",
     "qtt_workspace_size", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy", "qtt_status_string", "library_path", "SYMBOLS",
 ]
 
-VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "fused"}
+VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "merged"}
+MAX_STAGE_LEVELS = 6
 
 
 def library_path() -> str:
@@ -52,9 +53,7 @@ def qtt_status_string(code: int) -> str:
     return _lib.load().qtt_status_string(code).decode()
 
 
-def qtt_create(cores, ranks=None) -> int:
-    """cores: list of d float64 arrays (r_{k-1}, 2, 2, r_k). Returns a handle (int)."""
-    lib = _lib.load()
+def _marshal_cores(cores, ranks):
     d = len(cores)
     if d < 1:
         raise ValueError("need at least one core")
@@ -67,11 +66,52 @@ def qtt_create(cores, ranks=None) -> int:
     for k, a in enumerate(arrs):
         if a.shape != (ranks[k], 2, 2, ranks[k + 1]):
             raise ValueError(f"core {k + 1} has shape {a.shape}, expected {(ranks[k], 2, 2, ranks[k + 1])}")
+    return arrs, ranks
+
+
+def qtt_create_ex(cores, ranks=None, max_stage_levels: int = MAX_STAGE_LEVELS) -> int:
+    """cores: list of d float64 arrays (r_{k-1}, 2, 2, r_k). Returns a handle (int)."""
+    lib = _lib.load()
+    arrs, ranks = _marshal_cores(cores, ranks)
+    d = len(arrs)
+    r_arr = (C.c_int64 * (d + 1))(*ranks)
+    p_arr = (C.c_void_p * d)(*[a.ctypes.data for a in arrs])
+    h = C.c_void_p()
+    _lib.check("qtt_create_ex", lib.qtt_create_ex(C.byref(h), d, r_arr, p_arr, int(max_stage_levels)))
+    return int(h.value)
+
+
+def qtt_create(cores, ranks=None) -> int:
+    """cores: list of d float64 arrays (r_{k-1}, 2, 2, r_k). Returns a handle (int)."""
+    lib = _lib.load()
+    arrs, ranks = _marshal_cores(cores, ranks)
+    d = len(arrs)
     r_arr = (C.c_int64 * (d + 1))(*ranks)
     p_arr = (C.c_void_p * d)(*[a.ctypes.data for a in arrs])
     h = C.c_void_p()
     _lib.check("qtt_create", lib.qtt_create(C.byref(h), d, r_arr, p_arr))
     return int(h.value)
+
+
+def qtt_plan_stages(ranks, smem_optin: int = 0, max_stage_levels: int = MAX_STAGE_LEVELS):
+    """Host-only: the stage schedule for a rank profile, as [(k_first, k_last, variant_code)]."""
+    lib = _lib.load()
+    ranks = [int(r) for r in ranks]
+    d = len(ranks) - 1
+    if d < 1:
+        raise ValueError("need d >= 1")
+    r_arr = (C.c_int64 * (d + 1))(*ranks)
+    n = C.c_int()
+    a, b, v = (C.c_int * d)(), (C.c_int * d)(), (C.c_int * d)()
+    _lib.check("qtt_plan_stages", lib.qtt_plan_stages(d, r_arr, int(smem_optin), int(max_stage_levels),
+                                                      C.byref(n), a, b, v))
+    return [(a[i], b[i], v[i]) for i in range(n.value)]
+
+
+def plan_stages(ranks, max_stage_levels: int = MAX_STAGE_LEVELS):
+    """Like qtt_plan_stages with variant names: [{'k_first', 'k_last', 'variant'}]."""
+    return [dict(k_first=a, k_last=b, variant=VARIANT_NAMES.get(v, str(v)))
+            for a, b, v in qtt_plan_stages(ranks, 0, max_stage_levels)]
 
 
 def qtt_apply(h: int, x, y, nrhs: int, stream=None) -> None:
@@ -127,9 +167,12 @@ def qtt_destroy(h: int) -> None:
 class QttOperator:
     """A QTT matrix resident on the current CUDA device; ``apply`` computes y = A x."""
 
-    def __init__(self, cores, ranks=None):
+    def __init__(self, cores, ranks=None, max_stage_levels: int | None = None):
         self._h = None
-        self._h = qtt_create(cores, ranks)
+        if max_stage_levels is None:
+            self._h = qtt_create(cores, ranks)
+        else:
+            self._h = qtt_create_ex(cores, ranks, max_stage_levels)
         info = qtt_get_info(self._h)
         self.d = info["d"]
         self.N = info["N"]

@@ -18,7 +18,7 @@ QTT_ERROR_CUDA = 4
 
 # every symbol include/qtt.h declares
 SYMBOLS = (
-    "qtt_status_string", "qtt_create", "qtt_apply", "qtt_workspace_size", "qtt_apply_ws",
+    "qtt_status_string", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "qtt_apply", "qtt_workspace_size", "qtt_apply_ws",
     "qtt_apply_host", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy",
 )
@@ -43,6 +43,11 @@ def load():
     lib.qtt_status_string.argtypes = [st]
     lib.qtt_create.restype = st
     lib.qtt_create.argtypes = [C.POINTER(h), C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p)]
+    lib.qtt_create_ex.restype = st
+    lib.qtt_create_ex.argtypes = [C.POINTER(h), C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.c_int]
+    ip = C.POINTER(C.c_int)
+    lib.qtt_plan_stages.restype = st
+    lib.qtt_plan_stages.argtypes = [C.c_int, C.POINTER(i64), C.c_size_t, C.c_int, ip, ip, ip, ip]
     lib.qtt_apply.restype = st
     lib.qtt_apply.argtypes = [h, dp, dp, i64, C.c_void_p]
     lib.qtt_workspace_size.restype = st

@@ -1,7 +1,8 @@
 // C ABI of libqtt_b200.so (declared and documented in include/qtt.h).
 //
-// Host side of the QTT apply: argument validation, core packing,
-// the per-level stage plan (B4), workspace management and launches.  The
+// Host side of the QTT apply: argument validation, core packing and super-core
+// contraction, the stage plan (B4, qtt_plan.cpp), workspace
+// management and launches.  The
 // arithmetic of PAPER.md Alg. 2 runs entirely in the kernels
 // (qtt_level_dmma.cu); nothing here touches vector data.
 #include "../../include/qtt.h"
@@ -19,13 +20,12 @@ namespace {
 
 using qtt::LevelArgs;
 
-struct Level {
-  int r_in = 0, r_out = 0;
-  int variant = qtt::kGeneric;
-  int KB = 0, NB = 0, RP = 0, rep = 1, stages = 2, ctas_per_sm = 1;
-  size_t smem = 0;
-  double* d_bpack = nullptr;   // DMMA fragment-packed core
-  double* d_core = nullptr;    // raw core (generic kernel)
+// One launch of an apply: levels k0..k1 (a single level, or a merged stage).
+struct Stage {
+  qtt::StagePlan plan;
+  int ctas_per_sm = 1;
+  double* d_bpack = nullptr;   // DMMA fragment-packed (super-)core
+  double* d_core = nullptr;    // raw core (generic kernel, single level only)
 };
 
 struct StageEvents {
@@ -42,7 +42,7 @@ struct qtt_plan {
   int d = 0;
   int64_t N = 0;
   std::vector<int64_t> ranks;
-  std::vector<Level> levels;
+  std::vector<Stage> stages;
   int64_t max_interior_rank = 0;
   // cached workspace (qtt_apply)
   void* ws = nullptr;
@@ -82,13 +82,46 @@ qtt_status_t from_cuda(cudaError_t e) {
   return QTT_ERROR_CUDA;
 }
 
-// B operand of level k in MMA-fragment order (see qtt_level_dmma.cu):
-//   Bmat[kk][n], kk = j*r_in + a (the column-merged index of Alg. 2 line 6),
-//   n = i*RP + b (the row-separated output, Alg. 2 line 8), value G[a,i,j,b];
+// Super-core of levels k0..k1 (PAPER Eq. TTdeccores P:519-523 restricted to the
+// stage's digits; qtt_plan.cpp): W[a][ii][jj][b], ii/jj = the stage's output /
+// input digits, first level least significant.  Accumulated in long double.
+std::vector<double> super_core(const double* const* cores, const int64_t* ranks, int k0, int k1) {
+  const int r0 = int(ranks[k0 - 1]);
+  std::vector<long double> W(cores[k0 - 1], cores[k0 - 1] + size_t(r0) * 4 * ranks[k0]);
+  int n_i = 2;
+  int rc = int(ranks[k0]);
+  for (int k = k0 + 1; k <= k1; ++k) {
+    const double* G = cores[k - 1];
+    const int rb = int(ranks[k]);
+    const int n2 = 2 * n_i;
+    std::vector<long double> V(size_t(r0) * n2 * n2 * rb, 0.0L);
+    for (int a = 0; a < r0; ++a)
+      for (int ii = 0; ii < n_i; ++ii)
+        for (int jj = 0; jj < n_i; ++jj)
+          for (int c = 0; c < rc; ++c) {
+            const long double w = W[((size_t(a) * n_i + ii) * n_i + jj) * rc + c];
+            if (w == 0.0L) continue;
+            for (int i = 0; i < 2; ++i)
+              for (int j = 0; j < 2; ++j) {
+                const double* g = G + ((size_t(c) * 2 + i) * 2 + j) * rb;
+                long double* v = &V[((size_t(a) * n2 + ii + n_i * i) * n2 + jj + n_i * j) * rb];
+                for (int b = 0; b < rb; ++b) v[b] += w * g[b];
+              }
+          }
+    W.swap(V);
+    n_i = n2;
+    rc = rb;
+  }
+  return std::vector<double>(W.begin(), W.end());
+}
+
+// B operand of a stage in MMA-fragment order (see qtt_dmma_kernel.cuh):
+//   Bmat[kk][n], kk = jj*r_in + a (the column-merged index of Alg. 2 line 6),
+//   n = ii*RP + b (the row-separated output, Alg. 2 line 8), value W[a,ii,jj,b];
 //   pack[kb][nb][lane][v] = Bmat[kb*16 + 4*(lane%4) + v][nb*8 + lane/4].
-std::vector<double> pack_dmma(const double* G, int r_in, int r_out, int KB, int NB, int RP) {
+std::vector<double> pack_dmma(const double* W, const qtt::StagePlan& sp) {
+  const int KB = sp.KB, NB = sp.NB, RP = sp.RP, r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i;
   std::vector<double> out(size_t(KB) * NB * 32 * 4, 0.0);
-  const int K = 2 * r_in;
   for (int kb = 0; kb < KB; ++kb)
     for (int nb = 0; nb < NB; ++nb)
       for (int lane = 0; lane < 32; ++lane)
@@ -96,10 +129,10 @@ std::vector<double> pack_dmma(const double* G, int r_in, int r_out, int KB, int 
           const int kk = kb * 16 + 4 * (lane % 4) + v;
           const int n = nb * 8 + lane / 4;
           double val = 0.0;
-          if (kk < K) {
-            const int j = kk / r_in, a = kk % r_in;
-            const int i = n / RP, b = n % RP;
-            if (i < 2 && b < r_out) val = G[((size_t(a) * 2 + i) * 2 + j) * r_out + b];
+          if (kk < sp.K) {
+            const int jj = kk / r_in, a = kk % r_in;
+            const int ii = n / RP, b = n % RP;
+            if (ii < n_i && b < r_out) val = W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b];
           }
           out[((size_t(kb) * NB + nb) * 32 + lane) * 4 + v] = val;
         }
@@ -115,13 +148,13 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-// Workspace layout: [256 B: per-level tile counters of the dynamic scheduler]
-// [buffer 0][buffer 1], each buffer max interior rank * N * nrhs doubles (the
-// ping-pong intermediate y_k of Alg. 2).
+// Workspace layout: [256 B: per-stage tile counters of the dynamic scheduler]
+// [buffer 0][buffer 1], each buffer max stage-boundary rank * N * nrhs doubles
+// (the ping-pong intermediate y_k of Alg. 2 at the stage boundaries).
 constexpr size_t kWsHeader = 256;
 
 size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs) {
-  if (h->d <= 1) return 0;
+  if (h->stages.size() <= 1) return 0;
   const size_t one = size_t(h->max_interior_rank) * size_t(h->N) * size_t(nrhs) * sizeof(double);
   return (one + 255) / 256 * 256;
 }
@@ -129,9 +162,9 @@ size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs) {
 size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs) { return kWsHeader + 2 * ws_buf_bytes(h, nrhs); }
 
 void free_plan(qtt_plan* h) {
-  for (auto& L : h->levels) {
-    if (L.d_bpack) cudaFree(L.d_bpack);
-    if (L.d_core) cudaFree(L.d_core);
+  for (auto& S : h->stages) {
+    if (S.d_bpack) cudaFree(S.d_bpack);
+    if (S.d_core) cudaFree(S.d_core);
   }
   if (h->ws) cudaFree(h->ws);
   if (h->hx) cudaFree(h->hx);
@@ -144,60 +177,35 @@ void free_plan(qtt_plan* h) {
   delete h;
 }
 
-qtt_status_t plan_level(qtt_plan* h, Level& L, const double* G) {
-  const int r_in = L.r_in, r_out = L.r_out;
-  const size_t core_elems = size_t(r_in) * 4 * r_out;
-  cudaError_t e = cudaMalloc(&L.d_core, core_elems * sizeof(double));
-  if (e != cudaSuccess) return from_cuda(e);
-  e = cudaMemcpy(L.d_core, G, core_elems * sizeof(double), cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return from_cuda(e);
-
-  const int K = 2 * r_in;
-  const int RP = (r_out + 1) / 2 * 2;
-  const int KB = (K + 15) / 16;
-  const int NB = (2 * RP + 7) / 8;
-  L.RP = RP;
-  if (KB > qtt::kMaxKB || NB > qtt::kMaxNB) {
-    L.variant = qtt::kGeneric;
-    return QTT_SUCCESS;
+qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
+  const qtt::StagePlan& sp = S.plan;
+  if (sp.variant == qtt::kGeneric) {
+    const size_t core_elems = size_t(sp.r_in) * 4 * sp.r_out;
+    cudaError_t e = cudaMalloc(&S.d_core, core_elems * sizeof(double));
+    if (e != cudaSuccess) return from_cuda(e);
+    return from_cuda(cudaMemcpy(S.d_core, cores[sp.k0 - 1], core_elems * sizeof(double), cudaMemcpyHostToDevice));
   }
-  // TMA stage: >= 16 KiB per stage (HBM bytes in flight), <= 64 KiB.
-  const size_t sub_bytes = size_t(qtt::kDmmaRowsPerSubtile) * K * 8;
-  int rep = int(std::max<size_t>(1, (16384 + sub_bytes - 1) / sub_bytes));
-  while (rep > 1 && sub_bytes * rep > 65536) --rep;
-  int stages = qtt::kMaxStages;
-  size_t smem = 0;
-  for (; stages >= 2; --stages) {
-    smem = qtt::dmma_smem_bytes(KB, NB, K, rep, stages);
-    if (smem <= h->smem_optin) break;
-  }
-  if (stages < 2) {
-    L.variant = qtt::kGeneric;
-    return QTT_SUCCESS;
-  }
-  // The attribute is per kernel instance and shared by every level (and plan)
-  // that uses it, so raise it to the device maximum rather than this level's need.
-  e = qtt::dmma_prepare(KB, NB, h->smem_optin);
+  // The attribute is per kernel instance and shared by every stage (and plan)
+  // that uses it, so raise it to the device maximum rather than this stage's need.
+  cudaError_t e = qtt::dmma_prepare(sp.KB, sp.NB, h->smem_optin);
   if (e != cudaSuccess) return from_cuda(e);
   int occ = 0;
-  e = qtt::dmma_occupancy(KB, NB, smem, &occ);
+  e = qtt::dmma_occupancy(sp.KB, sp.NB, sp.smem, &occ);
   if (e != cudaSuccess) return from_cuda(e);
-  L.variant = qtt::kDmma;
-  L.KB = KB;
-  L.NB = NB;
-  L.rep = rep;
-  L.stages = stages;
-  L.smem = smem;
-  L.ctas_per_sm = std::max(1, occ);
-  std::vector<double> pk = pack_dmma(G, r_in, r_out, KB, NB, RP);
-  e = cudaMalloc(&L.d_bpack, pk.size() * sizeof(double));
+  S.ctas_per_sm = std::max(1, occ);
+  std::vector<double> pk;
+  if (sp.k0 == sp.k1) {
+    pk = pack_dmma(cores[sp.k0 - 1], sp);
+  } else {
+    const std::vector<double> W = super_core(cores, h->ranks.data(), sp.k0, sp.k1);
+    pk = pack_dmma(W.data(), sp);
+  }
+  e = cudaMalloc(&S.d_bpack, pk.size() * sizeof(double));
   if (e != cudaSuccess) return from_cuda(e);
-  e = cudaMemcpy(L.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice);
-  return from_cuda(e);
+  return from_cuda(cudaMemcpy(S.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice));
 }
 
 qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st) {
-  const int64_t half = h->N / 2;
   unsigned char* base = static_cast<unsigned char*>(ws);
   int* counters = reinterpret_cast<int*>(base);
   const size_t bb = ws_buf_bytes(h, nrhs);
@@ -205,39 +213,43 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
   cudaError_t me = cudaMemsetAsync(counters, 0, kWsHeader, st);
   if (me != cudaSuccess) return from_cuda(me);
   const double* in = x;
-  for (int k = 0; k < h->d; ++k) {
-    const Level& L = h->levels[k];
-    double* out = (k == h->d - 1) ? y : buf[k & 1];
+  const int ns = int(h->stages.size());
+  for (int si = 0; si < ns; ++si) {
+    const Stage& S = h->stages[si];
+    const qtt::StagePlan& sp = S.plan;
+    double* out = (si == ns - 1) ? y : buf[si & 1];
+    const int L = sp.k1 - sp.k0 + 1;
     LevelArgs a;
     a.in = in;
     a.out = out;
-    a.bpack = L.d_bpack;
-    a.core = L.d_core;
-    a.M = nrhs * half;
-    a.half = half;
-    a.log2_half = h->d - 1;
-    a.tile_counter = counters + k;
-    a.r_in = L.r_in;
-    a.r_out = L.r_out;
-    a.RP = L.RP;
-    a.K = 2 * L.r_in;
-    a.KB = L.KB;
-    a.NB = L.NB;
-    a.rep = L.rep;
-    a.stages = L.stages;
-    a.smem = L.smem;
+    a.bpack = S.d_bpack;
+    a.core = S.d_core;
+    a.n_i = sp.n_i;
+    a.log2_q = h->d - L;
+    a.q = int64_t(1) << a.log2_q;
+    a.M = nrhs * a.q;
+    a.tile_counter = counters + si;
+    a.r_in = sp.r_in;
+    a.r_out = sp.r_out;
+    a.RP = sp.RP;
+    a.K = sp.K;
+    a.KB = sp.KB;
+    a.NB = sp.NB;
+    a.rep = sp.rep;
+    a.stages = sp.stages;
+    a.smem = sp.smem;
     StageEvents ev{};
     if (h->timing) {
-      ev.stage = k;
+      ev.stage = si;
       if (cudaEventCreate(&ev.start) != cudaSuccess || cudaEventCreate(&ev.stop) != cudaSuccess)
         return QTT_ERROR_CUDA;
       cudaEventRecord(ev.start, st);
     }
     cudaError_t e;
-    if (L.variant == qtt::kDmma) {
-      const int64_t rows_per_stage = int64_t(qtt::kDmmaRowsPerSubtile) * L.rep;
+    if (sp.variant != qtt::kGeneric) {
+      const int64_t rows_per_stage = int64_t(qtt::kDmmaRowsPerSubtile) * sp.rep;
       const int64_t tiles = (a.M + rows_per_stage - 1) / rows_per_stage;
-      a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms) * L.ctas_per_sm));
+      a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms) * S.ctas_per_sm));
       e = qtt::launch_level_dmma(a, st);
     } else {
       e = qtt::launch_level_generic(a, st, h->num_sms);
@@ -281,9 +293,14 @@ const char* qtt_status_string(qtt_status_t s) {
 }
 
 qtt_status_t qtt_create(qtt_handle_t* out, int d, const int64_t* ranks, const double* const* cores) {
+  return qtt_create_ex(out, d, ranks, cores, qtt::kMaxStageLevels);
+}
+
+qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks, const double* const* cores,
+                           int max_stage_levels) {
   if (!out) return QTT_ERROR_INVALID_VALUE;
   *out = nullptr;
-  if (d < 1 || d > 30 || !ranks || !cores) return QTT_ERROR_INVALID_VALUE;
+  if (d < 1 || d > 30 || !ranks || !cores || max_stage_levels < 1) return QTT_ERROR_INVALID_VALUE;
   if (ranks[0] != 1 || ranks[d] != 1) return QTT_ERROR_INVALID_VALUE;
   for (int k = 0; k <= d; ++k)
     if (ranks[k] < 1 || ranks[k] > 4096) return QTT_ERROR_INVALID_VALUE;
@@ -314,15 +331,16 @@ qtt_status_t qtt_create(qtt_handle_t* out, int d, const int64_t* ranks, const do
   h->d = d;
   h->N = int64_t(1) << d;
   h->ranks.assign(ranks, ranks + d + 1);
-  for (int k = 1; k < d; ++k) h->max_interior_rank = std::max<int64_t>(h->max_interior_rank, ranks[k]);
   qtt_status_t st = QTT_SUCCESS;
   try {
-    h->levels.resize(d);
-    for (int k = 0; k < d && st == QTT_SUCCESS; ++k) {
-      h->levels[k].r_in = int(ranks[k]);
-      h->levels[k].r_out = int(ranks[k + 1]);
-      st = plan_level(h, h->levels[k], cores[k]);
+    const std::vector<qtt::StagePlan> plan = qtt::plan_stages(d, ranks, h->smem_optin, max_stage_levels);
+    h->stages.resize(plan.size());
+    for (size_t s = 0; s < plan.size(); ++s) {
+      h->stages[s].plan = plan[s];
+      // the intermediate buffers hold only stage-boundary ranks
+      if (s + 1 < plan.size()) h->max_interior_rank = std::max<int64_t>(h->max_interior_rank, plan[s].r_out);
     }
+    for (size_t s = 0; s < plan.size() && st == QTT_SUCCESS; ++s) st = upload_stage(h, h->stages[s], cores);
   } catch (const std::bad_alloc&) {
     st = QTT_ERROR_OUT_OF_MEMORY;
   }
@@ -333,7 +351,7 @@ qtt_status_t qtt_create(qtt_handle_t* out, int d, const int64_t* ranks, const do
     free_plan(h);
     return st;
   }
-  h->stage_ms.assign(d, 0.0);
+  h->stage_ms.assign(h->stages.size(), 0.0);
   *out = h;
   return QTT_SUCCESS;
 }
@@ -428,15 +446,15 @@ qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank,
     for (int k = 0; k < h->d; ++k) s += double(h->ranks[k]) * double(h->ranks[k + 1]);
     *flops_per_rhs = 4.0 * s * double(h->N);
   }
-  if (launches_per_apply) *launches_per_apply = h->d;
+  if (launches_per_apply) *launches_per_apply = int(h->stages.size());
   return QTT_SUCCESS;
 }
 
 qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int* variant) {
-  if (!h || s < 0 || s >= h->d) return QTT_ERROR_INVALID_VALUE;
-  if (k_first) *k_first = s + 1;
-  if (k_last) *k_last = s + 1;
-  if (variant) *variant = h->levels[s].variant;
+  if (!h || s < 0 || s >= int(h->stages.size())) return QTT_ERROR_INVALID_VALUE;
+  if (k_first) *k_first = h->stages[s].plan.k0;
+  if (k_last) *k_last = h->stages[s].plan.k1;
+  if (variant) *variant = h->stages[s].plan.variant;
   return QTT_SUCCESS;
 }
 
@@ -460,7 +478,7 @@ qtt_status_t qtt_stage_times(qtt_handle_t h, float* ms, int n_stages, int* n_app
   }
   h->pending.clear();
   if (ms)
-    for (int s = 0; s < n_stages && s < h->d; ++s) ms[s] = float(h->stage_ms[s]);
+    for (int s = 0; s < n_stages && s < int(h->stages.size()); ++s) ms[s] = float(h->stage_ms[s]);
   if (n_applies) *n_applies = h->timed_applies;
   std::fill(h->stage_ms.begin(), h->stage_ms.end(), 0.0);
   h->timed_applies = 0;

@@ -1,42 +1,64 @@
-// Internal interface between the host planner (qtt_api.cpp) and the kernel
-// translation units.  Not part of the public ABI (see include/qtt.h).
+// Internal interface between the host planner (qtt_api.cpp, qtt_plan.cpp) and
+// the kernel translation units.  Not part of the public ABI (see include/qtt.h).
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <vector>
+
 #include <cuda_runtime.h>
+#ifdef __CUDACC__
+#define QTT_HD __host__ __device__
+#else
+#define QTT_HD
+#endif
 
 namespace qtt {
 
 // Kernel variants (also reported through qtt_get_stage).
-enum Variant : int { kGeneric = 0, kDmma = 1, kFused = 2 };
+//   kGeneric : one thread per output element, any rank, one level per launch.
+//   kDmma    : one level per launch on the FP64 tensor cores (DMMA).
+//   kMerged  : L >= 2 consecutive levels whose cores were contracted into one
+//              super-core at create time, applied as ONE DMMA GEMM per launch;
+//              the level intermediates never exist.
+enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2 };
 
-// Largest ranks the DMMA level kernel is instantiated for: K = 2 r_in <= 16*kMaxKB,
-// 2 * roundup(r_out, 2) <= 8*kMaxNB.
-constexpr int kMaxKB = 6;
-constexpr int kMaxNB = 12;
+// DMMA kernel instances: K = n_i * r_in <= 16*KB, n_i * roundup(r_out, 2) <= 8*NB.
+constexpr int kMaxKB = 8;
+constexpr int kMaxNB = 16;
+QTT_HD constexpr bool dmma_instantiated(int KB, int NB) {
+  return KB >= 1 && NB >= 1 &&
+         ((KB <= 6 && NB <= 12) || (KB <= 8 && NB <= 8) || (KB <= 4 && NB <= 16));
+}
 constexpr int kDmmaRowGroups = 4;                // 4 x 16 rows = one 64-row sub-tile
 constexpr int kDmmaRowsPerSubtile = 16 * kDmmaRowGroups;
-// Column groups of consumer warps for a level with NB n8-blocks: 2-3 warps per
-// SM sub-partition for the wide levels, fewer for narrow (memory-bound) ones.
-__host__ __device__ constexpr int dmma_col_groups(int NB) { return NB >= 9 ? 3 : (NB >= 2 ? 2 : 1); }
-__host__ __device__ constexpr int dmma_threads(int NB) { return (kDmmaRowGroups * dmma_col_groups(NB) + 1) * 32; }
+// Column groups of consumer warps for a stage with NB n8-blocks: 2-3 warps per
+// SM sub-partition for the wide stages, fewer for narrow (memory-bound) ones.
+QTT_HD constexpr int dmma_col_groups(int NB) { return NB >= 9 ? 3 : (NB >= 2 ? 2 : 1); }
+QTT_HD constexpr int dmma_threads(int NB) { return (kDmmaRowGroups * dmma_col_groups(NB) + 1) * 32; }
 constexpr int kMaxStages = 8;
+constexpr int kBarBytes = 256;   // full[8] + empty[8] mbarriers + tile_id[8]
+constexpr int kMaxStageLevels = 6;   // most levels one merged stage may cover
 
-// One level (= one core, PAPER Alg. 2 lines 5-8) as a GEMM over the rotating
-// layout:  out[(m + half*(s+i)) * r_out + b] = sum_{j,a} G[a,i,j,b] * in[(2m+j) * r_in + a]
-// for rows m < M = nrhs * N/2, s = m / half.
+// One stage (L consecutive levels k0..k0+L-1, n_i = 2^L) as a GEMM over the
+// rotating layout (PAPER Alg. 2 lines 5-8 applied L times):
+//   row m < M = nrhs * N / n_i of the A operand = the n_i * r_in contiguous
+//   doubles at in + m * n_i * r_in  (input rows n_i*m .. n_i*m + n_i - 1);
+//   out[(m + Q*(s*(n_i-1) + ii)) * r_out + b] = sum_{jj,a} W[a,ii,jj,b] * A[m][jj*r_in + a]
+// with Q = N / n_i, s = m / Q (the RHS), W the stage's super-core.  L = 1 is
+// one level of Alg. 2 (W = G_k): out row m + (N/2)(s + i_k).
 struct LevelArgs {
   const double* in = nullptr;
   double* out = nullptr;
   const double* bpack = nullptr;   // DMMA: packed B fragments (KB*NB*32 double4)
   const double* core = nullptr;    // generic: raw core [a][i][j][b]
-  int64_t M = 0;                   // GEMM rows: nrhs * N / 2
-  int64_t half = 0;                // N / 2
-  int log2_half = 0;               // half = 2^log2_half
+  int64_t M = 0;                   // GEMM rows: nrhs * N / n_i
+  int64_t q = 0;                   // Q = N / n_i
+  int log2_q = 0;                  // Q = 2^log2_q
+  int n_i = 2;                     // 2^L output (and input) digit combinations
   int* tile_counter = nullptr;     // zeroed before the launch; dynamic tile scheduler
   int r_in = 0, r_out = 0;
-  int RP = 0;                      // r_out rounded up to even (column padding per half)
-  int K = 0;                       // 2 * r_in
+  int RP = 0;                      // r_out rounded up to even (column padding per ii block)
+  int K = 0;                       // n_i * r_in
   int KB = 0, NB = 0;              // k16 / n8 fragment blocks
   int rep = 1;                     // 64-row sub-tiles per TMA stage
   int stages = 2;                  // TMA pipeline depth
@@ -44,7 +66,22 @@ struct LevelArgs {
   size_t smem = 0;
 };
 
+// Host-side stage plan (qtt_plan.cpp): pure function of the rank profile and
+// device limits, no CUDA calls.
+struct StagePlan {
+  int k0 = 1, k1 = 1;              // 1-based levels covered
+  int variant = kGeneric;
+  int r_in = 0, r_out = 0, n_i = 2;
+  int K = 0, KB = 0, NB = 0, RP = 0, rep = 1, stages = 2;
+  size_t smem = 0;
+  double est_seconds = 0;          // cost-model estimate at nrhs = 1
+};
+
 size_t dmma_smem_bytes(int KB, int NB, int K, int rep, int stages);
+// Tiling of a DMMA stage; false if it does not fit smem_optin.
+bool dmma_tiling(int K, int KB, int NB, size_t smem_optin, int* rep, int* stages, size_t* smem);
+std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels);
+
 cudaError_t dmma_prepare(int KB, int NB, size_t smem);   // sets the max dynamic smem attribute
 cudaError_t dmma_occupancy(int KB, int NB, size_t smem, int* ctas_per_sm);
 cudaError_t launch_level_dmma(const LevelArgs& a, cudaStream_t st);

@@ -1,0 +1,147 @@
+// Stage scheduler keyed on the rank profile and the
+// super-core contraction of merged stages.  Pure host code: no CUDA calls, so
+// the planner is testable without a GPU through qtt_plan_stages (include/qtt.h).
+//
+// PAPER.md Alg. 2 runs the levels k = 1..d strictly in order;
+// each level reads the N*r_{k-1} intermediate and writes the N*r_k one.  A
+// stage of L consecutive levels k0..k1 is applied here as ONE GEMM with the
+// super-core
+//   W[a][ii][jj][b] = sum_{bonds} G_k0[a,i_1,j_1,:] G_k0+1[:,i_2,j_2,:] ... G_k1[:,i_L,j_L,b]
+//   ii = sum_l i_l 2^{l-1},  jj = sum_l j_l 2^{l-1}
+// (the definition of the QTT matrix, Eq. TTdeccores P:519-523 with the
+// operator pairing P:953-962, restricted to the stage's digits), so the
+// intermediates inside the stage never exist.  Per element of N the GEMM does
+// 2^(L+1) r_in r_out flops (a multiply-add counted as 2) against Alg. 2's
+// 4 * sum_l r_{l-1} r_l: cheaper at the tapered ends of a rank
+// profile (r_0 = r_d = 1), equal for L = 2 at constant rank, dearer for L >= 3
+// at constant rank -- the planner weighs exactly that against the HBM bytes
+// the merge removes.
+#include "../../include/qtt.h"
+#include "qtt_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <vector>
+
+namespace qtt {
+
+namespace {
+
+// Cost model of one B200 (148 SMs, 1965 MHz): DMMA 148*64 FMA/clk, HBM copy
+// bandwidth as measured in MEASURED_PEAKS.json (~6.5 TB/s), launch ~3 us.
+constexpr double kFp64 = 37.2e12 * 0.95;
+constexpr double kHbm = 6.45e12 * 0.90;
+constexpr double kLaunch = 3.0e-6;
+constexpr double kSms = 148;
+
+uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+size_t dmma_smem_bytes(int KB, int NB, int K, int rep, int stages) {
+  const size_t stage = round_up(uint32_t(kDmmaRowsPerSubtile * rep) * uint32_t(K) * 8u, 128u);
+  return kBarBytes + size_t(KB) * NB * 32 * 32 + stage * stages;
+}
+
+bool dmma_tiling(int K, int KB, int NB, size_t smem_optin, int* rep_out, int* stages_out, size_t* smem_out) {
+  if (!dmma_instantiated(KB, NB)) return false;
+  // TMA stage: >= 16 KiB per stage (HBM bytes in flight), <= 64 KiB.
+  const size_t sub_bytes = size_t(kDmmaRowsPerSubtile) * K * 8;
+  int rep = int(std::max<size_t>(1, (16384 + sub_bytes - 1) / sub_bytes));
+  while (rep > 1 && sub_bytes * rep > 65536) --rep;
+  for (int stages = kMaxStages; stages >= 2; --stages) {
+    const size_t smem = dmma_smem_bytes(KB, NB, K, rep, stages);
+    if (smem <= smem_optin) {
+      *rep_out = rep;
+      *stages_out = stages;
+      *smem_out = smem;
+      return true;
+    }
+  }
+  return false;
+}
+
+// Shape and estimated time of a stage k0..k1 (1-based), or false if no kernel
+// instance covers it.  Estimates are at N = n, nrhs = 1.
+static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t smem_optin, StagePlan* sp) {
+  const int L = k1 - k0 + 1;
+  const int n_i = 1 << L;
+  const int r_in = int(ranks[k0 - 1]), r_out = int(ranks[k1]);
+  sp->k0 = k0;
+  sp->k1 = k1;
+  sp->r_in = r_in;
+  sp->r_out = r_out;
+  sp->n_i = n_i;
+  sp->K = n_i * r_in;
+  sp->RP = (r_out + 1) / 2 * 2;
+  sp->KB = (sp->K + 15) / 16;
+  sp->NB = (n_i * sp->RP + 7) / 8;
+  const double M = double(n) / n_i;
+  const double bytes = 8.0 * double(n) * (r_in + r_out);
+  if (dmma_tiling(sp->K, sp->KB, sp->NB, smem_optin, &sp->rep, &sp->stages, &sp->smem)) {
+    sp->variant = L == 1 ? kDmma : kMerged;
+    const double flops = 2.0 * M * 16.0 * sp->KB * 8.0 * sp->NB;   // padded tensor-pipe work
+    const double tiles = std::ceil(M / (kDmmaRowsPerSubtile * sp->rep));
+    const double u = std::min(1.0, tiles / kSms);                   // fraction of SMs busy
+    sp->est_seconds = std::max(flops / (kFp64 * u), bytes / (kHbm * u)) + kLaunch;
+    return true;
+  }
+  if (L != 1) return false;
+  sp->variant = kGeneric;   // any rank, one thread per output element
+  const double flops = 4.0 * double(r_in) * r_out * double(n);
+  sp->est_seconds = std::max(flops / (kFp64 * 0.05), bytes / (kHbm * 0.5)) + kLaunch;
+  return true;
+}
+
+// Dynamic programme over the level sequence: best[k] = min over the last
+// stage [k0, k] of best[k0-1] + est(k0..k).  The estimate scales with N; for
+// the plan only the relative cost of flops, bytes and launches matters, and
+// the launch term is what keeps small-N problems (c1, c2) from being cut
+// into many launches, so N is the real N.
+std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels) {
+  const int64_t n = int64_t(1) << d;
+  const int maxL = std::max(1, std::min(max_stage_levels, kMaxStageLevels));
+  std::vector<double> best(d + 1, std::numeric_limits<double>::infinity());
+  std::vector<StagePlan> choice(d + 1);
+  best[0] = 0;
+  for (int k = 1; k <= d; ++k) {
+    for (int L = 1; L <= std::min(maxL, k); ++L) {
+      StagePlan sp;
+      if (!stage_shape(ranks, k - L + 1, k, n, smem_optin, &sp)) continue;
+      const double c = best[k - L] + sp.est_seconds;
+      if (c < best[k]) {
+        best[k] = c;
+        choice[k] = sp;
+      }
+    }
+  }
+  std::vector<StagePlan> out;
+  for (int k = d; k > 0; k = choice[k].k0 - 1) out.push_back(choice[k]);
+  std::reverse(out.begin(), out.end());
+  return out;
+}
+
+}  // namespace qtt
+
+extern "C" qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
+                                        int* n_stages, int* k_first, int* k_last, int* variant) {
+  if (d < 1 || d > 30 || !ranks || !n_stages || max_stage_levels < 1) return QTT_ERROR_INVALID_VALUE;
+  if (ranks[0] != 1 || ranks[d] != 1) return QTT_ERROR_INVALID_VALUE;
+  for (int k = 0; k <= d; ++k)
+    if (ranks[k] < 1 || ranks[k] > 4096) return QTT_ERROR_INVALID_VALUE;
+  if (smem_optin == 0) smem_optin = 232448;   // B200 cudaDevAttrMaxSharedMemoryPerBlockOptin
+  try {
+    const std::vector<qtt::StagePlan> p = qtt::plan_stages(d, ranks, smem_optin, max_stage_levels);
+    *n_stages = int(p.size());
+    for (size_t s = 0; s < p.size(); ++s) {
+      if (k_first) k_first[s] = p[s].k0;
+      if (k_last) k_last[s] = p[s].k1;
+      if (variant) variant[s] = p[s].variant;
+    }
+  } catch (...) {
+    return QTT_ERROR_OUT_OF_MEMORY;
+  }
+  return QTT_SUCCESS;
+}

@@ -25,8 +25,8 @@ def qtt():
     return q
 
 
-def gpu_apply(q, cores, x, **kw):
-    op = q.QttOperator(cores)
+def gpu_apply(q, cores, x, max_stage_levels=None, **kw):
+    op = q.QttOperator(cores, max_stage_levels=max_stage_levels)
     try:
         xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
         y = op.apply(xt, **kw)
@@ -96,19 +96,58 @@ def test_constant_rank_sweep(qtt, r):
     assert all(s["variant"] != "generic" for s in stages), stages
 
 
-def test_generic_path_large_rank(qtt):
-    ranks = [1, 2, 4, 70, 70, 4, 2, 1]
-    _, cores, x = random_case(77, 7, 70, 1, ranks=ranks)
-    y, stages = gpu_apply(qtt, cores, x)
-    assert any(s["variant"] == "generic" for s in stages)
+@pytest.mark.parametrize("maxL", [1, 6])
+def test_generic_path_large_rank(qtt, maxL):
+    ranks = [1, 2, 4, 70, 70, 70, 4, 2, 1]
+    _, cores, x = random_case(77, 8, 70, 2, ranks=ranks)
+    y, stages = gpu_apply(qtt, cores, x, max_stage_levels=maxL)
+    if maxL == 1:
+        assert any(s["variant"] == "generic" for s in stages)
     oracle.assert_close(y, oracle.apply_alg2(cores, x))
 
 
+# ------------------------------------------------------------------ merged stages (super-cores)
+@pytest.mark.parametrize("maxL", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("seed,d,maxr,nrhs", [(21, 10, 6, 3), (22, 13, 12, 2), (23, 15, 24, 1), (24, 9, 3, 7)])
+def test_merged_stage_limits(qtt, maxL, seed, d, maxr, nrhs):
+    """Every cap on the stage length gives the oracle's result (multi-RHS
+    epilogue of merged stages included)."""
+    ranks, cores, x = random_case(seed, d, maxr, nrhs)
+    y, stages = gpu_apply(qtt, cores, x, max_stage_levels=maxL)
+    assert all(s["k_last"] - s["k_first"] + 1 <= maxL for s in stages)
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_config_plan_has_merged_stages(qtt, name):
+    cfg, cores, _ = generate(name, with_x=False)
+    op = qtt.QttOperator(cores)
+    try:
+        st = op.stages()
+    finally:
+        op.close()
+    assert any(s["variant"] == "merged" for s in st)
+    assert st == qtt.plan_stages(cfg.ranks)
+
+
+def test_merged_closed_forms(qtt):
+    """Merged stages on the exact closed forms: identity and shift stay bitwise."""
+    d = 14
+    x = np.random.default_rng(4).standard_normal((3, 1 << d))
+    for maxL in (2, 5, 6):
+        y, st = gpu_apply(qtt, CF.identity_cores(d), x, max_stage_levels=maxL)
+        assert any(s["variant"] == "merged" for s in st)
+        np.testing.assert_array_equal(y, x)
+        y, _ = gpu_apply(qtt, CF.shift_cores(d, 777), x, max_stage_levels=maxL)
+        np.testing.assert_array_equal(y, np.roll(x, 777, axis=1))
+
+
 # ------------------------------------------------------------------ BASELINE configs
+@pytest.mark.parametrize("maxL", [1, None])
 @pytest.mark.parametrize("name", ["c1", "c2", "c3"])
-def test_config_full_vector(qtt, name):
+def test_config_full_vector(qtt, name, maxL):
     cfg, cores, x = generate(name)
-    y, _ = gpu_apply(qtt, cores, x)
+    y, _ = gpu_apply(qtt, cores, x, max_stage_levels=maxL)
     ref = oracle.apply_alg2(cores, x)
     oracle.assert_close(y, ref)
     if name == "c1":

@@ -1,0 +1,83 @@
+"""Stage scheduler (host logic, no GPU): qtt_plan_stages through the C ABI.
+
+A stage is a run of consecutive levels applied by one launch; L >= 2 levels
+use the super-core (the QTT definition, PAPER Eq. TTdeccores P:519-523,
+restricted to the stage's digits).  These tests check the schedule's
+structure; its numerics are checked on the GPU (tests/test_gpu_parity.py).
+"""
+import pytest
+
+from qtt_workload import configs
+
+
+@pytest.fixture(scope="module")
+def q():
+    from paper_1511_06029_b200 import build
+    build.build()
+    import paper_1511_06029_b200 as q
+    q._lib.load()
+    return q
+
+
+def check_cover(plan, d, max_levels):
+    assert plan[0][0] == 1 and plan[-1][1] == d
+    for (a0, b0, _), (a1, _, _) in zip(plan, plan[1:]):
+        assert a1 == b0 + 1
+    for a, b, v in plan:
+        assert 1 <= b - a + 1 <= max_levels
+        assert v in (0, 1, 2)
+        assert (v == 2) == (b > a)          # merged <=> more than one level
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("maxL", [1, 2, 3, 6])
+def test_plan_covers_levels(q, name, maxL):
+    cfg = configs.make_config(name)
+    plan = q.qtt_plan_stages(cfg.ranks, 0, maxL)
+    check_cover(plan, cfg.d, maxL)
+    if maxL == 1:
+        assert len(plan) == cfg.d and all(v == 1 for _, _, v in plan)
+
+
+def test_c4_plan_merges_tapered_ends_only(q):
+    """c4 (r_k = min(2^k, 2^(24-k), 48)): the r=48 interior levels stay one per
+    launch (a merge there would cost more flops or exceed the instance set);
+    the tapered ends are merged, which removes HBM round trips and flops."""
+    cfg = configs.make_config("c4")
+    plan = q.qtt_plan_stages(cfg.ranks)
+    for a, b, v in plan:
+        if 7 <= a <= 18:
+            assert a == b and v == 1
+    assert plan[0][1] >= 2 and plan[-1][0] <= 23
+    assert len(plan) < cfg.d
+
+
+def test_small_problem_few_launches(q):
+    # c1 (N = 4096) is latency-bound: the plan uses far fewer launches than levels
+    cfg = configs.make_config("c1")
+    assert len(q.qtt_plan_stages(cfg.ranks)) <= cfg.d // 2
+
+
+def test_large_rank_uses_generic_when_unmerged(q):
+    ranks = [1, 2, 4] + [70] * 6 + [4, 2, 1]
+    plan = q.qtt_plan_stages(ranks, 0, 1)
+    assert [v for _, _, v in plan] == [1, 1] + [0] * 7 + [1, 1]
+    check_cover(q.qtt_plan_stages(ranks), len(ranks) - 1, 6)
+
+
+def test_rank_one_and_d1(q):
+    assert q.qtt_plan_stages([1, 1]) == [(1, 1, 1)]
+    plan = q.qtt_plan_stages([1] * 11)
+    check_cover(plan, 10, 6)
+
+
+def test_plan_validation(q):
+    from paper_1511_06029_b200 import QttError
+    with pytest.raises(QttError):
+        q.qtt_plan_stages([2, 1])
+    with pytest.raises(QttError):
+        q.qtt_plan_stages([1, 0, 1])
+    with pytest.raises(QttError):
+        q.qtt_plan_stages([1, 2, 1], 0, 0)
+    with pytest.raises(QttError):
+        q.qtt_plan_stages([1] * 32)

@@ -85,6 +85,43 @@ __global__ void dmma_burn(double* out, int iters) {
   if (s == 12345.678) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+
+// Mixed probe: even warps issue DMMA m8n8k4 chains, odd warps DFMA chains, in
+// the same CTAs.  If DMMA and DFMA run on separate units the combined rate
+// exceeds either alone; if they share the FP64 pipe it does not.
+__global__ void mixed_burn(double* out, int dmma_iters, int dfma_iters, double fa, double fb) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0;
+  if ((warp & 1) == 0) {
+    double a = 1e-3 * threadIdx.x, b = 1e-3 * (threadIdx.x + 1);
+    double d[8][2];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) d[c][0] = d[c][1] = 0.0;
+    for (int it = 0; it < dmma_iters; ++it) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(d[c][0]), "+d"(d[c][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s += d[c][0] + d[c][1];
+  } else {
+    double acc[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) acc[c] = threadIdx.x * 1e-9 + c;
+    for (int it = 0; it < dfma_iters; ++it) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) acc[c] = fma(acc[c], fa, fb);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += acc[c];
+  }
+  if (s == 12345.678) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void copy_f64(const double2* __restrict__ in, double2* __restrict__ out, size_t n2) {
   size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -146,6 +183,19 @@ int main() {
       double flops = 2.0 * mnk[s][0] * mnk[s][1] * mnk[s][2] * (double)NA * iters * (double)blocks * wpb;
       printf(" \"dmma_%s_w%d_tflops\": %.3f,\n", names[s], wpb, flops / ms * 1e-9);
     }
+  }
+  // mixed DMMA + DFMA (separate units or one FP64 pipe?)
+  for (int ratio : {1, 2, 4}) {
+    // per warp: DMMA warp does 8*dmma_iters m8n8k4 (512 flop each); DFMA warp does
+    // 64*dfma_iters fma per thread (64 flop per warp-instr pair... 2*32 per instr)
+    int blocks = sms * 4, threads = 32 * 16;
+    int dmma_iters = 2048, dfma_iters = 2048 * 8 * 512 / (64 * 2 * 32) / ratio;
+    float ms = time_ms([&] { mixed_burn<<<blocks, threads>>>(out, dmma_iters, dfma_iters, 0.999999, 1e-7); }, 5);
+    double warps = (double)blocks * 16 / 2;
+    double f_dmma = warps * dmma_iters * 8 * 512.0;
+    double f_dfma = warps * 32.0 * dfma_iters * 8 * kChains * 2.0;
+    printf(" \"mixed_r%d_total_tflops\": %.3f, \"mixed_r%d_dmma_share\": %.3f,\n", ratio,
+           (f_dmma + f_dfma) / ms * 1e-9, ratio, f_dmma / (f_dmma + f_dfma));
   }
   // copy
   {
