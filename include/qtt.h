@@ -75,7 +75,7 @@ qtt_status_t qtt_create(qtt_handle_t* out, int d, const int64_t* ranks,
 /*
  * qtt_create_ex -- qtt_create with the longest merged stage capped at
  * `max_stage_levels` levels (>= 1; 1 = one launch per level, i.e. PAPER
- * Alg. 2 executed level by level; qtt_create uses 6).  Otherwise identical.
+ * Alg. 2 executed level by level; qtt_create uses 10).  Otherwise identical.
  */
 qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks,
                            const double* const* cores, int max_stage_levels);

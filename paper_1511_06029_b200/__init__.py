@@ -27,8 +27,8 @@ __all__ = [
     "qtt_stage_times", "qtt_destroy", "qtt_status_string", "library_path", "SYMBOLS",
 ]
 
-VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "merged"}
-MAX_STAGE_LEVELS = 6
+VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "merged", 3: "wide"}
+MAX_STAGE_LEVELS = 10
 
 
 def library_path() -> str:

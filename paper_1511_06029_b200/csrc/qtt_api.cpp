@@ -139,6 +139,33 @@ std::vector<double> pack_dmma(const double* W, const qtt::StagePlan& sp) {
   return out;
 }
 
+// Super-core of a wide stage, streamed by k-chunk (qtt_wide_kernel.cu):
+//   pack[cb][ch][kb][nb][lane][v] = Bmat[ch*BK + kb*16 + 4*(lane%4) + v][(cb*NB + nb)*8 + lane/4]
+// with Bmat[jj*r_in + a][ii*r_out + b] = W[a,ii,jj,b] (no column padding per ii).
+std::vector<double> pack_wide(const double* W, const qtt::StagePlan& sp) {
+  const int NB = sp.NB, r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i;
+  const int nout = n_i * r_out;
+  const size_t chunk = size_t(qtt::kWideKBC) * NB * 32 * 4;
+  std::vector<double> out(size_t(sp.ncb) * sp.nchunks * chunk, 0.0);
+  for (int cb = 0; cb < sp.ncb; ++cb)
+    for (int ch = 0; ch < sp.nchunks; ++ch)
+      for (int kb = 0; kb < qtt::kWideKBC; ++kb)
+        for (int nb = 0; nb < NB; ++nb)
+          for (int lane = 0; lane < 32; ++lane)
+            for (int v = 0; v < 4; ++v) {
+              const int kk = ch * qtt::kWideBK + kb * 16 + 4 * (lane % 4) + v;
+              const int n = (cb * NB + nb) * 8 + lane / 4;
+              double val = 0.0;
+              if (kk < sp.K && n < nout) {
+                const int jj = kk / r_in, a = kk % r_in;
+                const int ii = n / r_out, b = n % r_out;
+                val = W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b];
+              }
+              out[(size_t(cb) * sp.nchunks + ch) * chunk + ((size_t(kb) * NB + nb) * 32 + lane) * 4 + v] = val;
+            }
+  return out;
+}
+
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -184,6 +211,16 @@ qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
     cudaError_t e = cudaMalloc(&S.d_core, core_elems * sizeof(double));
     if (e != cudaSuccess) return from_cuda(e);
     return from_cuda(cudaMemcpy(S.d_core, cores[sp.k0 - 1], core_elems * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (sp.variant == qtt::kWide) {
+    cudaError_t e = qtt::wide_prepare(sp.NB, h->smem_optin);
+    if (e != cudaSuccess) return from_cuda(e);
+    S.ctas_per_sm = 1;
+    const std::vector<double> W = super_core(cores, h->ranks.data(), sp.k0, sp.k1);
+    const std::vector<double> pk = pack_wide(W.data(), sp);
+    e = cudaMalloc(&S.d_bpack, pk.size() * sizeof(double));
+    if (e != cudaSuccess) return from_cuda(e);
+    return from_cuda(cudaMemcpy(S.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice));
   }
   // The attribute is per kernel instance and shared by every stage (and plan)
   // that uses it, so raise it to the device maximum rather than this stage's need.
@@ -245,8 +282,15 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
         return QTT_ERROR_CUDA;
       cudaEventRecord(ev.start, st);
     }
+    a.nchunks = sp.nchunks;
+    a.ncb = sp.ncb;
+    a.nout = sp.n_i * sp.r_out;
     cudaError_t e;
-    if (sp.variant != qtt::kGeneric) {
+    if (sp.variant == qtt::kWide) {
+      const int64_t tiles = (a.M + qtt::kDmmaRowsPerSubtile - 1) / qtt::kDmmaRowsPerSubtile * sp.ncb;
+      a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms)));
+      e = qtt::launch_wide(a, st);
+    } else if (sp.variant != qtt::kGeneric) {
       const int64_t rows_per_stage = int64_t(qtt::kDmmaRowsPerSubtile) * sp.rep;
       const int64_t tiles = (a.M + rows_per_stage - 1) / rows_per_stage;
       a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms) * S.ctas_per_sm));

@@ -20,7 +20,9 @@ namespace qtt {
 //   kMerged  : L >= 2 consecutive levels whose cores were contracted into one
 //              super-core at create time, applied as ONE DMMA GEMM per launch;
 //              the level intermediates never exist.
-enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2 };
+//   kWide    : a merged stage whose super-core is too large for shared memory:
+//              streamed from L2 in k-chunks next to the A tiles (qtt_wide_kernel.cu).
+enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2, kWide = 3 };
 
 // DMMA kernel instances: K = n_i * r_in <= 16*KB, n_i * roundup(r_out, 2) <= 8*NB.
 constexpr int kMaxKB = 8;
@@ -37,7 +39,16 @@ QTT_HD constexpr int dmma_col_groups(int NB) { return NB >= 9 ? 3 : (NB >= 2 ? 2
 QTT_HD constexpr int dmma_threads(int NB) { return (kDmmaRowGroups * dmma_col_groups(NB) + 1) * 32; }
 constexpr int kMaxStages = 8;
 constexpr int kBarBytes = 256;   // full[8] + empty[8] mbarriers + tile_id[8]
-constexpr int kMaxStageLevels = 6;   // most levels one merged stage may cover
+constexpr int kMaxStageLevels = 10;  // most levels one merged stage may cover
+
+// Wide (streamed super-core) kernel: 64-row tiles, BN = 8*NB columns per
+// column block, k-chunks of kWideBK; instances for NB in {4, 8, 12, 16}.
+constexpr int kWideKBC = 2;                  // k16 blocks per chunk
+constexpr int kWideBK = 16 * kWideKBC;       // 32
+constexpr int kWideSA = kWideBK + 2;         // padded smem row stride (doubles): conflict-free A fragments
+constexpr int kWideStages = 4;
+constexpr size_t kWideMaxCoreBytes = size_t(64) << 20;
+QTT_HD constexpr bool wide_instantiated(int NB) { return NB == 4 || NB == 8 || NB == 12 || NB == 16; }
 
 // One stage (L consecutive levels k0..k0+L-1, n_i = 2^L) as a GEMM over the
 // rotating layout (PAPER Alg. 2 lines 5-8 applied L times):
@@ -64,6 +75,10 @@ struct LevelArgs {
   int stages = 2;                  // TMA pipeline depth
   int grid = 0;
   size_t smem = 0;
+  // wide variant only
+  int nchunks = 1;                 // K / kWideBK
+  int ncb = 1;                     // column blocks of 8*NB columns
+  int nout = 0;                    // n_i * r_out real output columns (RP = r_out)
 };
 
 // Host-side stage plan (qtt_plan.cpp): pure function of the rank profile and
@@ -73,6 +88,7 @@ struct StagePlan {
   int variant = kGeneric;
   int r_in = 0, r_out = 0, n_i = 2;
   int K = 0, KB = 0, NB = 0, RP = 0, rep = 1, stages = 2;
+  int nchunks = 1, ncb = 1;        // wide variant
   size_t smem = 0;
   double est_seconds = 0;          // cost-model estimate at nrhs = 1
 };
@@ -86,5 +102,9 @@ cudaError_t dmma_prepare(int KB, int NB, size_t smem);   // sets the max dynamic
 cudaError_t dmma_occupancy(int KB, int NB, size_t smem, int* ctas_per_sm);
 cudaError_t launch_level_dmma(const LevelArgs& a, cudaStream_t st);
 cudaError_t launch_level_generic(const LevelArgs& a, cudaStream_t st, int num_sms);
+size_t wide_smem_bytes(int NB);
+QTT_HD constexpr int wide_threads(int NB) { return dmma_threads(NB); }
+cudaError_t wide_prepare(int NB, size_t smem);
+cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st);
 
 }  // namespace qtt

@@ -34,6 +34,8 @@ namespace {
 constexpr double kFp64 = 37.2e12 * 0.95;
 constexpr double kHbm = 6.45e12 * 0.90;
 constexpr double kLaunch = 3.0e-6;
+constexpr double kFp64Wide = 37.2e12 * 0.88;   // streamed super-core: some issue slots go to TMA
+constexpr double kL2 = 7.0e12;                   // L2 -> SM bytes the wide kernel may pull
 constexpr double kSms = 148;
 
 uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
@@ -80,14 +82,44 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
   sp->NB = (n_i * sp->RP + 7) / 8;
   const double M = double(n) / n_i;
   const double bytes = 8.0 * double(n) * (r_in + r_out);
+  bool ok = false;
   if (dmma_tiling(sp->K, sp->KB, sp->NB, smem_optin, &sp->rep, &sp->stages, &sp->smem)) {
     sp->variant = L == 1 ? kDmma : kMerged;
     const double flops = 2.0 * M * 16.0 * sp->KB * 8.0 * sp->NB;   // padded tensor-pipe work
     const double tiles = std::ceil(M / (kDmmaRowsPerSubtile * sp->rep));
     const double u = std::min(1.0, tiles / kSms);                   // fraction of SMs busy
     sp->est_seconds = std::max(flops / (kFp64 * u), bytes / (kHbm * u)) + kLaunch;
-    return true;
+    ok = true;
   }
+  // Wide variant: super-core streamed from L2 in k-chunks (qtt_wide_kernel.cu).
+  const int nout = n_i * r_out;
+  const double wbytes = 8.0 * sp->K * nout;
+  if (L >= 2 && sp->K % kWideBK == 0 && wbytes <= double(kWideMaxCoreBytes)) {
+    const int NBw = nout <= 32 ? 4 : nout <= 64 ? 8 : nout <= 96 ? 12 : 16;
+    const size_t smem = wide_smem_bytes(NBw);
+    if (smem <= smem_optin) {
+      const int ncb = (nout + 8 * NBw - 1) / (8 * NBw);
+      const double flops = 2.0 * M * sp->K * ncb * 8.0 * NBw;
+      const double tiles = std::ceil(M / kDmmaRowsPerSubtile) * ncb;
+      const double u = std::min(1.0, tiles / kSms);
+      const double l2 = tiles * (kDmmaRowsPerSubtile * 8.0 * sp->K + 8.0 * sp->K * 8.0 * NBw);
+      const double t = std::max({flops / (kFp64Wide * u), (bytes + wbytes) / (kHbm * u), l2 / kL2}) + kLaunch;
+      if (!ok || t < sp->est_seconds) {
+        sp->variant = kWide;
+        sp->NB = NBw;
+        sp->KB = kWideKBC;
+        sp->RP = r_out;
+        sp->ncb = ncb;
+        sp->nchunks = sp->K / kWideBK;
+        sp->rep = 1;
+        sp->stages = kWideStages;
+        sp->smem = smem;
+        sp->est_seconds = t;
+        ok = true;
+      }
+    }
+  }
+  if (ok) return true;
   if (L != 1) return false;
   sp->variant = kGeneric;   // any rank, one thread per output element
   const double flops = 4.0 * double(r_in) * r_out * double(n);

@@ -107,8 +107,9 @@ def test_generic_path_large_rank(qtt, maxL):
 
 
 # ------------------------------------------------------------------ merged stages (super-cores)
-@pytest.mark.parametrize("maxL", [1, 2, 3, 4, 6])
-@pytest.mark.parametrize("seed,d,maxr,nrhs", [(21, 10, 6, 3), (22, 13, 12, 2), (23, 15, 24, 1), (24, 9, 3, 7)])
+@pytest.mark.parametrize("maxL", [1, 2, 3, 4, 6, 10])
+@pytest.mark.parametrize("seed,d,maxr,nrhs", [(21, 10, 6, 3), (22, 13, 12, 2), (23, 15, 24, 1), (24, 9, 3, 7),
+                                              (25, 14, 40, 2)])
 def test_merged_stage_limits(qtt, maxL, seed, d, maxr, nrhs):
     """Every cap on the stage length gives the oracle's result (multi-RHS
     epilogue of merged stages included)."""
@@ -126,15 +127,37 @@ def test_config_plan_has_merged_stages(qtt, name):
         st = op.stages()
     finally:
         op.close()
-    assert any(s["variant"] == "merged" for s in st)
+    assert any(s["variant"] in ("merged", "wide") for s in st)
     assert st == qtt.plan_stages(cfg.ranks)
+
+
+WIDE_CASES = [
+    # ranks, nrhs: boundary stages whose super-core is streamed (variant "wide"),
+    # odd r_out (scalar epilogue), r_out = 1, ragged M (< 64 rows), multi-RHS
+    ([1, 2, 4, 8, 16, 32, 48, 48, 48, 32, 16, 8, 4, 2, 1], 1),
+    ([1, 2, 4, 8, 16, 32, 48, 48, 48, 32, 16, 8, 4, 2, 1], 3),
+    ([1, 2, 4, 8, 16, 24, 24, 24, 24, 24, 24, 24, 1], 2),
+    ([1] + [20] * 11 + [1], 1),
+    ([1] + [32] * 13 + [1], 2),
+    ([1, 2, 4, 8, 16, 17, 17, 17, 9, 5, 3, 1], 5),
+    ([1] + [40] * 9 + [1], 1),
+]
+
+
+@pytest.mark.parametrize("ranks,nrhs", WIDE_CASES)
+def test_wide_stages(qtt, ranks, nrhs):
+    d = len(ranks) - 1
+    _, cores, x = random_case(300 + d + nrhs, d, max(ranks), nrhs, ranks=ranks)
+    y, st = gpu_apply(qtt, cores, x)
+    assert any(s["variant"] == "wide" for s in st), st
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
 
 
 def test_merged_closed_forms(qtt):
     """Merged stages on the exact closed forms: identity and shift stay bitwise."""
     d = 14
     x = np.random.default_rng(4).standard_normal((3, 1 << d))
-    for maxL in (2, 5, 6):
+    for maxL in (2, 5, 6, 10):
         y, st = gpu_apply(qtt, CF.identity_cores(d), x, max_stage_levels=maxL)
         assert any(s["variant"] == "merged" for s in st)
         np.testing.assert_array_equal(y, x)

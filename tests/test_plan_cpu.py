@@ -25,12 +25,12 @@ def check_cover(plan, d, max_levels):
         assert a1 == b0 + 1
     for a, b, v in plan:
         assert 1 <= b - a + 1 <= max_levels
-        assert v in (0, 1, 2)
-        assert (v == 2) == (b > a)          # merged <=> more than one level
+        assert v in (0, 1, 2, 3)
+        assert (v in (2, 3)) == (b > a)     # merged / wide <=> more than one level
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
-@pytest.mark.parametrize("maxL", [1, 2, 3, 6])
+@pytest.mark.parametrize("maxL", [1, 2, 3, 6, 10])
 def test_plan_covers_levels(q, name, maxL):
     cfg = configs.make_config(name)
     plan = q.qtt_plan_stages(cfg.ranks, 0, maxL)
@@ -46,7 +46,7 @@ def test_c4_plan_merges_tapered_ends_only(q):
     cfg = configs.make_config("c4")
     plan = q.qtt_plan_stages(cfg.ranks)
     for a, b, v in plan:
-        if 7 <= a <= 18:
+        if 8 <= a <= 17:
             assert a == b and v == 1
     assert plan[0][1] >= 2 and plan[-1][0] <= 23
     assert len(plan) < cfg.d
@@ -62,13 +62,13 @@ def test_large_rank_uses_generic_when_unmerged(q):
     ranks = [1, 2, 4] + [70] * 6 + [4, 2, 1]
     plan = q.qtt_plan_stages(ranks, 0, 1)
     assert [v for _, _, v in plan] == [1, 1] + [0] * 7 + [1, 1]
-    check_cover(q.qtt_plan_stages(ranks), len(ranks) - 1, 6)
+    check_cover(q.qtt_plan_stages(ranks), len(ranks) - 1, 10)
 
 
 def test_rank_one_and_d1(q):
     assert q.qtt_plan_stages([1, 1]) == [(1, 1, 1)]
     plan = q.qtt_plan_stages([1] * 11)
-    check_cover(plan, 10, 6)
+    check_cover(plan, 10, 10)
 
 
 def test_plan_validation(q):
