@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -298,7 +300,12 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
     } else {
       e = qtt::launch_level_generic(a, st, h->num_sms);
     }
-    if (e != cudaSuccess) return from_cuda(e);
+    if (e != cudaSuccess) {
+      if (std::getenv("QTT_DEBUG"))
+        std::fprintf(stderr, "qtt: stage %d (levels %d-%d, variant %d, KB %d NB %d smem %zu grid %d) launch failed: %s\n",
+                     si, sp.k0, sp.k1, sp.variant, sp.KB, sp.NB, a.smem, a.grid, cudaGetErrorString(e));
+      return from_cuda(e);
+    }
     if (h->timing) {
       cudaEventRecord(ev.stop, st);
       h->pending.push_back(ev);

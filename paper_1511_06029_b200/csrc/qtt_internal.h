@@ -45,7 +45,6 @@ constexpr int kMaxStageLevels = 10;  // most levels one merged stage may cover
 // column block, k-chunks of kWideBK; instances for NB in {4, 8, 12, 16}.
 constexpr int kWideKBC = 2;                  // k16 blocks per chunk
 constexpr int kWideBK = 16 * kWideKBC;       // 32
-constexpr int kWideSA = kWideBK + 2;         // padded smem row stride (doubles): conflict-free A fragments
 constexpr int kWideStages = 4;
 constexpr size_t kWideMaxCoreBytes = size_t(64) << 20;
 QTT_HD constexpr bool wide_instantiated(int NB) { return NB == 4 || NB == 8 || NB == 12 || NB == 16; }

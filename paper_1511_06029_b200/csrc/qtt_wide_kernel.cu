@@ -14,18 +14,22 @@
 //   * tile = 64 rows x (8*NB) columns of C; a dynamic scheduler (atomicAdd)
 //     hands out tiles column-block-minor, so CTAs running at the same time
 //     share A row tiles in L2;
-//   * producer warp: per k-chunk of 32, the A chunk (64 row segments of 256 B,
-//     one cp.async.bulk each, issued by the 32 lanes, into rows padded to 34
-//     doubles so the A fragment loads are bank-conflict free) and the W chunk
-//     (one contiguous cp.async.bulk of fragment-packed doubles, 8-32 KiB,
-//     L2-resident across tiles) land in a 4-stage mbarrier ring;
+//   * producer warp: per k-chunk of 32, the A chunk (two 64 x 16 boxes of a
+//     2-D TMA tensor map over A, cp.async.bulk.tensor with the 128-byte
+//     swizzle, so the A fragment loads are bank-conflict free; rows past M are
+//     zero-filled by the TMA unit) and the W chunk (one contiguous
+//     cp.async.bulk of fragment-packed doubles, 8-32 KiB, L2-resident across
+//     tiles) land in a 4-stage mbarrier ring;
 //   * 4 x CG consumer warps accumulate over all k-chunks of a tile in
 //     registers (DMMA m8n8k4, as in qtt_dmma_kernel.cuh) and store with the
 //     row-separation epilogue of the stage (out row m + Q*(s*(2^L-1) + ii)).
 #include "qtt_dmma_kernel.cuh"
 
-#include <cstdint>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 namespace qtt {
 namespace wide {
@@ -34,35 +38,56 @@ namespace {
 using dmma::bulk_g2s;
 using dmma::dmma_884;
 using dmma::fence_mbar_init;
-using dmma::load_a16;
 using dmma::mbar_arrive;
 using dmma::mbar_arrive_expect_tx;
 using dmma::mbar_init;
 using dmma::mbar_wait;
 
-constexpr uint32_t kAStageBytes = uint32_t(kDmmaRowsPerSubtile) * kWideSA * 8;   // 17408
+// A chunk in smem: kWideKBC boxes of [64 rows][16 doubles] = 8 KiB each, 128-byte
+// swizzled (16-byte granule c of row r stored at granule c ^ (r % 8)).
+constexpr uint32_t kABoxBytes = uint32_t(kDmmaRowsPerSubtile) * 16 * 8;
+constexpr uint32_t kAStageBytes = kWideKBC * kABoxBytes;   // 16384
 __host__ __device__ constexpr uint32_t b_chunk_bytes(int NB) { return uint32_t(kWideKBC) * NB * 32 * 32; }
 __host__ __device__ constexpr uint32_t stage_bytes(int NB) { return kAStageBytes + b_chunk_bytes(NB); }
 
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dmma::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(dmma::smem_u32(bar))
+      : "memory");
+}
+
 // Accumulate one k-chunk (kWideKBC k16 blocks) into c: 16 rows x NBC n8-blocks.
+// A fragments come from a swizzled box: lane (g, t0) needs doubles
+// 4*t0 .. 4*t0+3 (16-byte granules 2*t0, 2*t0+1) of rows row0 and row0 + 8,
+// both congruent to g mod 8.  Operands are loaded one granule (two k4 steps)
+// at a time so that only half of the A and B fragments are live at once.
 template <int NB, int NBC>
-__device__ __forceinline__ void chunk_mma(double (&c)[NBC][4], const double* r0, const double* r1,
-                                          const double4* sB, int nb0, int lane) {
-  const int t0 = lane & 3;
+__device__ __forceinline__ void chunk_mma(double (&c)[NBC][4], const unsigned char* sA, int row0,
+                                          const double2* sB, int nb0, int lane) {
+  const int t0 = lane & 3, g = lane >> 2;
 #pragma unroll
   for (int kb = 0; kb < kWideKBC; ++kb) {
-    double a[8];
-    load_a16<true>(a, r0, r1, kb * 16 + 4 * t0, kWideBK);
-    double4 b[NBC];
+    const unsigned char* p0 = sA + kb * kABoxBytes + row0 * 128;
+    const unsigned char* p1 = p0 + 8 * 128;
 #pragma unroll
-    for (int nb = 0; nb < NBC; ++nb) b[nb] = sB[(kb * NB + nb0 + nb) * 32 + lane];
+    for (int half = 0; half < 2; ++half) {
+      const int off = ((2 * t0 + half) ^ g) * 16;
+      const double2 x = *reinterpret_cast<const double2*>(p0 + off);
+      const double2 y = *reinterpret_cast<const double2*>(p1 + off);
+      double2 b[NBC];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+      for (int nb = 0; nb < NBC; ++nb) b[nb] = sB[((kb * NB + nb0 + nb) * 32 + lane) * 2 + half];
 #pragma unroll
       for (int nb = 0; nb < NBC; ++nb) {
-        const double bq = q == 0 ? b[nb].x : q == 1 ? b[nb].y : q == 2 ? b[nb].z : b[nb].w;
-        dmma_884(c[nb][0], c[nb][1], a[2 * q], bq);
-        dmma_884(c[nb][2], c[nb][3], a[2 * q + 1], bq);
+        dmma_884(c[nb][0], c[nb][1], x.x, b[nb].x);
+        dmma_884(c[nb][2], c[nb][3], y.x, b[nb].x);
+      }
+#pragma unroll
+      for (int nb = 0; nb < NBC; ++nb) {
+        dmma_884(c[nb][0], c[nb][1], x.y, b[nb].y);
+        dmma_884(c[nb][2], c[nb][3], y.y, b[nb].y);
       }
     }
   }
@@ -76,28 +101,35 @@ __device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const Leve
   const int g = lane >> 2, t0 = lane & 3;
   const int r_out = p.r_out;
   const bool vec = (r_out % 2) == 0;
+  // (ii, b) of this lane's first column, then advanced by 8 columns per n-block
+  const int n_lane = n_first + 2 * t0;
+  const int ii_lane = n_lane / r_out;
+  const int b_lane = n_lane - ii_lane * r_out;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int64_t m = m_first + g + 8 * h;
     if (m >= p.M) continue;
     const int64_t rowbase = m + (((m >> p.log2_q) * (p.n_i - 1)) << p.log2_q);
+    int ii = ii_lane, b = b_lane;
 #pragma unroll
     for (int nb = 0; nb < NBC; ++nb) {
-      const int n = n_first + nb * 8 + 2 * t0;
-      if (n >= p.nout) continue;
-      const int ii = n / r_out;
-      const int b = n - ii * r_out;
-      double* dst = p.out + (rowbase + (int64_t(ii) << p.log2_q)) * r_out + b;
-      if (vec) {
-        *reinterpret_cast<double2*>(dst) = make_double2(c[nb][2 * h], c[nb][2 * h + 1]);
-      } else {
-        dst[0] = c[nb][2 * h];
-        const int n1 = n + 1;
-        if (n1 < p.nout) {
-          const int ii1 = n1 / r_out;
-          const int b1 = n1 - ii1 * r_out;
-          p.out[(rowbase + (int64_t(ii1) << p.log2_q)) * r_out + b1] = c[nb][2 * h + 1];
+      const int n = n_lane + nb * 8;
+      if (n < p.nout) {
+        double* dst = p.out + (rowbase + (int64_t(ii) << p.log2_q)) * r_out + b;
+        if (vec) {
+          *reinterpret_cast<double2*>(dst) = make_double2(c[nb][2 * h], c[nb][2 * h + 1]);
+        } else {
+          dst[0] = c[nb][2 * h];
+          if (n + 1 < p.nout) {
+            const bool wrap = (b + 1 == r_out);
+            p.out[(rowbase + (int64_t(ii + wrap) << p.log2_q)) * r_out + (wrap ? 0 : b + 1)] = c[nb][2 * h + 1];
+          }
         }
+      }
+      b += 8;
+      while (b >= r_out) {
+        b -= r_out;
+        ++ii;
       }
     }
   }
@@ -120,9 +152,7 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
       for (int nb = 0; nb < NBC; ++nb) c[nb][0] = c[nb][1] = c[nb][2] = c[nb][3] = 0.0;
     }
     const unsigned char* st = ring + size_t(s) * stage_bytes(NB);
-    const double* r0 = reinterpret_cast<const double*>(st) + size_t(rg * 16 + g) * kWideSA;
-    const double* r1 = r0 + 8 * kWideSA;
-    chunk_mma<NB, NBC>(c, r0, r1, reinterpret_cast<const double4*>(st + kAStageBytes), nb0, lane);
+    chunk_mma<NB, NBC>(c, st, rg * 16 + g, reinterpret_cast<const double2*>(st + kAStageBytes), nb0, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (++chunk == p.nchunks) {
@@ -135,7 +165,8 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
 }
 
 template <int NB>
-__global__ void __launch_bounds__(dmma_threads(NB), 1) wide_dmma_kernel(const LevelArgs p) {
+__global__ void __launch_bounds__(dmma_threads(NB), 1)
+wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   constexpr int CG = dmma_col_groups(NB);
   constexpr int CW = kDmmaRowGroups * CG;
   constexpr int NBW = (NB + CG - 1) / CG;
@@ -145,7 +176,9 @@ __global__ void __launch_bounds__(dmma_threads(NB), 1) wide_dmma_kernel(const Le
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
   int64_t* tile_id = reinterpret_cast<int64_t*>(empty + kMaxStages);
-  unsigned char* ring = smem + kBarBytes;
+  // the 128-byte swizzle needs 1024-byte aligned boxes
+  unsigned char* ring = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem) + kBarBytes + 1023) & ~uintptr_t(1023));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -159,43 +192,36 @@ __global__ void __launch_bounds__(dmma_threads(NB), 1) wide_dmma_kernel(const Le
   __syncthreads();
 
   if (warp == CW) {
-    // ---------------- producer warp: tile scheduler + TMA bulk loads ----------------
-    const int64_t M = p.M;
-    const int64_t K = p.K;
-    const int64_t ntiles = ((M + kDmmaRowsPerSubtile - 1) / kDmmaRowsPerSubtile) * p.ncb;
-    const uint32_t bbytes = b_chunk_bytes(NB);
-    int it = 0;
-    for (;;) {
-      int64_t t = 0;
-      if (lane == 0) t = atomicAdd(p.tile_counter, 1);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= ntiles) {
-        const int s = it % kWideStages;
-        mbar_wait(&empty[s], (uint32_t(it / kWideStages) & 1u) ^ 1u);
-        if (lane == 0) {
+    // ---------------- producer warp (one elected lane): tile scheduler + TMA loads ----------------
+    if (lane == 0) {
+      const int64_t M = p.M;
+      const int64_t ntiles = ((M + kDmmaRowsPerSubtile - 1) / kDmmaRowsPerSubtile) * p.ncb;
+      const uint32_t bbytes = b_chunk_bytes(NB);
+      int it = 0;
+      for (;;) {
+        const int64_t t = atomicAdd(p.tile_counter, 1);
+        if (t >= ntiles) {
+          const int s = it % kWideStages;
+          mbar_wait(&empty[s], (uint32_t(it / kWideStages) & 1u) ^ 1u);
           tile_id[s] = -1;
           mbar_arrive(&full[s]);
+          break;
         }
-        break;
-      }
-      const int64_t rt = t / p.ncb;
-      const int cb = int(t - rt * p.ncb);
-      const int64_t m0 = rt * kDmmaRowsPerSubtile;
-      const int rows = int((M - m0) < kDmmaRowsPerSubtile ? (M - m0) : kDmmaRowsPerSubtile);
-      const double* arow = p.in + m0 * K;
-      const double* bsrc = p.bpack + size_t(cb) * p.nchunks * (bbytes / 8);
-      for (int ch = 0; ch < p.nchunks; ++ch, ++it) {
-        const int s = it % kWideStages;
-        mbar_wait(&empty[s], (uint32_t(it / kWideStages) & 1u) ^ 1u);
-        unsigned char* st = ring + size_t(s) * stage_bytes(NB);
-        if (lane == 0) {
+        const int64_t rt = t / p.ncb;
+        const int cb = int(t - rt * p.ncb);
+        const int m0 = int(rt * kDmmaRowsPerSubtile);
+        const double* bsrc = p.bpack + size_t(cb) * p.nchunks * (bbytes / 8);
+        for (int ch = 0; ch < p.nchunks; ++ch, ++it) {
+          const int s = it % kWideStages;
+          mbar_wait(&empty[s], (uint32_t(it / kWideStages) & 1u) ^ 1u);
+          unsigned char* st = ring + size_t(s) * stage_bytes(NB);
           tile_id[s] = t;
-          mbar_arrive_expect_tx(&full[s], uint32_t(rows) * kWideBK * 8u + bbytes);
+          mbar_arrive_expect_tx(&full[s], kAStageBytes + bbytes);
+#pragma unroll
+          for (int kb = 0; kb < kWideKBC; ++kb)
+            tma_load_2d(st + kb * kABoxBytes, &tmA, ch * kWideBK + kb * 16, m0, &full[s]);
           bulk_g2s(st + kAStageBytes, bsrc + size_t(ch) * (bbytes / 8), bbytes, &full[s]);
         }
-        __syncwarp();
-        for (int r = lane; r < rows; r += 32)
-          bulk_g2s(st + size_t(r) * kWideSA * 8, arow + r * K + ch * kWideBK, kWideBK * 8, &full[s]);
       }
     }
     return;
@@ -211,7 +237,19 @@ __global__ void __launch_bounds__(dmma_threads(NB), 1) wide_dmma_kernel(const Le
   }
 }
 
-using KernelFn = void (*)(const LevelArgs);
+using KernelFn = void (*)(const LevelArgs, const CUtensorMap);
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
 
 KernelFn lookup(int NB) {
   switch (NB) {
@@ -226,7 +264,7 @@ KernelFn lookup(int NB) {
 }  // namespace
 }  // namespace wide
 
-size_t wide_smem_bytes(int NB) { return kBarBytes + size_t(kWideStages) * wide::stage_bytes(NB); }
+size_t wide_smem_bytes(int NB) { return kBarBytes + 1024 + size_t(kWideStages) * wide::stage_bytes(NB); }
 
 cudaError_t wide_prepare(int NB, size_t smem) {
   wide::KernelFn f = wide::lookup(NB);
@@ -237,8 +275,19 @@ cudaError_t wide_prepare(int NB, size_t smem) {
 
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
   wide::KernelFn f = wide::lookup(a.NB);
-  if (!f) return cudaErrorInvalidValue;
-  f<<<a.grid, dmma_threads(a.NB), a.smem, st>>>(a);
+  auto encode = wide::encode_fn();
+  if (!f || !encode) return cudaErrorInvalidValue;
+  // A viewed as a 2-D tensor [M rows][K doubles], boxes of 64 rows x 16 doubles
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {cuuint64_t(a.K), cuuint64_t(a.M)};
+  const cuuint64_t strides[1] = {cuuint64_t(a.K) * sizeof(double)};
+  const cuuint32_t box[2] = {16, cuuint32_t(kDmmaRowsPerSubtile)};
+  const cuuint32_t estr[2] = {1, 1};
+  if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(a.in), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  f<<<a.grid, dmma_threads(a.NB), a.smem, st>>>(a, map);
   return cudaGetLastError();
 }
 
