@@ -135,6 +135,35 @@ qtt_status_t qtt_apply_ws(qtt_handle_t h, const double* x, double* y, int64_t nr
 qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host,
                             int64_t nrhs, qtt_stream_t stream);
 
+/*
+ * Morton ordering (grid points indexed by successive
+ * bisection along each coordinate, "i.e., Morton ordered"; Remark
+ * rem:interlace P:855-870).  A grid of n^dim points, n = 2^levels, dim in
+ * {1,2,3}, d = dim*levels <= 30, stored in natural C order [z][y][x] (x
+ * fastest), maps to the QTT-order vector x_qtt[q] whose index bit
+ * dim*l + a is bit l of coordinate a (a = 0 x, 1 y, 2 z; l = 0 finest) --
+ * DESIGN.md reading R18.
+ *   qtt_morton_pack   : grid (natural) -> x (QTT order)
+ *   qtt_morton_unpack : x (QTT order) -> grid (natural)
+ * Both take DEVICE pointers to nrhs column-major blocks of N = 2^d doubles
+ * (8-byte aligned, non-overlapping), are stream-ordered, and return
+ * QTT_ERROR_INVALID_VALUE for bad dim/levels/nrhs or overlap,
+ * QTT_ERROR_NOT_SUPPORTED for host pointers.
+ */
+qtt_status_t qtt_morton_pack(const double* grid, double* x, int dim, int levels, int64_t nrhs,
+                             qtt_stream_t stream);
+qtt_status_t qtt_morton_unpack(const double* x, double* grid, int dim, int levels, int64_t nrhs,
+                               qtt_stream_t stream);
+
+/*
+ * qtt_apply_grid -- y = A x for vectors given as natural-order grids:
+ * Morton pack, qtt_apply, Morton unpack on `stream` (dim must divide d).
+ * grid_in / grid_out: DEVICE, nrhs blocks of N doubles, non-overlapping.  The
+ * two QTT-order staging vectors are cached in the handle (cudaMallocAsync).
+ */
+qtt_status_t qtt_apply_grid(qtt_handle_t h, const double* grid_in, double* grid_out, int dim, int64_t nrhs,
+                            qtt_stream_t stream);
+
 /* Plan facts: d, N, max rank, algorithmic flops per right-hand side
  * (4 * sum_k r_{k-1} r_k * N) and the number of kernel
  * launches one apply enqueues.  Any output pointer may be NULL. */

@@ -18,9 +18,10 @@ from .qtt_oracle import (
     tt_vector_entries, kron_vector_cores,
 )
 from .checks import compare, assert_close
+from . import morton
 
 __all__ = [
     "entry", "dense_matrix", "apply_dense", "apply_bitwise", "alg2_sweep",
     "apply_alg2", "apply_rows", "compose", "transpose", "compressed_matvec",
-    "tt_vector_dense", "tt_vector_entries", "kron_vector_cores", "compare", "assert_close",
+    "tt_vector_dense", "tt_vector_entries", "kron_vector_cores", "compare", "assert_close", "morton",
 ]

@@ -25,6 +25,7 @@ __all__ = [
     "QttOperator", "QttError", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "plan_stages", "qtt_apply", "qtt_apply_ws", "qtt_apply_host",
     "qtt_workspace_size", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy", "qtt_status_string", "library_path", "SYMBOLS",
+    "morton_pack", "morton_unpack",
 ]
 
 VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "merged", 3: "wide"}
@@ -163,6 +164,39 @@ def qtt_destroy(h: int) -> None:
     _lib.check("qtt_destroy", _lib.load().qtt_destroy(h))
 
 
+def _grid_args(t, dim: int, levels: int):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    N = 1 << (dim * levels)
+    if t.numel() % N or t.numel() == 0:
+        raise ValueError(f"tensor size {t.numel()} is not a multiple of N = {N}")
+    return t.numel() // N
+
+
+def morton_pack(grid, dim: int, levels: int, out=None, stream=None):
+    """Natural-order grid(s) (C order [z][y][x], nrhs blocks) -> QTT-order vectors (nrhs, N)."""
+    import torch
+    nrhs = _grid_args(grid, dim, levels)
+    N = 1 << (dim * levels)
+    y = torch.empty((nrhs, N), dtype=torch.float64, device=grid.device) if out is None else out
+    _grid_args(y, dim, levels)
+    _lib.check("qtt_morton_pack", _lib.load().qtt_morton_pack(
+        _ptr(grid), _ptr(y), int(dim), int(levels), int(nrhs), _stream_handle(stream)))
+    return y
+
+
+def morton_unpack(x, dim: int, levels: int, out=None, stream=None):
+    """QTT-order vectors (nrhs, N) -> natural-order grids, same shape as x unless out is given."""
+    import torch
+    nrhs = _grid_args(x, dim, levels)
+    y = torch.empty_like(x) if out is None else out
+    _grid_args(y, dim, levels)
+    _lib.check("qtt_morton_unpack", _lib.load().qtt_morton_unpack(
+        _ptr(x), _ptr(y), int(dim), int(levels), int(nrhs), _stream_handle(stream)))
+    return y
+
+
 # ----------------------------------------------------------------- object API
 class QttOperator:
     """A QTT matrix resident on the current CUDA device; ``apply`` computes y = A x."""
@@ -217,6 +251,20 @@ class QttOperator:
         return y
 
     __matmul__ = apply
+
+    def apply_grid(self, grid, dim: int, out=None, stream=None):
+        """y = A x with x, y natural-order grids (Morton pack / apply / unpack)."""
+        import torch
+        if self.d % dim:
+            raise ValueError(f"dim={dim} does not divide d={self.d}")
+        nrhs = _grid_args(grid, dim, self.d // dim)
+        y = torch.empty_like(grid) if out is None else out
+        _grid_args(y, dim, self.d // dim)
+        if y.numel() != grid.numel():
+            raise ValueError("out must have as many elements as grid")
+        _lib.check("qtt_apply_grid", _lib.load().qtt_apply_grid(
+            self.handle, _ptr(grid), _ptr(y), int(dim), int(nrhs), _stream_handle(stream)))
+        return y
 
     def apply_host(self, x: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
         x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))

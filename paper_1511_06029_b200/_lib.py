@@ -20,7 +20,7 @@ QTT_ERROR_CUDA = 4
 SYMBOLS = (
     "qtt_status_string", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "qtt_apply", "qtt_workspace_size", "qtt_apply_ws",
     "qtt_apply_host", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
-    "qtt_stage_times", "qtt_destroy",
+    "qtt_stage_times", "qtt_destroy", "qtt_morton_pack", "qtt_morton_unpack", "qtt_apply_grid",
 )
 
 _lib = None
@@ -65,6 +65,12 @@ def load():
     lib.qtt_set_stage_timing.argtypes = [h, C.c_int]
     lib.qtt_stage_times.restype = st
     lib.qtt_stage_times.argtypes = [h, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]
+    for name in ("qtt_morton_pack", "qtt_morton_unpack"):
+        fn = getattr(lib, name)
+        fn.restype = st
+        fn.argtypes = [dp, dp, C.c_int, C.c_int, i64, C.c_void_p]
+    lib.qtt_apply_grid.restype = st
+    lib.qtt_apply_grid.argtypes = [h, dp, dp, C.c_int, i64, C.c_void_p]
     lib.qtt_destroy.restype = st
     lib.qtt_destroy.argtypes = [h]
     _lib = lib

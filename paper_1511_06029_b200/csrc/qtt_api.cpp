@@ -50,6 +50,11 @@ struct qtt_plan {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   cudaStream_t ws_stream = nullptr;
+  // cached QTT-order staging vectors (qtt_apply_grid)
+  double* gx = nullptr;
+  double* gy = nullptr;
+  size_t g_elems = 0;
+  cudaStream_t g_stream = nullptr;
   // cached staging buffers (qtt_apply_host)
   double* hx = nullptr;
   double* hy = nullptr;
@@ -196,6 +201,8 @@ void free_plan(qtt_plan* h) {
     if (S.d_core) cudaFree(S.d_core);
   }
   if (h->ws) cudaFree(h->ws);
+  if (h->gx) cudaFree(h->gx);
+  if (h->gy) cudaFree(h->gy);
   if (h->hx) cudaFree(h->hx);
   if (h->hy) cudaFree(h->hy);
   for (auto& e : h->pending) {
@@ -486,6 +493,61 @@ qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host
   }
 }
 
+static qtt_status_t morton_common(const double* in, double* out, int dim, int levels, int64_t nrhs,
+                                  qtt_stream_t stream, bool pack) {
+  if (!in || !out || dim < 1 || dim > 3 || levels < 1 || dim * levels > 30 || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  const int64_t N = int64_t(1) << (dim * levels);
+  if (nrhs > (int64_t(1) << 40) / N) return QTT_ERROR_INVALID_VALUE;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(in), b = reinterpret_cast<uintptr_t>(out);
+  const uintptr_t bytes = uintptr_t(N) * uintptr_t(nrhs) * sizeof(double);
+  if (a < b + bytes && b < a + bytes) return QTT_ERROR_INVALID_VALUE;
+  if ((a % 8) || (b % 8)) return QTT_ERROR_NOT_SUPPORTED;
+  if (!is_device_ptr(in) || !is_device_ptr(out)) return QTT_ERROR_NOT_SUPPORTED;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return QTT_ERROR_CUDA;
+  return from_cuda(qtt::launch_morton(in, out, dim, levels, nrhs, pack, reinterpret_cast<cudaStream_t>(stream), sms));
+}
+
+qtt_status_t qtt_morton_pack(const double* grid, double* x, int dim, int levels, int64_t nrhs, qtt_stream_t stream) {
+  return morton_common(grid, x, dim, levels, nrhs, stream, true);
+}
+
+qtt_status_t qtt_morton_unpack(const double* x, double* grid, int dim, int levels, int64_t nrhs,
+                               qtt_stream_t stream) {
+  return morton_common(x, grid, dim, levels, nrhs, stream, false);
+}
+
+qtt_status_t qtt_apply_grid(qtt_handle_t h, const double* grid_in, double* grid_out, int dim, int64_t nrhs,
+                            qtt_stream_t stream) {
+  if (!h || !grid_in || !grid_out || dim < 1 || dim > 3 || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  if (h->d % dim) return QTT_ERROR_INVALID_VALUE;
+  const int levels = h->d / dim;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  try {
+    DeviceGuard g(h->device);
+    const size_t elems = size_t(h->N) * size_t(nrhs);
+    if (elems > h->g_elems) {
+      if (h->gx) cudaFreeAsync(h->gx, h->g_stream);
+      if (h->gy) cudaFreeAsync(h->gy, h->g_stream);
+      h->gx = h->gy = nullptr;
+      h->g_elems = 0;
+      cudaError_t e = cudaMallocAsync(&h->gx, elems * sizeof(double), st);
+      if (e == cudaSuccess) e = cudaMallocAsync(&h->gy, elems * sizeof(double), st);
+      if (e != cudaSuccess) return from_cuda(e);
+      h->g_elems = elems;
+      h->g_stream = st;
+    }
+    qtt_status_t s = qtt_morton_pack(grid_in, h->gx, dim, levels, nrhs, stream);
+    if (s != QTT_SUCCESS) return s;
+    s = qtt_apply(h, h->gx, h->gy, nrhs, stream);
+    if (s != QTT_SUCCESS) return s;
+    return qtt_morton_unpack(h->gy, grid_out, dim, levels, nrhs, stream);
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
 qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank, double* flops_per_rhs,
                           int* launches_per_apply) {
   if (!h) return QTT_ERROR_INVALID_VALUE;
@@ -541,6 +603,7 @@ qtt_status_t qtt_destroy(qtt_handle_t h) {
   DeviceGuard g(h->device);
   if (h->last) cudaEventSynchronize(h->last);
   if (h->ws && h->ws_stream) cudaStreamSynchronize(h->ws_stream);
+  if (h->gx && h->g_stream) cudaStreamSynchronize(h->g_stream);
   free_plan(h);
   return QTT_SUCCESS;
 }

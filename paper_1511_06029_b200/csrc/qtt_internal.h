@@ -105,5 +105,8 @@ size_t wide_smem_bytes(int NB);
 QTT_HD constexpr int wide_threads(int NB) { return dmma_threads(NB); }
 cudaError_t wide_prepare(int NB, size_t smem);
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st);
+// Morton pack (natural grid -> QTT order) or unpack, qtt_morton.cu
+cudaError_t launch_morton(const double* in, double* out, int dim, int levels, int64_t nrhs, bool pack,
+                          cudaStream_t st, int num_sms);
 
 }  // namespace qtt

@@ -1,0 +1,145 @@
+// Morton pack / unpack: natural grid order <-> QTT (hierarchical) order.
+//
+// the volume grid's N = 2^d points are indexed "according
+// to successive bisection of the domain along each coordinate direction (i.e.,
+// Morton ordered)"; Remark rem:interlace: the ordering defines the
+// hierarchical partition the QTT ranks depend on.  Convention (R18,
+// SPEC S:114): QTT index bit dim*l + a = bit l of coordinate a (a = 0 x, 1 y,
+// 2 z), l = 0 the finest level; the natural grid is row-major with x fastest.
+//
+// Both directions are HBM-bound permutations (8 bytes read + 8 written per
+// element).  Tiled path: one CTA moves one aligned block of 2^12 consecutive
+// QTT indices = a 16^3 cube (dim 3) or 64^2 square (dim 2) of the grid,
+// reading/writing the grid side in full 128-byte (dim 3) or 512-byte (dim 2)
+// rows and the QTT side as one contiguous 32 KiB run, through a padded smem
+// tile.  Grids smaller than one tile use a per-element kernel.
+#include "qtt_internal.h"
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace qtt {
+namespace {
+
+constexpr int kTileBits = 12;                 // 4096 elements per CTA
+constexpr int kTile = 1 << kTileBits;
+constexpr int kThreads = 256;
+
+// coordinate bits of a QTT index (de-interleave), dim in {1,2,3}
+__device__ __forceinline__ void deinterleave(int64_t q, int dim, int levels, int64_t (&c)[3]) {
+  c[0] = c[1] = c[2] = 0;
+  for (int l = 0; l < levels; ++l)
+    for (int a = 0; a < dim; ++a) c[a] |= ((q >> (dim * l + a)) & 1) << l;
+}
+
+// natural row-major offset of coordinates (x fastest)
+__device__ __forceinline__ int64_t natural(const int64_t (&c)[3], int dim, int levels) {
+  int64_t off = 0;
+  for (int a = dim - 1; a >= 0; --a) off = (off << levels) | c[a];
+  return off;
+}
+
+template <bool PACK>
+__global__ void morton_simple_kernel(const double* __restrict__ in, double* __restrict__ out, int dim, int levels,
+                                     int64_t total, int64_t N) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t s = t / N, q = t - s * N;
+    int64_t c[3];
+    deinterleave(q, dim, levels, c);
+    const int64_t g = s * N + natural(c, dim, levels);
+    if (PACK) out[t] = in[g];
+    else out[g] = in[t];
+  }
+}
+
+// Tile of 2^12 consecutive QTT indices.  dim 3: 16 x 16 x 16 (4 bits per axis),
+// dim 2: 64 x 64 (6 bits per axis).  smem holds the tile in natural order with
+// rows of R doubles padded to R + 1.
+template <int DIM, bool PACK>
+__global__ void __launch_bounds__(kThreads) morton_tile_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                               int levels, int64_t N) {
+  constexpr int B = kTileBits / DIM;          // bits per axis inside the tile
+  constexpr int R = 1 << B;                   // row length (x extent)
+  constexpr int ROWS = kTile / R;
+  constexpr int RP = R + 1;
+  __shared__ double tile[ROWS * RP];
+
+  const int64_t tiles_per_rhs = N >> kTileBits;
+  const int64_t s = blockIdx.x / tiles_per_rhs;
+  const int64_t tq = blockIdx.x - s * tiles_per_rhs;      // tile index in QTT order
+  // tile origin in grid coordinates: the QTT bits above kTileBits, de-interleaved
+  int64_t c0[3] = {0, 0, 0};
+  for (int l = B; l < levels; ++l)
+    for (int a = 0; a < DIM; ++a) c0[a] |= ((tq >> (DIM * (l - B) + a)) & 1) << l;
+  const int64_t n = int64_t(1) << levels;
+  const int64_t gbase = s * N + (DIM == 3 ? (c0[2] * n + c0[1]) * n + c0[0] : c0[1] * n + c0[0]);
+  const int64_t qbase = s * N + (tq << kTileBits);
+
+  // local natural (x, y[, z]) of local QTT index u
+  auto local_xyz = [](int u, int& x, int& y, int& z) {
+    x = y = z = 0;
+#pragma unroll
+    for (int l = 0; l < B; ++l) {
+      x |= ((u >> (DIM * l)) & 1) << l;
+      y |= ((u >> (DIM * l + 1)) & 1) << l;
+      if (DIM == 3) z |= ((u >> (DIM * l + 2)) & 1) << l;
+    }
+  };
+
+  if (PACK) {
+    // grid rows -> smem (coalesced rows of R doubles)
+    for (int e = threadIdx.x; e < kTile; e += kThreads) {
+      const int x = e & (R - 1), row = e >> B;      // row = z*R + y (dim 3) or y (dim 2)
+      const int y = row & (R - 1), z = row >> B;
+      const double* src = in + gbase + (DIM == 3 ? (int64_t(z) * n + y) * n : int64_t(y) * n) + x;
+      tile[row * RP + x] = *src;
+    }
+    __syncthreads();
+    for (int u = threadIdx.x; u < kTile; u += kThreads) {
+      int x, y, z;
+      local_xyz(u, x, y, z);
+      out[qbase + u] = tile[(z * R + y) * RP + x];
+    }
+  } else {
+    for (int u = threadIdx.x; u < kTile; u += kThreads) {
+      int x, y, z;
+      local_xyz(u, x, y, z);
+      tile[(z * R + y) * RP + x] = in[qbase + u];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTile; e += kThreads) {
+      const int x = e & (R - 1), row = e >> B;
+      const int y = row & (R - 1), z = row >> B;
+      out[gbase + (DIM == 3 ? (int64_t(z) * n + y) * n : int64_t(y) * n) + x] = tile[row * RP + x];
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_morton(const double* in, double* out, int dim, int levels, int64_t nrhs, bool pack,
+                          cudaStream_t st, int num_sms) {
+  const int d = dim * levels;
+  const int64_t N = int64_t(1) << d;
+  const bool tiled = (dim == 3 && levels >= 4) || (dim == 2 && levels >= 6);
+  if (tiled) {
+    const int64_t blocks = nrhs * (N >> kTileBits);
+    if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
+    if (dim == 3) {
+      if (pack) morton_tile_kernel<3, true><<<int(blocks), kThreads, 0, st>>>(in, out, levels, N);
+      else morton_tile_kernel<3, false><<<int(blocks), kThreads, 0, st>>>(in, out, levels, N);
+    } else {
+      if (pack) morton_tile_kernel<2, true><<<int(blocks), kThreads, 0, st>>>(in, out, levels, N);
+      else morton_tile_kernel<2, false><<<int(blocks), kThreads, 0, st>>>(in, out, levels, N);
+    }
+  } else {
+    const int64_t total = N * nrhs;
+    int64_t blocks = (total + kThreads - 1) / kThreads;
+    blocks = blocks > int64_t(num_sms) * 16 ? int64_t(num_sms) * 16 : blocks;
+    if (pack) morton_simple_kernel<true><<<int(blocks), kThreads, 0, st>>>(in, out, dim, levels, total, N);
+    else morton_simple_kernel<false><<<int(blocks), kThreads, 0, st>>>(in, out, dim, levels, total, N);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace qtt

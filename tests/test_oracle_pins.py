@@ -283,3 +283,57 @@ def test_pins_catch_mutations(mut):
     if not np.allclose(mut(CF.kron_cores(F), x), x @ A.T, rtol=1e-12):
         caught = True
     assert caught
+
+
+# --- Morton ordering (rem:interlace P:855-870; R18) ----
+def test_morton_spec_example():
+    # coordinate bits x=(1,0,0), y=(0,1,0), z=(0,0,1) (finest first)
+    # i.e. x=1, y=2, z=4 -> digits interleave x,y,z per level: q bits
+    # 0 (x_0)=1, 4 (y_1)=1, 8 (z_2)=1
+    from oracle import morton as M
+    assert M.morton_coords((1 << 0) | (1 << 4) | (1 << 8), 3, 3) == (1, 2, 4)
+    assert M.natural_index((1, 2, 4), 3) == 1 + 8 * 2 + 64 * 4
+
+
+@pytest.mark.parametrize("dim,levels", [(1, 5), (2, 3), (3, 2), (3, 3), (2, 5)])
+def test_morton_bijection_and_bisection(dim, levels):
+    """Bijection; and every aligned run of 2^(dim*l) consecutive QTT indices is
+    an axis-aligned cube of side 2^l (the successive-bisection partition)."""
+    from oracle import morton as M
+    N = 1 << (dim * levels)
+    p = M.morton_perm(dim, levels)
+    assert sorted(p.tolist()) == list(range(N))
+    n = 1 << levels
+    coords = np.array(np.unravel_index(p, (n,) * dim)).T[:, ::-1]   # (x, y, z) of each q
+    for l in range(levels + 1):
+        run = 1 << (dim * l)
+        for start in range(0, N, run):
+            blk = coords[start:start + run]
+            lo = blk.min(axis=0)
+            assert np.all(blk.max(axis=0) - lo == (1 << l) - 1)
+            assert np.all(lo % (1 << l) == 0)
+
+
+def test_morton_dim1_identity_and_roundtrip():
+    from oracle import morton as M
+    assert np.array_equal(M.morton_perm(1, 6), np.arange(64))
+    g = np.random.default_rng(0).standard_normal((2, 512))
+    assert np.array_equal(M.unpack(M.pack(g, 3, 3), 3, 3), g)
+
+
+def test_morton_separable_function():
+    """A separable grid function f(x) g(y) h(z) packs to the Kronecker vector
+    h (x) g (x) f in QTT digit order: digit dim*l + a of q selects bit l of axis a."""
+    from oracle import morton as M
+    rng = np.random.default_rng(1)
+    lv = 3
+    n = 1 << lv
+    # small integers: every product is exact, so the check is bitwise
+    f, g, h = (rng.integers(-9, 10, n).astype(float) for _ in range(3))
+    grid = np.einsum("z,y,x->zyx", h, g, f).reshape(1, -1)
+    xq = M.pack(grid, 3, lv)[0]
+    for q in range(1 << (3 * lv)):
+        x = sum(((q >> (3 * l)) & 1) << l for l in range(lv))
+        y = sum(((q >> (3 * l + 1)) & 1) << l for l in range(lv))
+        z = sum(((q >> (3 * l + 2)) & 1) << l for l in range(lv))
+        assert xq[q] == f[x] * g[y] * h[z]
