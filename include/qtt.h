@@ -164,6 +164,31 @@ qtt_status_t qtt_morton_unpack(const double* x, double* grid, int dim, int level
 qtt_status_t qtt_apply_grid(qtt_handle_t h, const double* grid_in, double* grid_out, int dim, int64_t nrhs,
                             qtt_stream_t stream);
 
+/*
+ * Products of QTT operators (NEXT-1): the paper applies its BIE
+ * preconditioner as the product of two QTT matrices, X = M Y, because the
+ * factors' ranks are smaller than the product's (P:1377-1402 Eq.
+ * precond_mateq, Table TT-BIE-3).  A product handle
+ * applies y = F_0 F_1 ... F_{n-1} x right to left on one stream (F_{n-1}
+ * first), each factor through its own stage plan; the factors' costs add
+ * (the composed QTT would have rank r_M r_Y per bond).
+ *   qtt_product_create : factors = n_factors >= 1 handles with equal d on one
+ *                        device; NOT owned (they must outlive the product).
+ *   qtt_product_workspace_size / qtt_product_apply_ws : caller workspace =
+ *                        the largest factor workspace + one (n = 2) or two
+ *                        (n >= 3) N*nrhs intermediate vectors, 256-byte aligned.
+ *   qtt_product_apply  : workspace cached in the product handle.
+ * Argument rules and errors as qtt_apply / qtt_apply_ws.
+ */
+typedef struct qtt_product* qtt_product_t;
+qtt_status_t qtt_product_create(qtt_product_t* out, int n_factors, const qtt_handle_t* factors);
+qtt_status_t qtt_product_workspace_size(qtt_product_t p, int64_t nrhs, size_t* bytes);
+qtt_status_t qtt_product_apply(qtt_product_t p, const double* x, double* y, int64_t nrhs,
+                               qtt_stream_t stream);
+qtt_status_t qtt_product_apply_ws(qtt_product_t p, const double* x, double* y, int64_t nrhs,
+                                  void* ws, size_t ws_bytes, qtt_stream_t stream);
+qtt_status_t qtt_product_destroy(qtt_product_t p);
+
 /* Plan facts: d, N, max rank, algorithmic flops per right-hand side
  * (4 * sum_k r_{k-1} r_k * N) and the number of kernel
  * launches one apply enqueues.  Any output pointer may be NULL. */

@@ -25,7 +25,7 @@ __all__ = [
     "QttOperator", "QttError", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "plan_stages", "qtt_apply", "qtt_apply_ws", "qtt_apply_host",
     "qtt_workspace_size", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy", "qtt_status_string", "library_path", "SYMBOLS",
-    "morton_pack", "morton_unpack",
+    "morton_pack", "morton_unpack", "QttProduct",
 ]
 
 VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "merged", 3: "wide"}
@@ -291,6 +291,64 @@ class QttOperator:
         if self._h is not None:
             h, self._h = self._h, None
             qtt_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class QttProduct:
+    """y = F_0 F_1 ... F_{n-1} x for QttOperator factors (applied right to left).
+
+    The factors are referenced, not owned: keep them open while the product is used."""
+
+    def __init__(self, factors):
+        self._h = None
+        if not factors:
+            raise ValueError("need at least one factor")
+        self.factors = list(factors)
+        hs = (C.c_void_p * len(self.factors))(*[f.handle for f in self.factors])
+        h = C.c_void_p()
+        _lib.check("qtt_product_create", _lib.load().qtt_product_create(C.byref(h), len(self.factors), hs))
+        self._h = int(h.value)
+        self.N = self.factors[0].N
+        self.flops_per_rhs = sum(f.flops_per_rhs for f in self.factors)
+
+    def workspace_size(self, nrhs: int = 1) -> int:
+        b = C.c_size_t()
+        _lib.check("qtt_product_workspace_size", _lib.load().qtt_product_workspace_size(self._h, int(nrhs), C.byref(b)))
+        return int(b.value)
+
+    def apply(self, x, out=None, stream=None, workspace=None):
+        import torch
+        nrhs = self.factors[0]._check_x(x)
+        y = torch.empty_like(x) if out is None else out
+        if out is not None and (out.shape != x.shape or out.dtype != torch.float64 or not out.is_cuda
+                                or not out.is_contiguous()):
+            raise ValueError("out must be a contiguous float64 CUDA tensor shaped like x")
+        if workspace is None:
+            _lib.check("qtt_product_apply", _lib.load().qtt_product_apply(
+                self._h, _ptr(x), _ptr(y), nrhs, _stream_handle(stream)))
+        else:
+            _lib.check("qtt_product_apply_ws", _lib.load().qtt_product_apply_ws(
+                self._h, _ptr(x), _ptr(y), nrhs, _ptr(workspace),
+                workspace.numel() * workspace.element_size(), _stream_handle(stream)))
+        return y
+
+    __matmul__ = apply
+
+    def close(self):
+        if self._h is not None:
+            h, self._h = self._h, None
+            _lib.load().qtt_product_destroy(h)
 
     def __del__(self):
         try:

@@ -21,6 +21,8 @@ SYMBOLS = (
     "qtt_status_string", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "qtt_apply", "qtt_workspace_size", "qtt_apply_ws",
     "qtt_apply_host", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy", "qtt_morton_pack", "qtt_morton_unpack", "qtt_apply_grid",
+    "qtt_product_create", "qtt_product_workspace_size", "qtt_product_apply", "qtt_product_apply_ws",
+    "qtt_product_destroy",
 )
 
 _lib = None
@@ -71,6 +73,16 @@ def load():
         fn.argtypes = [dp, dp, C.c_int, C.c_int, i64, C.c_void_p]
     lib.qtt_apply_grid.restype = st
     lib.qtt_apply_grid.argtypes = [h, dp, dp, C.c_int, i64, C.c_void_p]
+    lib.qtt_product_create.restype = st
+    lib.qtt_product_create.argtypes = [C.POINTER(h), C.c_int, C.POINTER(h)]
+    lib.qtt_product_workspace_size.restype = st
+    lib.qtt_product_workspace_size.argtypes = [h, i64, C.POINTER(C.c_size_t)]
+    lib.qtt_product_apply.restype = st
+    lib.qtt_product_apply.argtypes = [h, dp, dp, i64, C.c_void_p]
+    lib.qtt_product_apply_ws.restype = st
+    lib.qtt_product_apply_ws.argtypes = [h, dp, dp, i64, dp, C.c_size_t, C.c_void_p]
+    lib.qtt_product_destroy.restype = st
+    lib.qtt_product_destroy.argtypes = [h]
     lib.qtt_destroy.restype = st
     lib.qtt_destroy.argtypes = [h]
     _lib = lib

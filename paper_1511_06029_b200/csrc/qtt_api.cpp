@@ -66,6 +66,16 @@ struct qtt_plan {
   int timed_applies = 0;
 };
 
+// Product of QTT operators applied right to left (qtt_product_create).
+struct qtt_product {
+  std::vector<qtt_plan*> factors;   // y = F_0 F_1 ... F_{n-1} x; not owned
+  int device = 0;
+  int64_t N = 0;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaStream_t ws_stream = nullptr;
+};
+
 namespace {
 
 struct DeviceGuard {
@@ -546,6 +556,112 @@ qtt_status_t qtt_apply_grid(qtt_handle_t h, const double* grid_in, double* grid_
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
+}
+
+// ---------------------------------------------------------------- products (NEXT-1)
+static size_t product_vec_bytes(const qtt_product* p, int64_t nrhs) {
+  return (size_t(p->N) * size_t(nrhs) * sizeof(double) + 255) / 256 * 256;
+}
+
+static size_t product_ws_bytes(const qtt_product* p, int64_t nrhs) {
+  size_t f = 0;
+  for (auto* h : p->factors) f = std::max(f, ws_bytes_for(h, nrhs));
+  const size_t nvec = p->factors.size() >= 3 ? 2 : (p->factors.size() == 2 ? 1 : 0);
+  return f + nvec * product_vec_bytes(p, nrhs);
+}
+
+qtt_status_t qtt_product_create(qtt_product_t* out, int n_factors, const qtt_handle_t* factors) {
+  if (!out) return QTT_ERROR_INVALID_VALUE;
+  *out = nullptr;
+  if (n_factors < 1 || !factors) return QTT_ERROR_INVALID_VALUE;
+  for (int i = 0; i < n_factors; ++i) {
+    if (!factors[i]) return QTT_ERROR_INVALID_VALUE;
+    if (factors[i]->d != factors[0]->d || factors[i]->device != factors[0]->device) return QTT_ERROR_INVALID_VALUE;
+  }
+  try {
+    qtt_product* p = new qtt_product();
+    p->factors.assign(factors, factors + n_factors);
+    p->device = factors[0]->device;
+    p->N = factors[0]->N;
+    *out = p;
+  } catch (const std::bad_alloc&) {
+    return QTT_ERROR_OUT_OF_MEMORY;
+  }
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_product_workspace_size(qtt_product_t p, int64_t nrhs, size_t* bytes) {
+  if (!p || !bytes || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  *bytes = product_ws_bytes(p, nrhs);
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_product_apply_ws(qtt_product_t p, const double* x, double* y, int64_t nrhs, void* ws,
+                                  size_t ws_bytes, qtt_stream_t stream) {
+  if (!p) return QTT_ERROR_INVALID_VALUE;
+  qtt_status_t s = check_apply_args(p->factors[0], x, y, nrhs);
+  if (s != QTT_SUCCESS) return s;
+  const size_t need = product_ws_bytes(p, nrhs);
+  if (!ws || ws_bytes < need) return QTT_ERROR_INVALID_VALUE;
+  if (reinterpret_cast<uintptr_t>(ws) % 256) return QTT_ERROR_NOT_SUPPORTED;
+  if (!is_device_ptr(ws)) return QTT_ERROR_NOT_SUPPORTED;
+  try {
+    DeviceGuard g(p->device);
+    const int n = int(p->factors.size());
+    unsigned char* base = static_cast<unsigned char*>(ws);
+    const size_t vb = product_vec_bytes(p, nrhs);
+    double* tmp[2] = {reinterpret_cast<double*>(base), reinterpret_cast<double*>(base + vb)};
+    const size_t nvec = n >= 3 ? 2 : (n == 2 ? 1 : 0);
+    void* fws = base + nvec * vb;
+    const double* in = x;
+    // F_{n-1} first; each factor's stages read the previous factor's output
+    for (int i = n - 1, step = 0; i >= 0; --i, ++step) {
+      double* out = (i == 0) ? y : tmp[step & 1];
+      s = enqueue(p->factors[i], in, out, nrhs, fws, reinterpret_cast<cudaStream_t>(stream));
+      if (s != QTT_SUCCESS) return s;
+      in = out;
+    }
+    return QTT_SUCCESS;
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_product_apply(qtt_product_t p, const double* x, double* y, int64_t nrhs, qtt_stream_t stream) {
+  if (!p) return QTT_ERROR_INVALID_VALUE;
+  qtt_status_t s = check_apply_args(p->factors[0], x, y, nrhs);
+  if (s != QTT_SUCCESS) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  try {
+    DeviceGuard g(p->device);
+    const size_t need = product_ws_bytes(p, nrhs);
+    if (need > p->ws_bytes) {
+      if (p->ws) cudaFreeAsync(p->ws, p->ws_stream);
+      p->ws = nullptr;
+      p->ws_bytes = 0;
+      cudaError_t e = cudaMallocAsync(&p->ws, need, st);
+      if (e != cudaSuccess) {
+        p->ws = nullptr;
+        return from_cuda(e);
+      }
+      p->ws_bytes = need;
+      p->ws_stream = st;
+    }
+    return qtt_product_apply_ws(p, x, y, nrhs, p->ws, p->ws_bytes, stream);
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_product_destroy(qtt_product_t p) {
+  if (!p) return QTT_SUCCESS;
+  DeviceGuard g(p->device);
+  if (p->ws) {
+    if (p->ws_stream) cudaStreamSynchronize(p->ws_stream);
+    cudaFree(p->ws);
+  }
+  delete p;
+  return QTT_SUCCESS;
 }
 
 qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank, double* flops_per_rhs,
