@@ -205,6 +205,112 @@ def run_cpu_baseline(cfg, cores, x, budget_s=20.0):
             "seconds": dt, "blas": apis, "host_cpus": os.cpu_count()}
 
 
+def stage_table(stages, r, N, nrhs, stage_ms, n_timed, P, BW):
+    """Per-stage roofline rows: T_s = max(F_s/P, B_s/BW) with F_s the
+    Alg. 2 flops of the stage's levels and B_s its HBM bytes; also the executed-flop basis."""
+    stage_rows = []
+    sum_T, sum_t = 0.0, 0.0
+    for s, st in enumerate(stages):
+        k0, k1 = st["k_first"], st["k_last"]
+        F = sum(4 * r[k - 1] * r[k] for k in range(k0, k1 + 1)) * N * nrhs
+        B = 8 * N * nrhs * (r[k0 - 1] + r[k1]) + 32 * sum(r[k - 1] * r[k] for k in range(k0, k1 + 1))
+        # flops the kernel actually executes (unpadded): a merged stage of L levels
+        # applies the 2^L r_in x 2^L r_out super-core, 2^(L+1) r_in r_out per element
+        F_exec = (2 ** (k1 - k0 + 2)) * r[k0 - 1] * r[k1] * N * nrhs if k1 > k0 else F
+        t = stage_ms[s] / max(n_timed, 1) * 1e-3
+        T = max(F / P, B / BW)
+        sum_T += T
+        sum_t += t
+        stage_rows.append({"levels": [k0, k1], "ranks": [r[k0 - 1], r[k1]], "variant": st["variant"],
+                           "ms": t * 1e3, "gflops": F / t / 1e9 if t else None,
+                           "gbs": B / t / 1e9 if t else None, "roofline_frac": T / t if t else None,
+                           "flops_alg2": F, "flops_executed": F_exec,
+                           "roofline_frac_executed": max(F_exec / P, B / BW) / t if t else None})
+    return stage_rows, sum_T, sum_t
+
+
+def time_applies(fn, steps, warmup, stream):
+    """Median and min ms of `fn()` over `steps` launches, CUDA events on `stream`."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts), min(ts)
+
+
+def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
+    """The other BASELINE configs and the NEXT rows, timed after the headline
+    (not part of `value`): per config ms/apply, Alg. 2 and executed rates and
+    per-stage roofline fractions; Morton pack/unpack GB/s at 256^3; the product
+    X = M Y of two c4-profile operators; the grid apply at 256^3."""
+    import torch
+    import paper_1511_06029_b200 as q
+    from qtt_workload import generate
+    out = {}
+    for name in ("c1", "c2", "c3", "c3x16", "c5"):
+        cfg, cores, x_np = generate(name)
+        with q.QttOperator(cores, max_stage_levels=max_stage_levels) as op:
+            x = torch.from_numpy(x_np).to(dev)
+            y = torch.empty_like(x)
+            ws = torch.empty(max(op.workspace_size(cfg.nrhs), 8) // 8 + 64, dtype=torch.float64, device=dev)
+            reps = 5 if name == "c5" else 20
+            fn = lambda: op.apply(x, out=y, workspace=ws, stream=stream)
+            med, mn = time_applies(fn, reps, 3, stream)
+            op.set_stage_timing(True)
+            op.stage_times()
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            op.set_stage_timing(False)
+            sms, nt = op.stage_times()
+            rows, sT, st_ = stage_table(op.stages(), cfg.ranks, cfg.N, cfg.nrhs, sms, nt, P, BW)
+            F = op.flops_per_rhs * cfg.nrhs
+            Fx = sum(rr["flops_executed"] for rr in rows)
+            out[name] = {"ms_median": med, "ms_min": mn, "gflops_alg2": F / (med * 1e-3) / 1e9,
+                         "tflops_executed": Fx / (med * 1e-3) / 1e12, "launches": op.launches_per_apply,
+                         "per_stage_frac": sT / st_ if st_ else None,
+                         "per_stage_frac_executed": sum(
+                             max(rr["flops_executed"] / P, (8 * cfg.N * cfg.nrhs * (rr["ranks"][0] + rr["ranks"][1])) / BW)
+                             for rr in rows) / st_ if st_ else None,
+                         "stages": [[rr["levels"][0], rr["levels"][1], rr["variant"]] for rr in rows]}
+            del x, y, ws
+        torch.cuda.empty_cache()
+    # NEXT-2: Morton pack / unpack at 256^3 (16 bytes moved per element)
+    N = 1 << 24
+    g = torch.randn(N, dtype=torch.float64, device=dev)
+    xq = torch.empty_like(g)
+    gb = torch.empty_like(g)
+    mp, _ = time_applies(lambda: q.morton_pack(g, 3, 8, out=xq, stream=stream), 20, 3, stream)
+    mu, _ = time_applies(lambda: q.morton_unpack(xq, 3, 8, out=gb, stream=stream), 20, 3, stream)
+    out["morton_256cubed"] = {"pack_ms": mp, "unpack_ms": mu, "pack_gbs": 16 * N / (mp * 1e-3) / 1e9,
+                              "unpack_gbs": 16 * N / (mu * 1e-3) / 1e9,
+                              "pack_frac_hbm": 16 * N / (mp * 1e-3) / BW, "unpack_frac_hbm": 16 * N / (mu * 1e-3) / BW}
+    # NEXT-1: product of two c4-profile operators, and the grid apply
+    _, cM, xg = generate("c4")
+    _, cY, _ = generate("c4", seed=1, with_x=False)
+    with q.QttOperator(cM) as M, q.QttOperator(cY) as Y, q.QttProduct([M, Y]) as PR:
+        x = torch.from_numpy(xg).to(dev)
+        y = torch.empty_like(x)
+        ws = torch.empty(PR.workspace_size(1) // 8 + 64, dtype=torch.float64, device=dev)
+        pm, _ = time_applies(lambda: PR.apply(x, out=y, workspace=ws, stream=stream), 5, 2, stream)
+        F = M.flops_per_rhs + Y.flops_per_rhs
+        out["product_c4xc4"] = {"ms_median": pm, "gflops_alg2": F / (pm * 1e-3) / 1e9}
+        gm, _ = time_applies(lambda: M.apply_grid(x, 3, out=y, stream=stream), 5, 2, stream)
+        out["grid_apply_c4"] = {"ms_median": gm, "gflops_alg2": M.flops_per_rhs / (gm * 1e-3) / 1e9}
+        del x, y, ws
+    torch.cuda.empty_cache()
+    return out
+
+
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -247,6 +353,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=20.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-extra", action="store_true", help="skip the other configs / NEXT-row measurements")
     ap.add_argument("--max-stage-levels", type=int, default=None,
                     help="cap on levels per launch (1 = Alg. 2 level by level); default: the library's")
     args = ap.parse_args(argv)
@@ -319,24 +426,7 @@ def main(argv=None):
     stages = op.stages()
     r = cfg.ranks
     N = cfg.N
-    stage_rows = []
-    sum_T, sum_t = 0.0, 0.0
-    for s, st in enumerate(stages):
-        k0, k1 = st["k_first"], st["k_last"]
-        F = sum(4 * r[k - 1] * r[k] for k in range(k0, k1 + 1)) * N * nrhs
-        B = 8 * N * nrhs * (r[k0 - 1] + r[k1]) + 32 * sum(r[k - 1] * r[k] for k in range(k0, k1 + 1))
-        # flops the kernel actually executes (unpadded): a merged stage of L levels
-        # applies the 2^L r_in x 2^L r_out super-core, 2^(L+1) r_in r_out per element
-        F_exec = (2 ** (k1 - k0 + 2)) * r[k0 - 1] * r[k1] * N * nrhs if k1 > k0 else F
-        t = stage_ms[s] / max(n_timed, 1) * 1e-3
-        T = max(F / P, B / BW)
-        sum_T += T
-        sum_t += t
-        stage_rows.append({"levels": [k0, k1], "ranks": [r[k0 - 1], r[k1]], "variant": st["variant"],
-                           "ms": t * 1e3, "gflops": F / t / 1e9 if t else None,
-                           "gbs": B / t / 1e9 if t else None, "roofline_frac": T / t if t else None,
-                           "flops_alg2": F, "flops_executed": F_exec,
-                           "roofline_frac_executed": max(F_exec / P, B / BW) / t if t else None})
+    stage_rows, sum_T, sum_t = stage_table(stages, r, N, nrhs, stage_ms, n_timed, P, BW)
     # dominant kernel: the stage shape with the largest share of the step
     by_kernel = {}
     for s, row in enumerate(stage_rows):
@@ -379,6 +469,13 @@ def main(argv=None):
             (8 * N * nrhs * (r[st["levels"][0] - 1] + r[st["levels"][1]])) / BW)
         for st in stage_rows) / sum_t if sum_t else None
 
+    extra = None
+    if world == 1 and not args.no_extra:
+        op.close()
+        del x, y, ws
+        torch.cuda.empty_cache()
+        extra = extra_measurements(dev, stream, P, BW, args.max_stage_levels)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(cfg, cores, x_np, budget_s=20.0)
@@ -406,6 +503,7 @@ def main(argv=None):
                 "h2d_bytes_per_step": int(x_np.nbytes), "d2h_bytes_per_step": int(x_np.nbytes)},
         "gpu_launches": op.launches_per_apply * args.steps,
         "clocks": clocks,
+        "other_configs_and_next_rows": extra,
     }
     if rank == 0:
         print(json.dumps(out))
