@@ -189,6 +189,30 @@ qtt_status_t qtt_product_apply_ws(qtt_product_t p, const double* x, double* y, i
                                   void* ws, size_t ws_bytes, qtt_stream_t stream);
 qtt_status_t qtt_product_destroy(qtt_product_t p);
 
+/*
+ * QTT-compressed matrix-vector product (NEXT-3; PAPER section 4.2
+ * "QTT Compressed matrix-vector product"): for b given in QTT
+ * form, the cores of c = A b are
+ *   G^c_k((alpha beta), i_k, (alpha' beta')) = sum_j G^A_k(alpha, i_k j_k, alpha') G^b_k(beta, j_k, beta')
+ * with ranks R_k = r^A_k * r^b_k (<= 4096, else QTT_ERROR_NOT_SUPPORTED).
+ *   b_ranks : host, d+1 ranks of b (b_ranks[0] == b_ranks[d] == 1).
+ *   b_cores : host array of d HOST pointers, core k of b as b_ranks[k-1]*2*b_ranks[k]
+ *             doubles [beta][j][beta'] (copied; free on return).
+ *   c_ranks : optional host array (d+1) receiving R_k.
+ * qtt_compressed_matvec writes the DENSE c (N doubles, device, 16-byte aligned):
+ * the product cores are densified on the GPU (Eq. TTdeccores for a vector,
+ * split at level d/2 into two halves and one GEMM).
+ * qtt_compressed_matvec_cores writes the product cores instead, concatenated
+ * k = 1..d as [R_{k-1}][2][R_k] row-major into DEVICE memory of >= the sum of
+ * their sizes in bytes (c_cores_bytes).  Both synchronize `stream` before
+ * returning (the workspace is allocated and freed on it).
+ */
+qtt_status_t qtt_compressed_matvec(qtt_handle_t h, const int64_t* b_ranks, const double* const* b_cores,
+                                   double* c, int64_t* c_ranks, qtt_stream_t stream);
+qtt_status_t qtt_compressed_matvec_cores(qtt_handle_t h, const int64_t* b_ranks,
+                                         const double* const* b_cores, double* c_cores,
+                                         size_t c_cores_bytes, int64_t* c_ranks, qtt_stream_t stream);
+
 /* Plan facts: d, N, max rank, algorithmic flops per right-hand side
  * (4 * sum_k r_{k-1} r_k * N) and the number of kernel
  * launches one apply enqueues.  Any output pointer may be NULL. */

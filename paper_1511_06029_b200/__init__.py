@@ -252,6 +252,41 @@ class QttOperator:
 
     __matmul__ = apply
 
+    def compressed_matvec(self, b_cores, out=None, stream=None, cores_only: bool = False):
+        """c = A b for b in QTT form (PAPER section 4.2).  b_cores: d arrays (r_{k-1}, 2, r_k).
+
+        Returns the dense c (torch float64 tensor of N entries on the current device), or with
+        cores_only=True the list of product cores (R_{k-1}, 2, R_k) as device tensors."""
+        import torch
+        bs = [np.ascontiguousarray(np.asarray(v, dtype=np.float64)) for v in b_cores]
+        if len(bs) != self.d:
+            raise ValueError(f"need {self.d} cores, got {len(bs)}")
+        br = [bs[0].shape[0]] + [v.shape[2] for v in bs]
+        for k, v in enumerate(bs):
+            if v.ndim != 3 or v.shape != (br[k], 2, br[k + 1]):
+                raise ValueError(f"b core {k + 1} has shape {v.shape}")
+        rb = (C.c_int64 * (self.d + 1))(*br)
+        ptrs = (C.c_void_p * self.d)(*[v.ctypes.data for v in bs])
+        cr = (C.c_int64 * (self.d + 1))()
+        lib = _lib.load()
+        if cores_only:
+            R = [a * b for a, b in zip(self.ranks, br)]
+            sizes = [R[k] * 2 * R[k + 1] for k in range(self.d)]
+            buf = torch.empty(sum(sizes), dtype=torch.float64, device="cuda")
+            _lib.check("qtt_compressed_matvec_cores", lib.qtt_compressed_matvec_cores(
+                self.handle, rb, ptrs, _ptr(buf), buf.numel() * 8, cr, _stream_handle(stream)))
+            out_cores, off = [], 0
+            for k in range(self.d):
+                out_cores.append(buf[off:off + sizes[k]].view(R[k], 2, R[k + 1]))
+                off += sizes[k]
+            return out_cores
+        y = torch.empty(self.N, dtype=torch.float64, device="cuda") if out is None else out
+        if y.numel() != self.N or y.dtype != torch.float64 or not y.is_cuda or not y.is_contiguous():
+            raise ValueError("out must be a contiguous float64 CUDA tensor of N entries")
+        _lib.check("qtt_compressed_matvec", lib.qtt_compressed_matvec(
+            self.handle, rb, ptrs, _ptr(y), cr, _stream_handle(stream)))
+        return y
+
     def apply_grid(self, grid, dim: int, out=None, stream=None):
         """y = A x with x, y natural-order grids (Morton pack / apply / unpack)."""
         import torch

@@ -22,7 +22,7 @@ SYMBOLS = (
     "qtt_apply_host", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy", "qtt_morton_pack", "qtt_morton_unpack", "qtt_apply_grid",
     "qtt_product_create", "qtt_product_workspace_size", "qtt_product_apply", "qtt_product_apply_ws",
-    "qtt_product_destroy",
+    "qtt_product_destroy", "qtt_compressed_matvec", "qtt_compressed_matvec_cores",
 )
 
 _lib = None
@@ -83,6 +83,11 @@ def load():
     lib.qtt_product_apply_ws.argtypes = [h, dp, dp, i64, dp, C.c_size_t, C.c_void_p]
     lib.qtt_product_destroy.restype = st
     lib.qtt_product_destroy.argtypes = [h]
+    lib.qtt_compressed_matvec.restype = st
+    lib.qtt_compressed_matvec.argtypes = [h, C.POINTER(i64), C.POINTER(C.c_void_p), dp, C.POINTER(i64), C.c_void_p]
+    lib.qtt_compressed_matvec_cores.restype = st
+    lib.qtt_compressed_matvec_cores.argtypes = [h, C.POINTER(i64), C.POINTER(C.c_void_p), dp, C.c_size_t,
+                                                C.POINTER(i64), C.c_void_p]
     lib.qtt_destroy.restype = st
     lib.qtt_destroy.argtypes = [h]
     _lib = lib

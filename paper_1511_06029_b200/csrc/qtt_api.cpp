@@ -45,6 +45,7 @@ struct qtt_plan {
   int64_t N = 0;
   std::vector<int64_t> ranks;
   std::vector<Stage> stages;
+  std::vector<double*> d_raw;      // raw cores G_k [a][i][j][b] (compressed matvec)
   int64_t max_interior_rank = 0;
   // cached workspace (qtt_apply)
   void* ws = nullptr;
@@ -210,6 +211,8 @@ void free_plan(qtt_plan* h) {
     if (S.d_bpack) cudaFree(S.d_bpack);
     if (S.d_core) cudaFree(S.d_core);
   }
+  for (double* p : h->d_raw)
+    if (p) cudaFree(p);
   if (h->ws) cudaFree(h->ws);
   if (h->gx) cudaFree(h->gx);
   if (h->gy) cudaFree(h->gy);
@@ -409,6 +412,13 @@ qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks, const
       if (s + 1 < plan.size()) h->max_interior_rank = std::max<int64_t>(h->max_interior_rank, plan[s].r_out);
     }
     for (size_t s = 0; s < plan.size() && st == QTT_SUCCESS; ++s) st = upload_stage(h, h->stages[s], cores);
+    h->d_raw.assign(d, nullptr);
+    for (int k = 0; k < d && st == QTT_SUCCESS; ++k) {
+      const size_t bytes = size_t(ranks[k]) * 4 * ranks[k + 1] * sizeof(double);
+      cudaError_t e = cudaMalloc(&h->d_raw[k], bytes);
+      if (e == cudaSuccess) e = cudaMemcpy(h->d_raw[k], cores[k], bytes, cudaMemcpyHostToDevice);
+      st = from_cuda(e);
+    }
   } catch (const std::bad_alloc&) {
     st = QTT_ERROR_OUT_OF_MEMORY;
   }
@@ -556,6 +566,85 @@ qtt_status_t qtt_apply_grid(qtt_handle_t h, const double* grid_in, double* grid_
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
+}
+
+// ---------------------------------------------------------------- compressed matvec (NEXT-3)
+static qtt_status_t compressed_common(qtt_handle_t h, const int64_t* b_ranks, const double* const* b_cores,
+                                      double* c_dense, double* c_cores, size_t c_cores_bytes, int64_t* c_ranks,
+                                      qtt_stream_t stream) {
+  if (!h || !b_ranks || !b_cores) return QTT_ERROR_INVALID_VALUE;
+  const int d = h->d;
+  if (b_ranks[0] != 1 || b_ranks[d] != 1) return QTT_ERROR_INVALID_VALUE;
+  for (int k = 0; k <= d; ++k)
+    if (b_ranks[k] < 1 || b_ranks[k] > 4096) return QTT_ERROR_INVALID_VALUE;
+  for (int k = 0; k < d; ++k)
+    if (!b_cores[k]) return QTT_ERROR_INVALID_VALUE;
+  std::vector<int64_t> R(d + 1);
+  for (int k = 0; k <= d; ++k) {
+    R[k] = h->ranks[k] * b_ranks[k];
+    if (R[k] > 4096) return QTT_ERROR_NOT_SUPPORTED;
+  }
+  if (c_ranks)
+    for (int k = 0; k <= d; ++k) c_ranks[k] = R[k];
+  std::vector<size_t> coff(d + 1, 0), boff(d + 1, 0);
+  for (int k = 0; k < d; ++k) {
+    coff[k + 1] = coff[k] + size_t(R[k]) * 2 * R[k + 1];
+    boff[k + 1] = boff[k] + size_t(b_ranks[k]) * 2 * b_ranks[k + 1];
+  }
+  if (c_cores && c_cores_bytes < coff[d] * sizeof(double)) return QTT_ERROR_INVALID_VALUE;
+  if (c_dense && !is_device_ptr(c_dense)) return QTT_ERROR_NOT_SUPPORTED;
+  if (c_cores && !is_device_ptr(c_cores)) return QTT_ERROR_NOT_SUPPORTED;
+  if (c_dense && (reinterpret_cast<uintptr_t>(c_dense) % 16)) return QTT_ERROR_NOT_SUPPORTED;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  try {
+    DeviceGuard g(h->device);
+    // b's cores: host -> device (pageable copy, synchronous w.r.t. the host arrays)
+    double* dV = nullptr;
+    cudaError_t e = cudaMallocAsync(&dV, std::max<size_t>(boff[d], 1) * sizeof(double), st);
+    if (e != cudaSuccess) return from_cuda(e);
+    for (int k = 0; k < d && e == cudaSuccess; ++k)
+      e = cudaMemcpyAsync(dV + boff[k], b_cores[k], (boff[k + 1] - boff[k]) * sizeof(double),
+                          cudaMemcpyHostToDevice, st);
+    double* dC = c_cores;
+    if (e == cudaSuccess && !dC) e = cudaMallocAsync(&dC, coff[d] * sizeof(double), st);
+    void* ws = nullptr;
+    const size_t wsb = c_dense ? qtt::densify_workspace_bytes(d, R.data()) : 0;
+    if (e == cudaSuccess && wsb) e = cudaMallocAsync(&ws, wsb, st);
+    if (e == cudaSuccess) {
+      std::vector<const double*> G(h->d_raw.begin(), h->d_raw.end()), V(d);
+      std::vector<double*> C(d);
+      for (int k = 0; k < d; ++k) {
+        V[k] = dV + boff[k];
+        C[k] = dC + coff[k];
+      }
+      e = qtt::compressed_cores(d, h->ranks.data(), G.data(), b_ranks, V.data(), C.data(), st, h->num_sms);
+      if (e == cudaSuccess && c_dense) {
+        std::vector<const double*> Cc(C.begin(), C.end());
+        e = qtt::tt_densify(d, R.data(), Cc.data(), c_dense, ws, st, h->num_sms, h->smem_optin);
+      }
+    }
+    if (ws) cudaFreeAsync(ws, st);
+    if (dC && dC != c_cores) cudaFreeAsync(dC, st);
+    cudaFreeAsync(dV, st);
+    // the host core arrays may be freed by the caller on return
+    cudaError_t se = cudaStreamSynchronize(st);
+    return from_cuda(e != cudaSuccess ? e : se);
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_compressed_matvec(qtt_handle_t h, const int64_t* b_ranks, const double* const* b_cores,
+                                   double* c, int64_t* c_ranks, qtt_stream_t stream) {
+  if (!c) return QTT_ERROR_INVALID_VALUE;
+  return compressed_common(h, b_ranks, b_cores, c, nullptr, 0, c_ranks, stream);
+}
+
+qtt_status_t qtt_compressed_matvec_cores(qtt_handle_t h, const int64_t* b_ranks, const double* const* b_cores,
+                                         double* c_cores, size_t c_cores_bytes, int64_t* c_ranks,
+                                         qtt_stream_t stream) {
+  if (!c_cores) return QTT_ERROR_INVALID_VALUE;
+  return compressed_common(h, b_ranks, b_cores, nullptr, c_cores, c_cores_bytes, c_ranks, stream);
 }
 
 // ---------------------------------------------------------------- products (NEXT-1)

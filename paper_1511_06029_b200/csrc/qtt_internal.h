@@ -105,6 +105,12 @@ size_t wide_smem_bytes(int NB);
 QTT_HD constexpr int wide_threads(int NB) { return dmma_threads(NB); }
 cudaError_t wide_prepare(int NB, size_t smem);
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st);
+// QTT-compressed matvec cores and TT-vector densification, qtt_compressed.cu
+cudaError_t compressed_cores(int d, const int64_t* ra, const double* const* dG, const int64_t* rb,
+                             const double* const* dV, double* const* dC, cudaStream_t st, int num_sms);
+size_t densify_workspace_bytes(int d, const int64_t* R);
+cudaError_t tt_densify(int d, const int64_t* R, const double* const* dH, double* out, void* ws, cudaStream_t st,
+                       int num_sms, size_t smem_optin);
 // Morton pack (natural grid -> QTT order) or unpack, qtt_morton.cu
 cudaError_t launch_morton(const double* in, double* out, int dim, int levels, int64_t nrhs, bool pack,
                           cudaStream_t st, int num_sms);

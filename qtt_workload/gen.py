@@ -53,3 +53,16 @@ def random_case(seed: int, d: int, max_rank: int, nrhs: int = 1, ranks=None):
     cores = random_cores(rng, ranks, scale)
     x = rng.standard_normal((nrhs, 1 << d))
     return list(ranks), cores, x
+
+
+def random_tt_vector(seed: int, d: int, max_rank: int, ranks=None):
+    """A random TT vector (cores (r_{k-1}, 2, r_k), scaled 1/sqrt(2 r_{k-1})) for the
+    compressed matvec (PAPER section 4.2); returns (ranks, cores)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    if ranks is None:
+        ranks = rank_profile_random(rng, d, max_rank)
+    cores = []
+    for k in range(d):
+        g = rng.standard_normal((ranks[k], 2, ranks[k + 1])) / np.sqrt(2.0 * ranks[k])
+        cores.append(np.ascontiguousarray(g))
+    return list(ranks), cores
