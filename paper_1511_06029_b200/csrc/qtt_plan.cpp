@@ -94,12 +94,14 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
   // Wide variant: super-core streamed from L2 in k-chunks (qtt_wide_kernel.cu).
   const int nout = n_i * r_out;
   const double wbytes = 8.0 * sp->K * nout;
-  if (L >= 2 && sp->K % kWideBK == 0 && wbytes <= double(kWideMaxCoreBytes)) {
+  // (K need not be a multiple of the k-chunk: the TMA unit zero-fills the A
+  // columns past K and the packed W rows past K are zero.)
+  if (wbytes <= double(kWideMaxCoreBytes)) {
     const int NBw = nout <= 32 ? 4 : nout <= 64 ? 8 : nout <= 96 ? 12 : 16;
     const size_t smem = wide_smem_bytes(NBw);
     if (smem <= smem_optin) {
       const int ncb = (nout + 8 * NBw - 1) / (8 * NBw);
-      const double flops = 2.0 * M * sp->K * ncb * 8.0 * NBw;
+      const double flops = 2.0 * M * std::ceil(sp->K / double(kWideBK)) * kWideBK * ncb * 8.0 * NBw;
       const double tiles = std::ceil(M / kDmmaRowsPerSubtile) * ncb;
       const double u = std::min(1.0, tiles / kSms);
       const double l2 = tiles * (kDmmaRowsPerSubtile * 8.0 * sp->K + 8.0 * sp->K * 8.0 * NBw);
@@ -110,7 +112,7 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
         sp->KB = kWideKBC;
         sp->RP = r_out;
         sp->ncb = ncb;
-        sp->nchunks = sp->K / kWideBK;
+        sp->nchunks = (sp->K + kWideBK - 1) / kWideBK;
         sp->rep = 1;
         sp->stages = kWideStages;
         sp->smem = smem;

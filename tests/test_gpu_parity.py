@@ -98,11 +98,27 @@ def test_constant_rank_sweep(qtt, r):
 
 @pytest.mark.parametrize("maxL", [1, 6])
 def test_generic_path_large_rank(qtt, maxL):
-    ranks = [1, 2, 4, 70, 70, 70, 4, 2, 1]
-    _, cores, x = random_case(77, 8, 70, 2, ranks=ranks)
+    # r = 1501: the 3002 x 3002 super-core of level 3 exceeds the wide kernel's 64 MiB -> generic
+    ranks = [1, 2, 1501, 1501, 2, 1]
+    _, cores, x = random_case(77, 5, 1501, 2, ranks=ranks)
     y, stages = gpu_apply(qtt, cores, x, max_stage_levels=maxL)
     if maxL == 1:
         assert any(s["variant"] == "generic" for s in stages)
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
+
+
+# ------------------------------------------------------------------ large ranks (NEXT-4: r up to 256)
+@pytest.mark.parametrize("r", [56, 64, 96, 128, 200, 256])
+@pytest.mark.parametrize("maxL", [1, None])
+def test_large_rank_path(qtt, r, maxL):
+    """Ranks above the smem-resident instances run on the wide (streamed
+    super-core) kernel, one level per launch (maxL=1) or merged; never the
+    generic kernel up to r = 256."""
+    d = 11
+    ranks = [1] + [r] * (d - 1) + [1]
+    _, cores, x = random_case(1000 + r, d, r, 2, ranks=ranks)
+    y, stages = gpu_apply(qtt, cores, x, max_stage_levels=maxL)
+    assert all(s["variant"] != "generic" for s in stages), stages
     oracle.assert_close(y, oracle.apply_alg2(cores, x))
 
 

@@ -26,7 +26,10 @@ def check_cover(plan, d, max_levels):
     for a, b, v in plan:
         assert 1 <= b - a + 1 <= max_levels
         assert v in (0, 1, 2, 3)
-        assert (v in (2, 3)) == (b > a)     # merged / wide <=> more than one level
+        if v == 2:
+            assert b > a                    # merged: a super-core of several levels
+        if v in (0, 1):
+            assert b == a                   # generic / dmma: one level
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
@@ -36,7 +39,9 @@ def test_plan_covers_levels(q, name, maxL):
     plan = q.qtt_plan_stages(cfg.ranks, 0, maxL)
     check_cover(plan, cfg.d, maxL)
     if maxL == 1:
-        assert len(plan) == cfg.d and all(v == 1 for _, _, v in plan)
+        assert len(plan) == cfg.d and all(v in (1, 3) for _, _, v in plan)
+        if cfg.N >= 1 << 21:
+            assert all(v == 1 for _, _, v in plan)      # large N: smem-resident cores at r <= 48
 
 
 def test_c4_plan_merges_tapered_ends_only(q):
@@ -58,11 +63,19 @@ def test_small_problem_few_launches(q):
     assert len(q.qtt_plan_stages(cfg.ranks)) <= cfg.d // 2
 
 
-def test_large_rank_uses_generic_when_unmerged(q):
+def test_large_rank_levels_use_wide_kernel(q):
+    # r = 70: 2 r = 140 > the smem-resident instances -> streamed super-core ("wide"), never generic
     ranks = [1, 2, 4] + [70] * 6 + [4, 2, 1]
     plan = q.qtt_plan_stages(ranks, 0, 1)
-    assert [v for _, _, v in plan] == [1, 1] + [0] * 7 + [1, 1]
+    assert [v for _, _, v in plan][2:9] == [3] * 7
+    assert all(v in (1, 3) for _, _, v in plan)
     check_cover(q.qtt_plan_stages(ranks), len(ranks) - 1, 10)
+
+
+def test_huge_rank_falls_back_to_generic(q):
+    # r_in = r_out = 1501: the level's super-core (3002 x 3002 doubles) exceeds 64 MiB
+    plan = q.qtt_plan_stages([1, 2, 1501, 1501, 2, 1], 0, 1)
+    assert [v for _, _, v in plan] == [1, 3, 0, 3, 1]
 
 
 def test_rank_one_and_d1(q):
