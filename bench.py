@@ -294,6 +294,40 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
     out["morton_256cubed"] = {"pack_ms": mp, "unpack_ms": mu, "pack_gbs": 16 * N / (mp * 1e-3) / 1e9,
                               "unpack_gbs": 16 * N / (mu * 1e-3) / 1e9,
                               "pack_frac_hbm": 16 * N / (mp * 1e-3) / BW, "unpack_frac_hbm": 16 * N / (mu * 1e-3) / BW}
+    # NEXT-4a: large constant ranks (wide kernel, streamed super-cores)
+    from qtt_workload import random_case
+    for d_, r_ in ((20, 128), (18, 256)):
+        ranks = [1] + [r_] * (d_ - 1) + [1]
+        _, cores, x_np = random_case(4242, d_, r_, 1, ranks=ranks)
+        with q.QttOperator(cores) as op:
+            x = torch.from_numpy(x_np).to(dev)
+            y = torch.empty_like(x)
+            ws = torch.empty(op.workspace_size(1) // 8 + 64, dtype=torch.float64, device=dev)
+            med, _ = time_applies(lambda: op.apply(x, out=y, workspace=ws, stream=stream), 5, 2, stream)
+            st_ = op.stages()
+            rows, _, _ = stage_table(st_, ranks, 1 << d_, 1, [1.0] * len(st_), 1, P, BW)
+            Fx = sum(rr["flops_executed"] for rr in rows)
+            out[f"rank{r_}_d{d_}"] = {"ms_median": med, "gflops_alg2": op.flops_per_rhs / (med * 1e-3) / 1e9,
+                                      "tflops_executed": Fx / (med * 1e-3) / 1e12,
+                                      "frac_executed_fp64": Fx / (med * 1e-3) / P,
+                                      "stages": [[a["k_first"], a["k_last"], a["variant"]] for a in st_]}
+            del x, y, ws
+    # NEXT-3: compressed matvec (c4 operator x rank-4 TT vector) + GPU densify; the call synchronizes
+    from qtt_workload import random_tt_vector
+    _, cA, _ = generate("c4", with_x=False)
+    _, bv = random_tt_vector(11, 24, 4)
+    with q.QttOperator(cA) as A:
+        c = torch.empty(1 << 24, dtype=torch.float64, device=dev)
+        A.compressed_matvec(bv, out=c, stream=stream)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            A.compressed_matvec(bv, out=c, stream=stream)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        out["compressed_c4_x_rank4"] = {"ms_wall_median": statistics.median(ts),
+                                        "note": "host wall time of the synchronous call: b cores H2D, "
+                                                "product cores, GPU densify of the 2^24-entry result"}
+        del c
     # NEXT-1: product of two c4-profile operators, and the grid apply
     _, cM, xg = generate("c4")
     _, cY, _ = generate("c4", seed=1, with_x=False)

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -102,35 +103,76 @@ qtt_status_t from_cuda(cudaError_t e) {
 
 // Super-core of levels k0..k1 (PAPER Eq. TTdeccores P:519-523 restricted to the
 // stage's digits; qtt_plan.cpp): W[a][ii][jj][b], ii/jj = the stage's output /
-// input digits, first level least significant.  Accumulated in long double.
+// input digits, first level least significant.  Contracted from the narrow
+// end of the stage (the rank-1 side of a boundary stage): left to right costs
+// sum_l r_in 4^l r_l r_{l+1}, right to left sum_l r_l r_{l+1} 4^(L-l) r_out
+// multiply-adds; fp64 accumulation (R17), inner loops contiguous.
 std::vector<double> super_core(const double* const* cores, const int64_t* ranks, int k0, int k1) {
-  const int r0 = int(ranks[k0 - 1]);
-  std::vector<long double> W(cores[k0 - 1], cores[k0 - 1] + size_t(r0) * 4 * ranks[k0]);
+  const int L = k1 - k0 + 1;
+  const int64_t r_in = ranks[k0 - 1], r_out = ranks[k1];
+  double lr = 0, rl = 0;
+  for (int l = 1; l < L; ++l) {
+    lr += double(r_in) * std::ldexp(1.0, 2 * l) * double(ranks[k0 - 1 + l]) * double(ranks[k0 + l]);
+    rl += double(ranks[k1 - l - 1]) * double(ranks[k1 - l]) * std::ldexp(1.0, 2 * l) * double(r_out);
+  }
+  if (lr <= rl) {
+    // left to right: V[a][ii + n i][jj + n j][b] = sum_c W[a][ii][jj][c] G[c][i][j][b]
+    const int r0 = int(r_in);
+    std::vector<double> W(cores[k0 - 1], cores[k0 - 1] + size_t(r0) * 4 * ranks[k0]);
+    int n_i = 2;
+    int rc = int(ranks[k0]);
+    for (int k = k0 + 1; k <= k1; ++k) {
+      const double* G = cores[k - 1];
+      const int rb = int(ranks[k]);
+      const int n2 = 2 * n_i;
+      std::vector<double> V(size_t(r0) * n2 * n2 * rb, 0.0);
+      for (int a = 0; a < r0; ++a)
+        for (int ii = 0; ii < n_i; ++ii)
+          for (int jj = 0; jj < n_i; ++jj)
+            for (int c = 0; c < rc; ++c) {
+              const double w = W[((size_t(a) * n_i + ii) * n_i + jj) * rc + c];
+              if (w == 0.0) continue;
+              for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 2; ++j) {
+                  const double* g = G + ((size_t(c) * 2 + i) * 2 + j) * rb;
+                  double* v = &V[((size_t(a) * n2 + ii + n_i * i) * n2 + jj + n_i * j) * rb];
+                  for (int b = 0; b < rb; ++b) v[b] = std::fma(w, g[b], v[b]);
+                }
+            }
+      W.swap(V);
+      n_i = n2;
+      rc = rb;
+    }
+    return W;
+  }
+  // right to left: U[c][ii][jj][b] over levels k+1..k1; prepend level k as the
+  // least significant digit: V[a][i + 2 ii][j + 2 jj][b] = sum_c G_k[a][i][j][c] U[c][ii][jj][b]
+  const int ro = int(r_out);
+  std::vector<double> U(cores[k1 - 1], cores[k1 - 1] + size_t(ranks[k1 - 1]) * 4 * ro);
   int n_i = 2;
-  int rc = int(ranks[k0]);
-  for (int k = k0 + 1; k <= k1; ++k) {
+  for (int k = k1 - 1; k >= k0; --k) {
     const double* G = cores[k - 1];
-    const int rb = int(ranks[k]);
+    const int ra = int(ranks[k - 1]), rc = int(ranks[k]);
     const int n2 = 2 * n_i;
-    std::vector<long double> V(size_t(r0) * n2 * n2 * rb, 0.0L);
-    for (int a = 0; a < r0; ++a)
-      for (int ii = 0; ii < n_i; ++ii)
-        for (int jj = 0; jj < n_i; ++jj)
+    std::vector<double> V(size_t(ra) * n2 * n2 * ro, 0.0);
+    for (int a = 0; a < ra; ++a)
+      for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j)
           for (int c = 0; c < rc; ++c) {
-            const long double w = W[((size_t(a) * n_i + ii) * n_i + jj) * rc + c];
-            if (w == 0.0L) continue;
-            for (int i = 0; i < 2; ++i)
-              for (int j = 0; j < 2; ++j) {
-                const double* g = G + ((size_t(c) * 2 + i) * 2 + j) * rb;
-                long double* v = &V[((size_t(a) * n2 + ii + n_i * i) * n2 + jj + n_i * j) * rb];
-                for (int b = 0; b < rb; ++b) v[b] += w * g[b];
+            const double g = G[((size_t(a) * 2 + i) * 2 + j) * rc + c];
+            if (g == 0.0) continue;
+            const double* u = &U[size_t(c) * n_i * n_i * ro];
+            for (int ii = 0; ii < n_i; ++ii)
+              for (int jj = 0; jj < n_i; ++jj) {
+                double* v = &V[((size_t(a) * n2 + i + 2 * ii) * n2 + j + 2 * jj) * ro];
+                const double* uu = u + (size_t(ii) * n_i + jj) * ro;
+                for (int b = 0; b < ro; ++b) v[b] = std::fma(g, uu[b], v[b]);
               }
           }
-    W.swap(V);
+    U.swap(V);
     n_i = n2;
-    rc = rb;
   }
-  return std::vector<double>(W.begin(), W.end());
+  return U;
 }
 
 // B operand of a stage in MMA-fragment order (see qtt_dmma_kernel.cuh):

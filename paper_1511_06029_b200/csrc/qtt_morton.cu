@@ -11,8 +11,9 @@
 // element).  Tiled path: one CTA moves one aligned block of 2^12 consecutive
 // QTT indices = a 16^3 cube (dim 3) or 64^2 square (dim 2) of the grid,
 // reading/writing the grid side in full 128-byte (dim 3) or 512-byte (dim 2)
-// rows and the QTT side as one contiguous 32 KiB run, through a padded smem
-// tile.  Grids smaller than one tile use a per-element kernel.
+// rows and the QTT side as one contiguous 32 KiB run, through an XOR-swizzled
+// smem tile (bank-conflict free both ways), streaming loads/stores (.cs).
+// Grids smaller than one tile use a per-element kernel.
 #include "qtt_internal.h"
 
 #include <cstdint>
@@ -53,16 +54,25 @@ __global__ void morton_simple_kernel(const double* __restrict__ in, double* __re
 }
 
 // Tile of 2^12 consecutive QTT indices.  dim 3: 16 x 16 x 16 (4 bits per axis),
-// dim 2: 64 x 64 (6 bits per axis).  smem holds the tile in natural order with
-// rows of R doubles padded to R + 1.
+// dim 2: 64 x 64 (6 bits per axis).  smem holds the tile in natural order,
+// rows of R doubles, with x XOR-swizzled per row so that both access patterns
+// are bank-conflict free for 8-byte elements (each half-warp touching 16
+// distinct bank pairs): the grid side reads 16 consecutive x of one row; the
+// QTT side reads 16 consecutive local indices u, i.e. x in c + {0..3} on 4
+// rows that differ in (y_0, z_0) (dim 3) or (y_0, y_1) (dim 2) -- the swizzle
+// puts those 4 rows on 4 different 4-aligned x offsets.
+template <int DIM>
+__device__ __forceinline__ int swz(int row) {
+  if (DIM == 3) return 4 * ((row & 1) | (((row >> 4) & 1) << 1));   // row = z*16 + y: (y_0, z_0)
+  return 4 * (row & 3);                                               // row = y: (y_0, y_1)
+}
+
 template <int DIM, bool PACK>
 __global__ void __launch_bounds__(kThreads) morton_tile_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                                int levels, int64_t N) {
   constexpr int B = kTileBits / DIM;          // bits per axis inside the tile
   constexpr int R = 1 << B;                   // row length (x extent)
-  constexpr int ROWS = kTile / R;
-  constexpr int RP = R + 1;
-  __shared__ double tile[ROWS * RP];
+  __shared__ double tile[kTile];
 
   const int64_t tiles_per_rhs = N >> kTileBits;
   const int64_t s = blockIdx.x / tiles_per_rhs;
@@ -75,42 +85,47 @@ __global__ void __launch_bounds__(kThreads) morton_tile_kernel(const double* __r
   const int64_t gbase = s * N + (DIM == 3 ? (c0[2] * n + c0[1]) * n + c0[0] : c0[1] * n + c0[0]);
   const int64_t qbase = s * N + (tq << kTileBits);
 
-  // local natural (x, y[, z]) of local QTT index u
-  auto local_xyz = [](int u, int& x, int& y, int& z) {
-    x = y = z = 0;
+  // smem slot of local QTT index u
+  auto slot_of_u = [](int u) {
+    int x = 0, y = 0, z = 0;
 #pragma unroll
     for (int l = 0; l < B; ++l) {
       x |= ((u >> (DIM * l)) & 1) << l;
       y |= ((u >> (DIM * l + 1)) & 1) << l;
       if (DIM == 3) z |= ((u >> (DIM * l + 2)) & 1) << l;
     }
+    const int row = DIM == 3 ? z * R + y : y;
+    return row * R + (x ^ swz<DIM>(row));
+  };
+  // global offset (from gbase) and smem slot of the e-th element in natural order
+  auto grid_of_e = [n](int e, int64_t& goff, int& slot) {
+    const int x = e & (R - 1), row = e >> B;      // row = z*R + y (dim 3) or y (dim 2)
+    const int y = row & (R - 1), z = row >> B;
+    goff = (DIM == 3 ? (int64_t(z) * n + y) * n : int64_t(y) * n) + x;
+    slot = row * R + (x ^ swz<DIM>(row));
   };
 
   if (PACK) {
-    // grid rows -> smem (coalesced rows of R doubles)
+#pragma unroll 4
     for (int e = threadIdx.x; e < kTile; e += kThreads) {
-      const int x = e & (R - 1), row = e >> B;      // row = z*R + y (dim 3) or y (dim 2)
-      const int y = row & (R - 1), z = row >> B;
-      const double* src = in + gbase + (DIM == 3 ? (int64_t(z) * n + y) * n : int64_t(y) * n) + x;
-      tile[row * RP + x] = *src;
+      int64_t goff;
+      int slot;
+      grid_of_e(e, goff, slot);
+      tile[slot] = __ldcs(in + gbase + goff);
     }
     __syncthreads();
-    for (int u = threadIdx.x; u < kTile; u += kThreads) {
-      int x, y, z;
-      local_xyz(u, x, y, z);
-      out[qbase + u] = tile[(z * R + y) * RP + x];
-    }
+#pragma unroll 4
+    for (int u = threadIdx.x; u < kTile; u += kThreads) __stcs(out + qbase + u, tile[slot_of_u(u)]);
   } else {
-    for (int u = threadIdx.x; u < kTile; u += kThreads) {
-      int x, y, z;
-      local_xyz(u, x, y, z);
-      tile[(z * R + y) * RP + x] = in[qbase + u];
-    }
+#pragma unroll 4
+    for (int u = threadIdx.x; u < kTile; u += kThreads) tile[slot_of_u(u)] = __ldcs(in + qbase + u);
     __syncthreads();
+#pragma unroll 4
     for (int e = threadIdx.x; e < kTile; e += kThreads) {
-      const int x = e & (R - 1), row = e >> B;
-      const int y = row & (R - 1), z = row >> B;
-      out[gbase + (DIM == 3 ? (int64_t(z) * n + y) * n : int64_t(y) * n) + x] = tile[row * RP + x];
+      int64_t goff;
+      int slot;
+      grid_of_e(e, goff, slot);
+      __stcs(out + gbase + goff, tile[slot]);
     }
   }
 }
