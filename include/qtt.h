@@ -213,6 +213,37 @@ qtt_status_t qtt_compressed_matvec_cores(qtt_handle_t h, const int64_t* b_ranks,
                                          const double* const* b_cores, double* c_cores,
                                          size_t c_cores_bytes, int64_t* c_ranks, qtt_stream_t stream);
 
+/*
+ * Top-bit sharding over P = 2^s GPUs (NEXT-4).  Split x and y
+ * into P contiguous blocks of n = N/P entries by the top s index bits (in
+ * Morton order: octree subdomains).  Levels 1..d-s pair only bits inside a
+ * block (Alg. 2 level k touches digit k), so part g applies them
+ * to its own block x_g, giving T_g[m][alpha] (n x r_{d-s}, natural row order);
+ * then it projects onto every output block h with
+ *   c_{h,g}[alpha] = G_{d-s+1}(alpha, h_1 g_1, :) ... G_d(:, h_s g_s, 0)
+ * (the QTT definition P:519-523 on the top s digits), and
+ *   y_h = sum_g T_g c_{h,g}         -- one ReduceScatter (sum) over the parts.
+ *   qtt_create_shard   : plan part `part` (0 <= part < 2^log2_parts, 1 <= log2_parts < d)
+ *                        of the operator; cores/ranks as qtt_create (all d cores).
+ *                        The handle's qtt_get_info reports the LOCAL d - s and n.
+ *   qtt_shard_apply[_ws]: x_local (DEVICE, n x nrhs column-major) -> send (DEVICE,
+ *                        nrhs blocks of [P][n]: send[s][h][m] = (T_g c_{h,g})[m] of RHS s);
+ *                        the caller reduce-scatters block h to part h (per RHS),
+ *                        e.g. NCCL through torch.distributed.  Workspace as
+ *                        qtt_workspace_size(h, nrhs).  qtt_apply on a shard handle
+ *                        returns QTT_ERROR_INVALID_VALUE.
+ *   qtt_shard_projection: HOST only (no GPU): writes W[h * r + alpha] = c_{h,part}[alpha],
+ *                        P x r_{d-s} doubles.
+ */
+qtt_status_t qtt_create_shard(qtt_handle_t* out, int d, const int64_t* ranks, const double* const* cores,
+                              int log2_parts, int part);
+qtt_status_t qtt_shard_apply(qtt_handle_t h, const double* x_local, double* send, int64_t nrhs,
+                             qtt_stream_t stream);
+qtt_status_t qtt_shard_apply_ws(qtt_handle_t h, const double* x_local, double* send, int64_t nrhs,
+                                void* ws, size_t ws_bytes, qtt_stream_t stream);
+qtt_status_t qtt_shard_projection(int d, const int64_t* ranks, const double* const* cores, int log2_parts,
+                                  int part, double* W);
+
 /* Plan facts: d, N, max rank, algorithmic flops per right-hand side
  * (4 * sum_k r_{k-1} r_k * N) and the number of kernel
  * launches one apply enqueues.  Any output pointer may be NULL. */

@@ -23,6 +23,7 @@ SYMBOLS = (
     "qtt_stage_times", "qtt_destroy", "qtt_morton_pack", "qtt_morton_unpack", "qtt_apply_grid",
     "qtt_product_create", "qtt_product_workspace_size", "qtt_product_apply", "qtt_product_apply_ws",
     "qtt_product_destroy", "qtt_compressed_matvec", "qtt_compressed_matvec_cores",
+    "qtt_create_shard", "qtt_shard_apply", "qtt_shard_apply_ws", "qtt_shard_projection",
 )
 
 _lib = None
@@ -88,6 +89,14 @@ def load():
     lib.qtt_compressed_matvec_cores.restype = st
     lib.qtt_compressed_matvec_cores.argtypes = [h, C.POINTER(i64), C.POINTER(C.c_void_p), dp, C.c_size_t,
                                                 C.POINTER(i64), C.c_void_p]
+    lib.qtt_create_shard.restype = st
+    lib.qtt_create_shard.argtypes = [C.POINTER(h), C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.c_int, C.c_int]
+    lib.qtt_shard_apply.restype = st
+    lib.qtt_shard_apply.argtypes = [h, dp, dp, i64, C.c_void_p]
+    lib.qtt_shard_apply_ws.restype = st
+    lib.qtt_shard_apply_ws.argtypes = [h, dp, dp, i64, dp, C.c_size_t, C.c_void_p]
+    lib.qtt_shard_projection.restype = st
+    lib.qtt_shard_projection.argtypes = [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.c_int, C.c_int, dp]
     lib.qtt_destroy.restype = st
     lib.qtt_destroy.argtypes = [h]
     _lib = lib

@@ -47,6 +47,11 @@ struct qtt_plan {
   std::vector<int64_t> ranks;
   std::vector<Stage> stages;
   std::vector<double*> d_raw;      // raw cores G_k [a][i][j][b] (compressed matvec)
+  // top-bit shard (qtt_create_shard): the handle's d, N, ranks, stages are the
+  // local levels 1..d-s; `proj` maps their output onto the 2^s output blocks
+  int shard_bits = 0;
+  int shard_part = 0;
+  Stage proj;
   int64_t max_interior_rank = 0;
   // cached workspace (qtt_apply)
   void* ws = nullptr;
@@ -176,35 +181,38 @@ std::vector<double> super_core(const double* const* cores, const int64_t* ranks,
 }
 
 // B operand of a stage in MMA-fragment order (see qtt_dmma_kernel.cuh):
-//   Bmat[kk][n], kk = jj*r_in + a (the column-merged index of Alg. 2 line 6),
-//   n = ii*RP + b (the row-separated output, Alg. 2 line 8), value W[a,ii,jj,b];
-//   pack[kb][nb][lane][v] = Bmat[kb*16 + 4*(lane%4) + v][nb*8 + lane/4].
-std::vector<double> pack_dmma(const double* W, const qtt::StagePlan& sp) {
-  const int KB = sp.KB, NB = sp.NB, RP = sp.RP, r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i;
+//   pack[kb][nb][lane][v] = Bmat(kb*16 + 4*(lane%4) + v, nb*8 + lane/4)
+// Bmat(kk, n) returns the GEMM operand (0 for padding).
+template <class F>
+std::vector<double> pack_dmma_fn(const qtt::StagePlan& sp, F bmat) {
+  const int KB = sp.KB, NB = sp.NB;
   std::vector<double> out(size_t(KB) * NB * 32 * 4, 0.0);
   for (int kb = 0; kb < KB; ++kb)
     for (int nb = 0; nb < NB; ++nb)
       for (int lane = 0; lane < 32; ++lane)
-        for (int v = 0; v < 4; ++v) {
-          const int kk = kb * 16 + 4 * (lane % 4) + v;
-          const int n = nb * 8 + lane / 4;
-          double val = 0.0;
-          if (kk < sp.K) {
-            const int jj = kk / r_in, a = kk % r_in;
-            const int ii = n / RP, b = n % RP;
-            if (ii < n_i && b < r_out) val = W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b];
-          }
-          out[((size_t(kb) * NB + nb) * 32 + lane) * 4 + v] = val;
-        }
+        for (int v = 0; v < 4; ++v)
+          out[((size_t(kb) * NB + nb) * 32 + lane) * 4 + v] = bmat(kb * 16 + 4 * (lane % 4) + v, nb * 8 + lane / 4);
   return out;
 }
 
-// Super-core of a wide stage, streamed by k-chunk (qtt_wide_kernel.cu):
-//   pack[cb][ch][kb][nb][lane][v] = Bmat[ch*BK + kb*16 + 4*(lane%4) + v][(cb*NB + nb)*8 + lane/4]
-// with Bmat[jj*r_in + a][ii*r_out + b] = W[a,ii,jj,b] (no column padding per ii).
-std::vector<double> pack_wide(const double* W, const qtt::StagePlan& sp) {
-  const int NB = sp.NB, r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i;
-  const int nout = n_i * r_out;
+// Stage super-core W[a][ii][jj][b] as the DMMA B operand:
+//   Bmat[kk][n], kk = jj*r_in + a (the column-merged index of Alg. 2 line 6),
+//   n = ii*RP + b (the row-separated output, Alg. 2 line 8), value W[a,ii,jj,b].
+std::vector<double> pack_dmma(const double* W, const qtt::StagePlan& sp) {
+  const int RP = sp.RP, r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i, K = sp.K;
+  return pack_dmma_fn(sp, [=](int kk, int n) {
+    if (kk >= K) return 0.0;
+    const int jj = kk / r_in, a = kk % r_in;
+    const int ii = n / RP, b = n % RP;
+    return (ii < n_i && b < r_out) ? W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b] : 0.0;
+  });
+}
+
+// B operand of a wide stage, streamed by k-chunk (qtt_wide_kernel.cu):
+//   pack[cb][ch][kb][nb][lane][v] = Bmat(ch*BK + kb*16 + 4*(lane%4) + v, (cb*NB + nb)*8 + lane/4)
+template <class F>
+std::vector<double> pack_wide_fn(const qtt::StagePlan& sp, F bmat) {
+  const int NB = sp.NB;
   const size_t chunk = size_t(qtt::kWideKBC) * NB * 32 * 4;
   std::vector<double> out(size_t(sp.ncb) * sp.nchunks * chunk, 0.0);
   for (int cb = 0; cb < sp.ncb; ++cb)
@@ -212,18 +220,49 @@ std::vector<double> pack_wide(const double* W, const qtt::StagePlan& sp) {
       for (int kb = 0; kb < qtt::kWideKBC; ++kb)
         for (int nb = 0; nb < NB; ++nb)
           for (int lane = 0; lane < 32; ++lane)
-            for (int v = 0; v < 4; ++v) {
-              const int kk = ch * qtt::kWideBK + kb * 16 + 4 * (lane % 4) + v;
-              const int n = (cb * NB + nb) * 8 + lane / 4;
-              double val = 0.0;
-              if (kk < sp.K && n < nout) {
-                const int jj = kk / r_in, a = kk % r_in;
-                const int ii = n / r_out, b = n % r_out;
-                val = W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b];
-              }
-              out[(size_t(cb) * sp.nchunks + ch) * chunk + ((size_t(kb) * NB + nb) * 32 + lane) * 4 + v] = val;
-            }
+            for (int v = 0; v < 4; ++v)
+              out[(size_t(cb) * sp.nchunks + ch) * chunk + ((size_t(kb) * NB + nb) * 32 + lane) * 4 + v] =
+                  bmat(ch * qtt::kWideBK + kb * 16 + 4 * (lane % 4) + v, (cb * NB + nb) * 8 + lane / 4);
   return out;
+}
+
+// Wide stage: Bmat[jj*r_in + a][ii*r_out + b] = W[a,ii,jj,b] (no column padding per ii).
+std::vector<double> pack_wide(const double* W, const qtt::StagePlan& sp) {
+  const int r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i, K = sp.K, nout = sp.n_i * sp.r_out;
+  return pack_wide_fn(sp, [=](int kk, int n) {
+    if (kk >= K || n >= nout) return 0.0;
+    const int jj = kk / r_in, a = kk % r_in;
+    const int ii = n / r_out, b = n % r_out;
+    return W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b];
+  });
+}
+
+// Top-bit sharding: projection vectors of part g onto every
+// output block h, c_{h,g}[alpha] = [G_{d-s+1}(alpha, h_1, g_1, :) ... G_d(:, h_s, g_s, 0)],
+// written as Wp[h * r + alpha], r = ranks[d-s].
+std::vector<double> shard_projection(int d, const int64_t* ranks, const double* const* cores, int s, int g) {
+  const int P = 1 << s;
+  const int r = int(ranks[d - s]);
+  std::vector<double> Wp(size_t(P) * r, 0.0);
+  for (int h = 0; h < P; ++h) {
+    // right to left: v over the bond below level k
+    std::vector<double> v(1, 1.0);
+    for (int l = s; l >= 1; --l) {
+      const int k = d - s + l;                       // 1-based level
+      const int hb = (h >> (l - 1)) & 1, gb = (g >> (l - 1)) & 1;
+      const int ra = int(ranks[k - 1]), rb = int(ranks[k]);
+      const double* G = cores[k - 1];
+      std::vector<double> u(ra, 0.0);
+      for (int a = 0; a < ra; ++a) {
+        double acc = 0.0;
+        for (int b = 0; b < rb; ++b) acc = std::fma(G[((size_t(a) * 2 + hb) * 2 + gb) * rb + b], v[b], acc);
+        u[a] = acc;
+      }
+      v.swap(u);
+    }
+    for (int a = 0; a < r; ++a) Wp[size_t(h) * r + a] = v[a];
+  }
+  return Wp;
 }
 
 bool is_device_ptr(const void* p) {
@@ -241,7 +280,7 @@ bool is_device_ptr(const void* p) {
 constexpr size_t kWsHeader = 256;
 
 size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs) {
-  if (h->stages.size() <= 1) return 0;
+  if (h->stages.size() <= 1 && h->shard_bits == 0) return 0;
   const size_t one = size_t(h->max_interior_rank) * size_t(h->N) * size_t(nrhs) * sizeof(double);
   return (one + 255) / 256 * 256;
 }
@@ -255,6 +294,7 @@ void free_plan(qtt_plan* h) {
   }
   for (double* p : h->d_raw)
     if (p) cudaFree(p);
+  if (h->proj.d_bpack) cudaFree(h->proj.d_bpack);
   if (h->ws) cudaFree(h->ws);
   if (h->gx) cudaFree(h->gx);
   if (h->gy) cudaFree(h->gy);
@@ -314,12 +354,14 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
   cudaError_t me = cudaMemsetAsync(counters, 0, kWsHeader, st);
   if (me != cudaSuccess) return from_cuda(me);
   const double* in = x;
-  const int ns = int(h->stages.size());
+  const int nloc = int(h->stages.size());
+  const int ns = nloc + (h->shard_bits ? 1 : 0);
   for (int si = 0; si < ns; ++si) {
-    const Stage& S = h->stages[si];
+    const bool proj = si == nloc;                  // shard projection stage
+    const Stage& S = proj ? h->proj : h->stages[si];
     const qtt::StagePlan& sp = S.plan;
     double* out = (si == ns - 1) ? y : buf[si & 1];
-    const int L = sp.k1 - sp.k0 + 1;
+    const int L = proj ? 0 : sp.k1 - sp.k0 + 1;
     LevelArgs a;
     a.in = in;
     a.out = out;
@@ -340,7 +382,7 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
     a.stages = sp.stages;
     a.smem = sp.smem;
     StageEvents ev{};
-    if (h->timing) {
+    if (h->timing && !proj) {
       ev.stage = si;
       if (cudaEventCreate(&ev.start) != cudaSuccess || cudaEventCreate(&ev.stop) != cudaSuccess)
         return QTT_ERROR_CUDA;
@@ -368,7 +410,7 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
                      si, sp.k0, sp.k1, sp.variant, sp.KB, sp.NB, a.smem, a.grid, cudaGetErrorString(e));
       return from_cuda(e);
     }
-    if (h->timing) {
+    if (h->timing && !proj) {
       cudaEventRecord(ev.stop, st);
       h->pending.push_back(ev);
     }
@@ -381,6 +423,7 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
 
 qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs) {
   if (!h || !x || !y || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  if (h->shard_bits) return QTT_ERROR_INVALID_VALUE;   // shard handles use qtt_shard_apply
   if (nrhs > (int64_t(1) << 40) / h->N) return QTT_ERROR_INVALID_VALUE;
   const uintptr_t xs = reinterpret_cast<uintptr_t>(x), ys = reinterpret_cast<uintptr_t>(y);
   const uintptr_t bytes = uintptr_t(h->N) * uintptr_t(nrhs) * sizeof(double);
@@ -409,8 +452,8 @@ qtt_status_t qtt_create(qtt_handle_t* out, int d, const int64_t* ranks, const do
   return qtt_create_ex(out, d, ranks, cores, qtt::kMaxStageLevels);
 }
 
-qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks, const double* const* cores,
-                           int max_stage_levels) {
+static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, const double* const* cores,
+                                int max_stage_levels, int shard_bits, int shard_part) {
   if (!out) return QTT_ERROR_INVALID_VALUE;
   *out = nullptr;
   if (d < 1 || d > 30 || !ranks || !cores || max_stage_levels < 1) return QTT_ERROR_INVALID_VALUE;
@@ -419,6 +462,8 @@ qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks, const
     if (ranks[k] < 1 || ranks[k] > 4096) return QTT_ERROR_INVALID_VALUE;
   for (int k = 0; k < d; ++k)
     if (!cores[k]) return QTT_ERROR_INVALID_VALUE;
+  if (shard_bits < 0 || shard_bits >= d || shard_part < 0 || shard_part >= (1 << shard_bits))
+    return QTT_ERROR_INVALID_VALUE;
   qtt_plan* h = nullptr;
   try {
     h = new qtt_plan();
@@ -441,21 +486,54 @@ qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks, const
   }
   h->num_sms = prop.multiProcessorCount;
   h->smem_optin = prop.sharedMemPerBlockOptin;
-  h->d = d;
-  h->N = int64_t(1) << d;
-  h->ranks.assign(ranks, ranks + d + 1);
+  // a shard applies the local levels 1..d-s; the rest is its projection
+  const int dl = d - shard_bits;
+  h->shard_bits = shard_bits;
+  h->shard_part = shard_part;
+  h->d = dl;
+  h->N = int64_t(1) << dl;
+  h->ranks.assign(ranks, ranks + dl + 1);
   qtt_status_t st = QTT_SUCCESS;
   try {
-    const std::vector<qtt::StagePlan> plan = qtt::plan_stages(d, ranks, h->smem_optin, max_stage_levels);
+    const std::vector<qtt::StagePlan> plan = qtt::plan_stages(dl, ranks, h->smem_optin, max_stage_levels);
     h->stages.resize(plan.size());
     for (size_t s = 0; s < plan.size(); ++s) {
       h->stages[s].plan = plan[s];
-      // the intermediate buffers hold only stage-boundary ranks
-      if (s + 1 < plan.size()) h->max_interior_rank = std::max<int64_t>(h->max_interior_rank, plan[s].r_out);
+      // the intermediate buffers hold only stage-boundary ranks (and a shard's local output)
+      if (s + 1 < plan.size() || shard_bits)
+        h->max_interior_rank = std::max<int64_t>(h->max_interior_rank, plan[s].r_out);
     }
     for (size_t s = 0; s < plan.size() && st == QTT_SUCCESS; ++s) st = upload_stage(h, h->stages[s], cores);
-    h->d_raw.assign(d, nullptr);
-    for (int k = 0; k < d && st == QTT_SUCCESS; ++k) {
+    if (st == QTT_SUCCESS && shard_bits) {
+      qtt::StagePlan& pp = h->proj.plan;
+      const int r = int(ranks[dl]), P = 1 << shard_bits;
+      if (!qtt::projection_plan(r, shard_bits, h->smem_optin, &pp)) {
+        st = QTT_ERROR_NOT_SUPPORTED;
+      } else {
+        const std::vector<double> Wp = shard_projection(d, ranks, cores, shard_bits, shard_part);
+        std::vector<double> pk;
+        cudaError_t e;
+        if (pp.variant == qtt::kWide) {
+          e = qtt::wide_prepare(pp.NB, h->smem_optin);
+          h->proj.ctas_per_sm = 1;
+          pk = pack_wide_fn(pp, [&](int kk, int n) { return (kk < r && n < P) ? Wp[size_t(n) * r + kk] : 0.0; });
+        } else {
+          e = qtt::dmma_prepare(pp.KB, pp.NB, h->smem_optin);
+          int occ = 0;
+          if (e == cudaSuccess) e = qtt::dmma_occupancy(pp.KB, pp.NB, pp.smem, &occ);
+          h->proj.ctas_per_sm = std::max(1, occ);
+          pk = pack_dmma_fn(pp, [&](int kk, int n) {
+            return (kk < r && n / 2 < P && n % 2 == 0) ? Wp[size_t(n / 2) * r + kk] : 0.0;
+          });
+        }
+        if (e == cudaSuccess) e = cudaMalloc(&h->proj.d_bpack, pk.size() * sizeof(double));
+        if (e == cudaSuccess)
+          e = cudaMemcpy(h->proj.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice);
+        st = from_cuda(e);
+      }
+    }
+    h->d_raw.assign(dl, nullptr);
+    for (int k = 0; k < dl && st == QTT_SUCCESS; ++k) {
       const size_t bytes = size_t(ranks[k]) * 4 * ranks[k + 1] * sizeof(double);
       cudaError_t e = cudaMalloc(&h->d_raw[k], bytes);
       if (e == cudaSuccess) e = cudaMemcpy(h->d_raw[k], cores[k], bytes, cudaMemcpyHostToDevice);
@@ -473,6 +551,89 @@ qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks, const
   }
   h->stage_ms.assign(h->stages.size(), 0.0);
   *out = h;
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks, const double* const* cores,
+                           int max_stage_levels) {
+  return create_impl(out, d, ranks, cores, max_stage_levels, 0, 0);
+}
+
+qtt_status_t qtt_create_shard(qtt_handle_t* out, int d, const int64_t* ranks, const double* const* cores,
+                              int log2_parts, int part) {
+  if (log2_parts < 1) return QTT_ERROR_INVALID_VALUE;
+  return create_impl(out, d, ranks, cores, qtt::kMaxStageLevels, log2_parts, part);
+}
+
+static qtt_status_t check_shard_args(qtt_plan* h, const double* x, const double* send, int64_t nrhs) {
+  if (!h || !x || !send || nrhs < 1 || h->shard_bits == 0) return QTT_ERROR_INVALID_VALUE;
+  if (nrhs > (int64_t(1) << 40) / (h->N << h->shard_bits)) return QTT_ERROR_INVALID_VALUE;
+  const uintptr_t xs = reinterpret_cast<uintptr_t>(x), ys = reinterpret_cast<uintptr_t>(send);
+  const uintptr_t xb = uintptr_t(h->N) * uintptr_t(nrhs) * sizeof(double);
+  const uintptr_t yb = xb << h->shard_bits;
+  if (xs < ys + yb && ys < xs + xb) return QTT_ERROR_INVALID_VALUE;
+  if ((xs % 16) || (ys % 16)) return QTT_ERROR_NOT_SUPPORTED;
+  if (!is_device_ptr(x) || !is_device_ptr(send)) return QTT_ERROR_NOT_SUPPORTED;
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_shard_apply_ws(qtt_handle_t h, const double* x_local, double* send, int64_t nrhs, void* ws,
+                                size_t ws_bytes, qtt_stream_t stream) {
+  qtt_status_t s = check_shard_args(h, x_local, send, nrhs);
+  if (s != QTT_SUCCESS) return s;
+  if (!ws || ws_bytes < ws_bytes_for(h, nrhs)) return QTT_ERROR_INVALID_VALUE;
+  if (reinterpret_cast<uintptr_t>(ws) % 256) return QTT_ERROR_NOT_SUPPORTED;
+  if (!is_device_ptr(ws)) return QTT_ERROR_NOT_SUPPORTED;
+  try {
+    DeviceGuard g(h->device);
+    return enqueue(h, x_local, send, nrhs, ws, reinterpret_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_shard_apply(qtt_handle_t h, const double* x_local, double* send, int64_t nrhs,
+                             qtt_stream_t stream) {
+  qtt_status_t s = check_shard_args(h, x_local, send, nrhs);
+  if (s != QTT_SUCCESS) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  try {
+    DeviceGuard g(h->device);
+    const size_t need = ws_bytes_for(h, nrhs);
+    if (need > h->ws_bytes) {
+      if (h->ws) cudaFreeAsync(h->ws, h->ws_stream);
+      h->ws = nullptr;
+      h->ws_bytes = 0;
+      cudaError_t e = cudaMallocAsync(&h->ws, need, st);
+      if (e != cudaSuccess) {
+        h->ws = nullptr;
+        return from_cuda(e);
+      }
+      h->ws_bytes = need;
+      h->ws_stream = st;
+    }
+    return enqueue(h, x_local, send, nrhs, h->ws, st);
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_shard_projection(int d, const int64_t* ranks, const double* const* cores, int log2_parts,
+                                  int part, double* W) {
+  if (d < 2 || d > 30 || !ranks || !cores || !W || log2_parts < 1 || log2_parts >= d || part < 0 ||
+      part >= (1 << log2_parts))
+    return QTT_ERROR_INVALID_VALUE;
+  if (ranks[0] != 1 || ranks[d] != 1) return QTT_ERROR_INVALID_VALUE;
+  for (int k = 0; k <= d; ++k)
+    if (ranks[k] < 1 || ranks[k] > 4096) return QTT_ERROR_INVALID_VALUE;
+  for (int k = d - log2_parts; k < d; ++k)
+    if (!cores[k]) return QTT_ERROR_INVALID_VALUE;
+  try {
+    const std::vector<double> Wp = shard_projection(d, ranks, cores, log2_parts, part);
+    std::copy(Wp.begin(), Wp.end(), W);
+  } catch (...) {
+    return QTT_ERROR_OUT_OF_MEMORY;
+  }
   return QTT_SUCCESS;
 }
 
@@ -614,7 +775,7 @@ qtt_status_t qtt_apply_grid(qtt_handle_t h, const double* grid_in, double* grid_
 static qtt_status_t compressed_common(qtt_handle_t h, const int64_t* b_ranks, const double* const* b_cores,
                                       double* c_dense, double* c_cores, size_t c_cores_bytes, int64_t* c_ranks,
                                       qtt_stream_t stream) {
-  if (!h || !b_ranks || !b_cores) return QTT_ERROR_INVALID_VALUE;
+  if (!h || !b_ranks || !b_cores || h->shard_bits) return QTT_ERROR_INVALID_VALUE;
   const int d = h->d;
   if (b_ranks[0] != 1 || b_ranks[d] != 1) return QTT_ERROR_INVALID_VALUE;
   for (int k = 0; k <= d; ++k)
@@ -806,11 +967,17 @@ qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank,
     for (int k = 0; k < h->d; ++k) s += double(h->ranks[k]) * double(h->ranks[k + 1]);
     *flops_per_rhs = 4.0 * s * double(h->N);
   }
-  if (launches_per_apply) *launches_per_apply = int(h->stages.size());
+  if (launches_per_apply) *launches_per_apply = int(h->stages.size()) + (h->shard_bits ? 1 : 0);
   return QTT_SUCCESS;
 }
 
 qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int* variant) {
+  if (h && h->shard_bits && s == int(h->stages.size())) {   // a shard's projection launch
+    if (k_first) *k_first = h->d + 1;
+    if (k_last) *k_last = h->d + h->shard_bits;
+    if (variant) *variant = h->proj.plan.variant;
+    return QTT_SUCCESS;
+  }
   if (!h || s < 0 || s >= int(h->stages.size())) return QTT_ERROR_INVALID_VALUE;
   if (k_first) *k_first = h->stages[s].plan.k0;
   if (k_last) *k_last = h->stages[s].plan.k1;

@@ -96,6 +96,7 @@ size_t dmma_smem_bytes(int KB, int NB, int K, int rep, int stages);
 // Tiling of a DMMA stage; false if it does not fit smem_optin.
 bool dmma_tiling(int K, int KB, int NB, size_t smem_optin, int* rep, int* stages, size_t* smem);
 std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels);
+bool projection_plan(int r, int s, size_t smem_optin, StagePlan* sp);
 
 cudaError_t dmma_prepare(int KB, int NB, size_t smem);   // sets the max dynamic smem attribute
 cudaError_t dmma_occupancy(int KB, int NB, size_t smem, int* ctas_per_sm);

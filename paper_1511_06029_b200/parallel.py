@@ -1,0 +1,190 @@
+"""Multi-GPU QTT apply by top-bit sharding (NEXT-4).
+
+One process per GPU.  With P = 2^s ranks, x and y are split into P contiguous
+blocks of n = N/P entries by the top s index bits (Morton order: octree
+subdomains).  Rank g runs its shard plan (``qtt_create_shard``): Alg. 2's
+levels 1..d-s on its own block (they never pair bits across blocks,
+PAPER.md P:1487-1496) and a projection of the result onto all P output
+blocks with the top s cores, all in the library's kernels.  The one exchange
+is a sum ReduceScatter of the [P][n] send buffers (NCCL over NVLink through
+torch.distributed; plumbing only).
+
+This module holds argument marshalling and the collective call; every flop
+runs in libqtt_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from . import _marshal_cores, _ptr, _stream_handle, QttOperator
+
+__all__ = ["ShardedQttOperator", "QttShard", "shard_projection", "exchange", "block_of"]
+
+
+def shard_projection(cores, log2_parts: int, part: int) -> np.ndarray:
+    """Host-only: c_{h,part} for every output block h, shape (P, r_{d-s})
+    (``qtt_shard_projection``; no GPU needed)."""
+    arrs, ranks = _marshal_cores(cores, None)
+    d = len(arrs)
+    P = 1 << log2_parts
+    r = ranks[d - log2_parts]
+    out = np.empty((P, r), dtype=np.float64)
+    _lib.check("qtt_shard_projection", _lib.load().qtt_shard_projection(
+        d, (C.c_int64 * (d + 1))(*ranks), (C.c_void_p * d)(*[a.ctypes.data for a in arrs]),
+        int(log2_parts), int(part), out.ctypes.data))
+    return out
+
+
+def block_of(x, part: int, parts: int):
+    """Rank `part`'s block of a full (nrhs, N) array: the entries whose top
+    log2(parts) index bits equal `part` (a contiguous slice)."""
+    n = x.shape[-1] // parts
+    return x[..., part * n:(part + 1) * n]
+
+
+def exchange(send, out, group=None):
+    """Sum-ReduceScatter of send [nrhs][P][n] into out [nrhs][n] (block = this rank).
+
+    NCCL: one reduce_scatter_tensor per RHS (block h of RHS s is contiguous).
+    Backends without reduce_scatter (gloo) fall back to all_reduce + slice."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    backend = dist.get_backend(group)
+    for s in range(send.shape[0]):
+        if backend == "nccl":
+            dist.reduce_scatter_tensor(out[s], send[s].reshape(-1), op=dist.ReduceOp.SUM, group=group)
+        else:
+            buf = send[s].clone()
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+            out[s].copy_(buf[rank])
+    return out
+
+
+class QttShard:
+    """Part `part` of 2^log2_parts of a QTT operator (``qtt_create_shard``): maps the
+    part's block of x to its [nrhs][P][n] send buffer.  No collective here."""
+
+    def __init__(self, cores, log2_parts: int, part: int):
+        self._h = None
+        arrs, ranks = _marshal_cores(cores, None)
+        self.d = len(arrs)
+        self.s = int(log2_parts)
+        self.part = int(part)
+        self.P = 1 << self.s
+        self.N = 1 << self.d
+        self.n = self.N >> self.s
+        self.ranks = ranks
+        h = C.c_void_p()
+        _lib.check("qtt_create_shard", _lib.load().qtt_create_shard(
+            C.byref(h), self.d, (C.c_int64 * (self.d + 1))(*ranks),
+            (C.c_void_p * self.d)(*[a.ctypes.data for a in arrs]), self.s, self.part))
+        self._h = int(h.value)
+
+    def workspace_size(self, nrhs: int = 1) -> int:
+        b = C.c_size_t()
+        _lib.check("qtt_workspace_size", _lib.load().qtt_workspace_size(self._h, int(nrhs), C.byref(b)))
+        return int(b.value)
+
+    def stages(self):
+        from . import qtt_get_info, qtt_get_stage
+        n = qtt_get_info(self._h)["launches_per_apply"]
+        return [qtt_get_stage(self._h, i) for i in range(n)]
+
+    def apply(self, x_local, send=None, stream=None, workspace=None):
+        import torch
+        xl = x_local if x_local.dim() == 2 else x_local.view(1, -1)
+        if xl.dtype != torch.float64 or not xl.is_cuda or not xl.is_contiguous() or xl.shape[-1] != self.n:
+            raise ValueError(f"x_local must be a contiguous float64 CUDA tensor with {self.n} columns")
+        nrhs = xl.shape[0]
+        if send is None:
+            send = torch.empty((nrhs, self.P, self.n), dtype=torch.float64, device=xl.device)
+        if workspace is None:
+            _lib.check("qtt_shard_apply", _lib.load().qtt_shard_apply(
+                self._h, _ptr(xl), _ptr(send), nrhs, _stream_handle(stream)))
+        else:
+            _lib.check("qtt_shard_apply_ws", _lib.load().qtt_shard_apply_ws(
+                self._h, _ptr(xl), _ptr(send), nrhs, _ptr(workspace),
+                workspace.numel() * workspace.element_size(), _stream_handle(stream)))
+        return send
+
+    def close(self):
+        if self._h is not None:
+            h, self._h = self._h, None
+            _lib.load().qtt_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class ShardedQttOperator:
+    """y = A x with x, y sharded by the top index bits over the ranks of `group`.
+
+    ``apply(x_local)`` takes this rank's block (shape (n,) or (nrhs, n)) and
+    returns this rank's block of y.  World size must be a power of two; with
+    one rank it is a plain QttOperator."""
+
+    def __init__(self, cores, group=None):
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world & (self.world - 1):
+            raise ValueError(f"world size {self.world} is not a power of two")
+        self.s = self.world.bit_length() - 1
+        arrs, ranks = _marshal_cores(cores, None)
+        self.d = len(arrs)
+        self.N = 1 << self.d
+        self.n = self.N >> self.s
+        self.flops_per_rhs = 4.0 * sum(ranks[k] * ranks[k + 1] for k in range(self.d)) * self.N
+        self._op = None
+        self._shard = None
+        if self.s == 0:
+            self._op = QttOperator(arrs)
+        else:
+            self._shard = QttShard(arrs, self.s, self.rank)
+
+    def workspace_size(self, nrhs: int = 1) -> int:
+        return (self._op or self._shard).workspace_size(nrhs)
+
+    def local_apply(self, x_local, send=None, stream=None, workspace=None):
+        """The kernel part only: this rank's [nrhs][P][n] send buffer."""
+        return self._shard.apply(x_local, send=send, stream=stream, workspace=workspace)
+
+    def apply(self, x_local, out=None, stream=None, workspace=None, send=None):
+        import torch
+        if self._op is not None:
+            return self._op.apply(x_local, out=out, stream=stream, workspace=workspace)
+        send = self.local_apply(x_local, send=send, stream=stream, workspace=workspace)
+        y = torch.empty((send.shape[0], self.n), dtype=torch.float64, device=send.device) if out is None else out
+        exchange(send, y.view(send.shape[0], self.n), self.group)
+        return y if x_local.dim() == 2 else y.view(-1)
+
+    def close(self):
+        for o in (self._op, self._shard):
+            if o is not None:
+                o.close()
+        self._op = self._shard = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
