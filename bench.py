@@ -377,6 +377,68 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- our arm
+def run_sharded(args, world, rank, local, dev, cfg, cores, x_np):
+    """One apply of the config sharded over `world` GPUs by the top index bits:
+    each rank runs its shard plan on its block, then one sum reduce-scatter
+    (NCCL).  value = Alg. 2 flops of the whole apply / max-over-ranks time."""
+    import torch
+    from paper_1511_06029_b200 import parallel as par
+    nrhs = cfg.nrhs
+    op = par.ShardedQttOperator(cores)
+    xb = torch.from_numpy(np.ascontiguousarray(par.block_of(x_np, rank, world))).to(dev)
+    send = torch.empty((nrhs, world, op.n), dtype=torch.float64, device=dev)
+    yb = torch.empty((nrhs, op.n), dtype=torch.float64, device=dev)
+    ws = torch.empty(op.workspace_size(nrhs) // 8 + 64, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    step = lambda: op.apply(xb, out=yb, workspace=ws, send=send, stream=stream)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        dist_barrier(world)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        dist_barrier(world)
+    ms_total = dist_max(e0.elapsed_time(e1), world, dev)
+    ms_step = ms_total / args.steps
+    flops = op.flops_per_rhs * nrhs
+    # e2e: this rank's block H2D, sharded apply, block D2H
+    xh = torch.from_numpy(np.ascontiguousarray(par.block_of(x_np, rank, world))).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    dist_barrier(world)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.e2e_steps):
+        xb.copy_(xh, non_blocking=True)
+        step()
+        yh.copy_(yb, non_blocking=True)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = dist_max(t0.elapsed_time(t1), world, dev) / args.e2e_steps
+    out = {"metric": METRIC, "value": flops * args.steps / (ms_total * 1e-3) / 1e9, "unit": UNIT,
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded; random cores with the config's rank profile)",
+           "config": dict(config_desc(cfg, nrhs), parallelism=f"top-bit shards x{world} + NCCL reduce-scatter"),
+           "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
+                   "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8)},
+           "gpu_launches": (len(op._shard.stages())) * args.steps,
+           "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(out))
+    op.close()
+    import torch.distributed as dist
+    dist.destroy_process_group()
+    return 0
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -390,6 +452,9 @@ def main(argv=None):
     ap.add_argument("--no-extra", action="store_true", help="skip the other configs / NEXT-row measurements")
     ap.add_argument("--max-stage-levels", type=int, default=None,
                     help="cap on levels per launch (1 = Alg. 2 level by level); default: the library's")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
+                    help="N>1: independent replicas (weak scaling, default) or one apply sharded by the "
+                         "top index bits with one NCCL reduce-scatter (strong scaling; DESIGN.md 9)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
@@ -406,6 +471,8 @@ def main(argv=None):
 
     cfg, cores, x_np = generate(args.config)
     nrhs = cfg.nrhs
+    if args.mode == "sharded" and world > 1:
+        return run_sharded(args, world, rank, local, dev, cfg, cores, x_np)
     op = q.QttOperator(cores, max_stage_levels=args.max_stage_levels)
     x = torch.from_numpy(x_np).to(dev)
     y = torch.empty_like(x)

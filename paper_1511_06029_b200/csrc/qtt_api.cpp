@@ -99,6 +99,7 @@ struct DeviceGuard {
 
 qtt_status_t from_cuda(cudaError_t e) {
   if (e == cudaSuccess) return QTT_SUCCESS;
+  if (std::getenv("QTT_DEBUG")) std::fprintf(stderr, "qtt: CUDA error %s\n", cudaGetErrorString(e));
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
     return QTT_ERROR_OUT_OF_MEMORY;
@@ -454,6 +455,8 @@ qtt_status_t qtt_create(qtt_handle_t* out, int d, const int64_t* ranks, const do
 
 static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, const double* const* cores,
                                 int max_stage_levels, int shard_bits, int shard_part) {
+  const int64_t* const full_ranks = ranks;
+  const double* const* const full_cores = cores;
   if (!out) return QTT_ERROR_INVALID_VALUE;
   *out = nullptr;
   if (d < 1 || d > 30 || !ranks || !cores || max_stage_levels < 1) return QTT_ERROR_INVALID_VALUE;
@@ -493,6 +496,21 @@ static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, 
   h->d = dl;
   h->N = int64_t(1) << dl;
   h->ranks.assign(ranks, ranks + dl + 1);
+  // A shard's local output T has rows of r_{d-s} doubles that the projection
+  // reads with 16-byte vector / TMA accesses: an odd r_{d-s} is padded by one
+  // zero bond column (an extra output of core d-s that is identically 0).
+  std::vector<const double*> lcores(cores, cores + d);
+  std::vector<double> padded;
+  if (shard_bits && (ranks[dl] % 2)) {
+    const int ra = int(ranks[dl - 1]), rb = int(ranks[dl]);
+    padded.assign(size_t(ra) * 4 * (rb + 1), 0.0);
+    for (size_t q = 0; q < size_t(ra) * 4; ++q)
+      std::copy(cores[dl - 1] + q * rb, cores[dl - 1] + (q + 1) * rb, padded.begin() + q * (rb + 1));
+    lcores[dl - 1] = padded.data();
+    h->ranks[dl] = rb + 1;
+  }
+  cores = lcores.data();
+  ranks = h->ranks.data();
   qtt_status_t st = QTT_SUCCESS;
   try {
     const std::vector<qtt::StagePlan> plan = qtt::plan_stages(dl, ranks, h->smem_optin, max_stage_levels);
@@ -506,11 +524,12 @@ static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, 
     for (size_t s = 0; s < plan.size() && st == QTT_SUCCESS; ++s) st = upload_stage(h, h->stages[s], cores);
     if (st == QTT_SUCCESS && shard_bits) {
       qtt::StagePlan& pp = h->proj.plan;
-      const int r = int(ranks[dl]), P = 1 << shard_bits;
-      if (!qtt::projection_plan(r, shard_bits, h->smem_optin, &pp)) {
+      const int rp = int(h->ranks[dl]), P = 1 << shard_bits;   // padded local top rank
+      const int r = int(full_ranks[dl]);
+      if (!qtt::projection_plan(rp, shard_bits, h->smem_optin, &pp)) {
         st = QTT_ERROR_NOT_SUPPORTED;
       } else {
-        const std::vector<double> Wp = shard_projection(d, ranks, cores, shard_bits, shard_part);
+        const std::vector<double> Wp = shard_projection(d, full_ranks, full_cores, shard_bits, shard_part);
         std::vector<double> pk;
         cudaError_t e;
         if (pp.variant == qtt::kWide) {
