@@ -281,7 +281,9 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
                          "per_stage_frac_executed": sum(
                              max(rr["flops_executed"] / P, (8 * cfg.N * cfg.nrhs * (rr["ranks"][0] + rr["ranks"][1])) / BW)
                              for rr in rows) / st_ if st_ else None,
-                         "stages": [[rr["levels"][0], rr["levels"][1], rr["variant"]] for rr in rows]}
+                         "stages": [[rr["levels"][0], rr["levels"][1], rr["variant"], round(rr["ms"], 4),
+                                     round(rr["roofline_frac_executed"] or 0, 3)] for rr in rows],
+                         "sum_stage_ms": sum(rr["ms"] for rr in rows)}
             del x, y, ws
         torch.cuda.empty_cache()
     # NEXT-2: Morton pack / unpack at 256^3 (16 bytes moved per element)

@@ -9,6 +9,8 @@ import ctypes as C
 import os
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqtt_b200.so")
+# A/B experiments may point at another in-tree build of the same library
+LIB_PATH = os.environ.get("QTT_LIB_PATH", LIB_PATH)
 
 QTT_SUCCESS = 0
 QTT_ERROR_INVALID_VALUE = 1

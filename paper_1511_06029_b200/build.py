@@ -13,8 +13,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libqtt_b200.so")
+OBJ = os.environ.get("QTT_OBJ_DIR", os.path.join(PKG, "build"))
+LIB = os.environ.get("QTT_LIB_OUT", os.path.join(PKG, "libqtt_b200.so"))
 
 SOURCES = ["qtt_dmma_inst_kb12.cu", "qtt_dmma_inst_kb34.cu", "qtt_dmma_inst_kb56.cu",
            "qtt_dmma_inst_kb78.cu", "qtt_wide_kernel.cu", "qtt_morton.cu", "qtt_compressed.cu", "qtt_level_dmma.cu", "qtt_plan.cpp", "qtt_api.cpp"]
@@ -23,6 +23,8 @@ HEADERS = ["qtt_internal.h", "qtt_dmma_kernel.cuh", os.path.join("..", "..", "in
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                   "-I" + os.path.join(ROOT, "include")]
+# experiment knobs (A/B builds): QTT_EXTRA_NVFLAGS="-DQTT_CG3_MIN_NB=6" QTT_LIB_OUT=path
+NVFLAGS += os.environ.get("QTT_EXTRA_NVFLAGS", "").split()
 
 
 def nvcc() -> str:

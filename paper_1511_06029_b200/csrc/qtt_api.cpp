@@ -67,6 +67,17 @@ struct qtt_plan {
   double* hy = nullptr;
   size_t h_elems = 0;
   cudaEvent_t last = nullptr;
+  // CUDA graphs of whole applies, keyed on (x, y, ws, nrhs): one cudaGraphLaunch
+  // replaces the memset + per-stage launches (latency-bound small problems)
+  struct Graph {
+    const double* x;
+    double* y;
+    void* ws;
+    int64_t nrhs;
+    cudaGraphExec_t exec;
+  };
+  std::vector<Graph> graphs;
+  cudaStream_t capture_stream = nullptr;
   bool timing = false;
   std::vector<StageEvents> pending;
   std::vector<double> stage_ms;
@@ -306,6 +317,8 @@ void free_plan(qtt_plan* h) {
     cudaEventDestroy(e.stop);
   }
   if (h->last) cudaEventDestroy(h->last);
+  for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+  if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   delete h;
 }
 
@@ -418,8 +431,51 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
     in = out;
   }
   if (h->timing) h->timed_applies++;
-  cudaEventRecord(h->last, st);
+  if (st != h->capture_stream) cudaEventRecord(h->last, st);
   return QTT_SUCCESS;
+}
+
+// enqueue() through a cached CUDA graph: captured once per (x, y, ws, nrhs) on
+// an internal stream, then replayed on `st` with one launch.  Falls back to a
+// plain enqueue while stage timing is on, when `st` is itself being captured,
+// or with QTT_NO_GRAPH set.
+qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st) {
+  static const bool no_graph = std::getenv("QTT_NO_GRAPH") != nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (no_graph || h->timing || cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return enqueue(h, x, y, nrhs, ws, st);
+  }
+  for (auto& g : h->graphs)
+    if (g.x == x && g.y == y && g.ws == ws && g.nrhs == nrhs) {
+      cudaError_t e = cudaGraphLaunch(g.exec, st);
+      if (e == cudaSuccess) e = cudaEventRecord(h->last, st);
+      return from_cuda(e);
+    }
+  if (!h->capture_stream && cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return QTT_ERROR_CUDA;
+  cudaError_t e = cudaStreamBeginCapture(h->capture_stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return from_cuda(e);
+  const qtt_status_t s = enqueue(h, x, y, nrhs, ws, h->capture_stream);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(h->capture_stream, &graph);
+  if (s != QTT_SUCCESS) {
+    if (graph) cudaGraphDestroy(graph);
+    return s;
+  }
+  if (e != cudaSuccess) return from_cuda(e);
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return from_cuda(e);
+  if (h->graphs.size() >= 8) {
+    cudaGraphExecDestroy(h->graphs.front().exec);
+    h->graphs.erase(h->graphs.begin());
+  }
+  h->graphs.push_back({x, y, ws, nrhs, exec});
+  e = cudaGraphLaunch(exec, st);
+  if (e == cudaSuccess) e = cudaEventRecord(h->last, st);
+  return from_cuda(e);
 }
 
 qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs) {
@@ -672,7 +728,7 @@ qtt_status_t qtt_apply_ws(qtt_handle_t h, const double* x, double* y, int64_t nr
   if (!is_device_ptr(ws)) return QTT_ERROR_NOT_SUPPORTED;
   try {
     DeviceGuard g(h->device);
-    return enqueue(h, x, y, nrhs, ws, reinterpret_cast<cudaStream_t>(stream));
+    return enqueue_graphed(h, x, y, nrhs, ws, reinterpret_cast<cudaStream_t>(stream));
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
@@ -689,6 +745,11 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
       if (h->ws) {
         // the old buffer may still be in use by work on its stream
         cudaFreeAsync(h->ws, h->ws_stream);
+        for (size_t i = h->graphs.size(); i-- > 0;)
+          if (h->graphs[i].ws == h->ws) {
+            cudaGraphExecDestroy(h->graphs[i].exec);
+            h->graphs.erase(h->graphs.begin() + i);
+          }
         h->ws = nullptr;
         h->ws_bytes = 0;
       }
@@ -700,7 +761,7 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
       h->ws_bytes = need;
       h->ws_stream = st;
     }
-    return enqueue(h, x, y, nrhs, h->ws, st);
+    return enqueue_graphed(h, x, y, nrhs, h->ws, st);
   } catch (...) {
     return QTT_ERROR_CUDA;
   }

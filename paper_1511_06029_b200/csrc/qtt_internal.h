@@ -35,7 +35,10 @@ constexpr int kDmmaRowGroups = 4;                // 4 x 16 rows = one 64-row sub
 constexpr int kDmmaRowsPerSubtile = 16 * kDmmaRowGroups;
 // Column groups of consumer warps for a stage with NB n8-blocks: 2-3 warps per
 // SM sub-partition for the wide stages, fewer for narrow (memory-bound) ones.
-QTT_HD constexpr int dmma_col_groups(int NB) { return NB >= 9 ? 3 : (NB >= 2 ? 2 : 1); }
+#ifndef QTT_CG3_MIN_NB
+#define QTT_CG3_MIN_NB 9
+#endif
+QTT_HD constexpr int dmma_col_groups(int NB) { return NB >= QTT_CG3_MIN_NB ? 3 : (NB >= 2 ? 2 : 1); }
 QTT_HD constexpr int dmma_threads(int NB) { return (kDmmaRowGroups * dmma_col_groups(NB) + 1) * 32; }
 constexpr int kMaxStages = 8;
 constexpr int kBarBytes = 256;   // full[8] + empty[8] mbarriers + tile_id[8]

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <limits>
 #include <vector>
@@ -37,6 +38,7 @@ constexpr double kLaunch = 3.0e-6;
 constexpr double kFp64Wide = 37.2e12 * 0.88;   // streamed super-core: some issue slots go to TMA
 constexpr double kL2 = 7.0e12;                   // L2 -> SM bytes the wide kernel may pull
 constexpr double kSms = 148;
+constexpr size_t kTwoCtaSmem = 113 * 1024;      // two resident-kernel CTAs per SM
 
 uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
@@ -49,6 +51,7 @@ size_t dmma_smem_bytes(int KB, int NB, int K, int rep, int stages) {
 
 bool dmma_tiling(int K, int KB, int NB, size_t smem_optin, int* rep_out, int* stages_out, size_t* smem_out) {
   if (!dmma_instantiated(KB, NB)) return false;
+
   // TMA stage: >= 16 KiB per stage (HBM bytes in flight), <= 64 KiB.
   const size_t sub_bytes = size_t(kDmmaRowsPerSubtile) * K * 8;
   int rep = int(std::max<size_t>(1, (16384 + sub_bytes - 1) / sub_bytes));
@@ -90,6 +93,19 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
     const double u = std::min(1.0, tiles / kSms);                   // fraction of SMs busy
     sp->est_seconds = std::max(flops / (kFp64 * u), bytes / (kHbm * u)) + kLaunch;
     ok = true;
+    // Near the ridge (HBM time >= 0.85 x FP64 time) two CTAs per SM with a
+    // shallower ring keep more bytes in flight than one CTA with a deep one
+    // (c5's single r = 24 level: 11.5 -> 9.2 ms); compute-bound levels keep
+    // one CTA and the deepest ring (c3's r = 32 levels lose 3% with two).
+    if (bytes / kHbm >= 0.85 * flops / kFp64) {
+      int rep2 = 0, st2 = 0;
+      size_t sm2 = 0;
+      if (dmma_tiling(sp->K, sp->KB, sp->NB, kTwoCtaSmem, &rep2, &st2, &sm2) && st2 >= 2) {
+        sp->rep = rep2;
+        sp->stages = st2;
+        sp->smem = sm2;
+      }
+    }
   }
   // Wide variant: super-core streamed from L2 in k-chunks (qtt_wide_kernel.cu).
   const int nout = n_i * r_out;

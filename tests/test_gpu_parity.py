@@ -310,3 +310,33 @@ def test_nan_inf_propagate(qtt):
     y, _ = gpu_apply(qtt, cores, x)
     ref = oracle.apply_alg2(cores, x)
     np.testing.assert_array_equal(np.isnan(y), np.isnan(ref))
+
+
+def test_graph_replay_matches_plain_enqueue(qtt):
+    """Applies replay a cached CUDA graph per (x, y, workspace, nrhs); the result is
+    bitwise that of the plain per-stage enqueue (stage timing on disables graphs),
+    across alternating buffers, RHS counts and a non-default stream."""
+    _, cores, x = random_case(31, 12, 9, 3)
+    op = qtt.QttOperator(cores)
+    try:
+        xs = [torch.from_numpy(x).cuda(), torch.from_numpy(x[::-1].copy()).cuda(), torch.from_numpy(x[:1].copy()).cuda()]
+        op.set_stage_timing(True)
+        plain = [op.apply(t) for t in xs]
+        torch.cuda.synchronize()
+        op.stage_times()
+        op.set_stage_timing(False)
+        ys = [torch.empty_like(t) for t in xs]
+        s = torch.cuda.Stream()
+        for rep in range(3):
+            for t, yb, p in zip(xs, ys, plain):
+                yb.zero_()
+                if rep == 2:
+                    with torch.cuda.stream(s):
+                        op.apply(t, out=yb, stream=s)
+                    s.synchronize()
+                else:
+                    op.apply(t, out=yb)
+                torch.cuda.synchronize()
+                assert torch.equal(yb, p)
+    finally:
+        op.close()
