@@ -37,6 +37,9 @@ constexpr double kHbm = 6.45e12 * 0.90;
 constexpr double kLaunch = 3.0e-6;
 constexpr double kFp64Wide = 37.2e12 * 0.88;   // streamed super-core: some issue slots go to TMA
 constexpr double kL2 = 7.0e12;                   // L2 -> SM bytes the wide kernel may pull
+constexpr double kTileLatency = 1.5e-6;          // one tile: TMA round trip + epilogue
+constexpr double kChunkLatency = 0.4e-6;         // one more k-chunk of a wide tile
+constexpr double kSmBw = 100e9;                  // bytes/s one SM's TMA pulls when few SMs are busy
 constexpr double kSms = 148;
 constexpr size_t kTwoCtaSmem = 113 * 1024;      // two resident-kernel CTAs per SM
 
@@ -88,10 +91,15 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
   bool ok = false;
   if (dmma_tiling(sp->K, sp->KB, sp->NB, smem_optin, &sp->rep, &sp->stages, &sp->smem)) {
     sp->variant = L == 1 ? kDmma : kMerged;
-    const double flops = 2.0 * M * 16.0 * sp->KB * 8.0 * sp->NB;   // padded tensor-pipe work
     const double tiles = std::ceil(M / (kDmmaRowsPerSubtile * sp->rep));
+    // padded tensor-pipe work: whole tiles of 64 * rep rows, K and N to fragment blocks
+    const double flops = 2.0 * tiles * kDmmaRowsPerSubtile * sp->rep * 16.0 * sp->KB * 8.0 * sp->NB;
     const double u = std::min(1.0, tiles / kSms);                   // fraction of SMs busy
-    sp->est_seconds = std::max(flops / (kFp64 * u), bytes / (kHbm * u)) + kLaunch;
+    // latency floor of tiny problems: each CTA's tiles run one after another,
+    // each at least one TMA round trip
+    const double tile_bytes = kDmmaRowsPerSubtile * sp->rep * 8.0 * sp->K;
+    const double lat = std::ceil(tiles / kSms) * (kTileLatency + tile_bytes / kSmBw) + sp->KB * sp->NB * 1024.0 / kSmBw;
+    sp->est_seconds = std::max({flops / (kFp64 * u), bytes / (kHbm * u), lat}) + kLaunch;
     ok = true;
     // Near the ridge (HBM time >= 0.85 x FP64 time) two CTAs per SM with a
     // shallower ring keep more bytes in flight than one CTA with a deep one
@@ -117,11 +125,15 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
     const size_t smem = wide_smem_bytes(NBw);
     if (smem <= smem_optin) {
       const int ncb = (nout + 8 * NBw - 1) / (8 * NBw);
-      const double flops = 2.0 * M * std::ceil(sp->K / double(kWideBK)) * kWideBK * ncb * 8.0 * NBw;
       const double tiles = std::ceil(M / kDmmaRowsPerSubtile) * ncb;
+      const double flops = 2.0 * tiles * kDmmaRowsPerSubtile * std::ceil(sp->K / double(kWideBK)) * kWideBK * 8.0 * NBw;
       const double u = std::min(1.0, tiles / kSms);
       const double l2 = tiles * (kDmmaRowsPerSubtile * 8.0 * sp->K + 8.0 * sp->K * 8.0 * NBw);
-      const double t = std::max({flops / (kFp64Wide * u), (bytes + wbytes) / (kHbm * u), l2 / kL2}) + kLaunch;
+      // a wide tile streams its k-chunks one after another
+      const double nch = std::ceil(sp->K / double(kWideBK));
+      const double tile_bytes = nch * kWideBK * 8.0 * (kDmmaRowsPerSubtile + 8.0 * NBw);
+      const double lat = std::ceil(tiles / kSms) * (kTileLatency + nch * kChunkLatency + tile_bytes / kSmBw);
+      const double t = std::max({flops / (kFp64Wide * u), (bytes + wbytes) / (kHbm * u), l2 / kL2, lat}) + kLaunch;
       if (!ok || t < sp->est_seconds) {
         sp->variant = kWide;
         sp->NB = NBw;
