@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--label", default="")
     ap.add_argument("--algorithmic-bytes", type=float, default=None)
     ap.add_argument("--algorithmic-flops", type=float, default=None)
+    ap.add_argument("--launch-index", type=int, default=0, help="launch whose numbers are the headline")
     ap.add_argument("-o", "--out", required=True)
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -60,7 +61,7 @@ def main():
                     continue
                 d[name] = v
         launches.append(d)
-    first = launches[0]
+    first = launches[a.launch_index]
     out = {"config": a.config, "label": a.label, "report": a.report, "launches": launches}
     if "dram_read" in first and "dram_write" in first:
         out["dram_bytes_per_launch"] = first["dram_read"] + first["dram_write"]
