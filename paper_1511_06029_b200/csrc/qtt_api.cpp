@@ -78,6 +78,9 @@ struct qtt_plan {
   };
   std::vector<Graph> graphs;
   cudaStream_t capture_stream = nullptr;
+  // qtt_apply_host pipelining: copy stream and chunk events
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> pipe_events;
   bool timing = false;
   std::vector<StageEvents> pending;
   std::vector<double> stage_ms;
@@ -319,6 +322,8 @@ void free_plan(qtt_plan* h) {
   if (h->last) cudaEventDestroy(h->last);
   for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  for (auto& e : h->pipe_events) cudaEventDestroy(e);
   delete h;
 }
 
@@ -360,6 +365,55 @@ qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
   return from_cuda(cudaMemcpy(S.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice));
 }
 
+// One launch of stage S over GEMM rows [m_base, m_base + M) (all rows: m_base = 0,
+// M = nrhs * N / n_i).  `in` points at the stage input's row 0.  A chunk
+// (m_base > 0) must lie in the first RHS: there every output row is
+// m + Q ii, so offsetting `out` by m_base rows is exact.
+cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* in, double* out, int64_t M,
+                         int64_t m_base, int* counter, cudaStream_t st) {
+  const qtt::StagePlan& sp = S.plan;
+  const int L = proj ? 0 : sp.k1 - sp.k0 + 1;
+  LevelArgs a;
+  a.in = in + m_base * sp.K;
+  a.out = out + m_base * sp.r_out;
+  a.bpack = S.d_bpack;
+  a.core = S.d_core;
+  a.n_i = sp.n_i;
+  a.log2_q = h->d - L;
+  a.q = int64_t(1) << a.log2_q;
+  a.M = M;
+  a.tile_counter = counter;
+  a.r_in = sp.r_in;
+  a.r_out = sp.r_out;
+  a.RP = sp.RP;
+  a.K = sp.K;
+  a.KB = sp.KB;
+  a.NB = sp.NB;
+  a.rep = sp.rep;
+  a.stages = sp.stages;
+  a.smem = sp.smem;
+  a.nchunks = sp.nchunks;
+  a.ncb = sp.ncb;
+  a.nout = sp.n_i * sp.r_out;
+  cudaError_t e;
+  if (sp.variant == qtt::kWide) {
+    const int64_t tiles = (a.M + qtt::kDmmaRowsPerSubtile - 1) / qtt::kDmmaRowsPerSubtile * sp.ncb;
+    a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms)));
+    e = qtt::launch_wide(a, st);
+  } else if (sp.variant != qtt::kGeneric) {
+    const int64_t rows_per_stage = int64_t(qtt::kDmmaRowsPerSubtile) * sp.rep;
+    const int64_t tiles = (a.M + rows_per_stage - 1) / rows_per_stage;
+    a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms) * S.ctas_per_sm));
+    e = qtt::launch_level_dmma(a, st);
+  } else {
+    e = qtt::launch_level_generic(a, st, h->num_sms);
+  }
+  if (e != cudaSuccess && std::getenv("QTT_DEBUG"))
+    std::fprintf(stderr, "qtt: stage (levels %d-%d, variant %d, KB %d NB %d smem %zu grid %d) launch failed: %s\n",
+                 sp.k0, sp.k1, sp.variant, sp.KB, sp.NB, a.smem, a.grid, cudaGetErrorString(e));
+  return e;
+}
+
 qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st) {
   unsigned char* base = static_cast<unsigned char*>(ws);
   int* counters = reinterpret_cast<int*>(base);
@@ -373,28 +427,7 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
   for (int si = 0; si < ns; ++si) {
     const bool proj = si == nloc;                  // shard projection stage
     const Stage& S = proj ? h->proj : h->stages[si];
-    const qtt::StagePlan& sp = S.plan;
     double* out = (si == ns - 1) ? y : buf[si & 1];
-    const int L = proj ? 0 : sp.k1 - sp.k0 + 1;
-    LevelArgs a;
-    a.in = in;
-    a.out = out;
-    a.bpack = S.d_bpack;
-    a.core = S.d_core;
-    a.n_i = sp.n_i;
-    a.log2_q = h->d - L;
-    a.q = int64_t(1) << a.log2_q;
-    a.M = nrhs * a.q;
-    a.tile_counter = counters + si;
-    a.r_in = sp.r_in;
-    a.r_out = sp.r_out;
-    a.RP = sp.RP;
-    a.K = sp.K;
-    a.KB = sp.KB;
-    a.NB = sp.NB;
-    a.rep = sp.rep;
-    a.stages = sp.stages;
-    a.smem = sp.smem;
     StageEvents ev{};
     if (h->timing && !proj) {
       ev.stage = si;
@@ -402,28 +435,10 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
         return QTT_ERROR_CUDA;
       cudaEventRecord(ev.start, st);
     }
-    a.nchunks = sp.nchunks;
-    a.ncb = sp.ncb;
-    a.nout = sp.n_i * sp.r_out;
-    cudaError_t e;
-    if (sp.variant == qtt::kWide) {
-      const int64_t tiles = (a.M + qtt::kDmmaRowsPerSubtile - 1) / qtt::kDmmaRowsPerSubtile * sp.ncb;
-      a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms)));
-      e = qtt::launch_wide(a, st);
-    } else if (sp.variant != qtt::kGeneric) {
-      const int64_t rows_per_stage = int64_t(qtt::kDmmaRowsPerSubtile) * sp.rep;
-      const int64_t tiles = (a.M + rows_per_stage - 1) / rows_per_stage;
-      a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms) * S.ctas_per_sm));
-      e = qtt::launch_level_dmma(a, st);
-    } else {
-      e = qtt::launch_level_generic(a, st, h->num_sms);
-    }
-    if (e != cudaSuccess) {
-      if (std::getenv("QTT_DEBUG"))
-        std::fprintf(stderr, "qtt: stage %d (levels %d-%d, variant %d, KB %d NB %d smem %zu grid %d) launch failed: %s\n",
-                     si, sp.k0, sp.k1, sp.variant, sp.KB, sp.NB, a.smem, a.grid, cudaGetErrorString(e));
-      return from_cuda(e);
-    }
+    const int L = proj ? 0 : S.plan.k1 - S.plan.k0 + 1;
+    const int64_t M = nrhs * (int64_t(1) << (h->d - L));
+    const cudaError_t e = launch_stage(h, S, proj, in, out, M, 0, counters + si, st);
+    if (e != cudaSuccess) return from_cuda(e);
     if (h->timing && !proj) {
       cudaEventRecord(ev.stop, st);
       h->pending.push_back(ev);
@@ -433,6 +448,76 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
   if (h->timing) h->timed_applies++;
   if (st != h->capture_stream) cudaEventRecord(h->last, st);
   return QTT_SUCCESS;
+}
+
+// qtt_apply_host for one RHS with the host<->device copies overlapped with the
+// first and last stages: the first stage runs in row chunks, chunk c waiting
+// only for its slice of x (H2D on a copy stream); the last stage runs in row
+// chunks, each followed by the D2H of the 2^L strided runs of y it wrote
+// (out row m + Q ii, r_d = 1) while the next chunk computes.
+qtt_status_t apply_host_pipelined(qtt_plan* h, const double* x_host, double* y_host, cudaStream_t st) {
+  const int ns = int(h->stages.size());
+  constexpr int kChunks = 8;
+  unsigned char* base = static_cast<unsigned char*>(h->ws);
+  int* counters = reinterpret_cast<int*>(base);
+  const size_t bb = ws_buf_bytes(h, 1);
+  double* buf[2] = {reinterpret_cast<double*>(base + kWsHeader), reinterpret_cast<double*>(base + kWsHeader + bb)};
+  if (!h->copy_stream && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return QTT_ERROR_CUDA;
+  if (h->pipe_events.empty()) {
+    h->pipe_events.resize(2 * kChunks + 2);
+    for (auto& ev : h->pipe_events)
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return QTT_ERROR_CUDA;
+  }
+  cudaStream_t cs = h->copy_stream;
+  cudaEvent_t* ev = h->pipe_events.data();
+  cudaError_t e = cudaEventRecord(ev[2 * kChunks], st);               // copies start after prior work on st
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[2 * kChunks], 0);
+  if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, kWsHeader, st);
+  if (e != cudaSuccess) return from_cuda(e);
+  auto chunk_rows = [](int64_t M, int c) {
+    const int64_t step = (M / kChunks + 63) / 64 * 64;
+    return std::min<int64_t>(M, step * c);
+  };
+  int ctr = ns;   // counters [0, ns) for unchunked stages, then one per chunk
+  const double* in = h->hx;
+  for (int si = 0; si < ns; ++si) {
+    const Stage& S = h->stages[si];
+    const int L = S.plan.k1 - S.plan.k0 + 1;
+    const int64_t M = int64_t(1) << (h->d - L);
+    double* out = (si == ns - 1) ? h->hy : buf[si & 1];
+    if (si == 0 || si == ns - 1) {
+      for (int c = 0; c < kChunks; ++c) {
+        const int64_t m0 = chunk_rows(M, c), m1 = chunk_rows(M, c + 1);
+        if (m1 <= m0) continue;
+        if (si == 0) {   // x slice [m0 * 2^L, m1 * 2^L) (r_0 = 1)
+          const size_t off = size_t(m0) << L, cnt = size_t(m1 - m0) << L;
+          e = cudaMemcpyAsync(h->hx + off, x_host + off, cnt * sizeof(double), cudaMemcpyHostToDevice, cs);
+          if (e == cudaSuccess) e = cudaEventRecord(ev[c], cs);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[c], 0);
+          if (e != cudaSuccess) return from_cuda(e);
+        }
+        e = launch_stage(h, S, false, in, out, m1 - m0, m0, counters + (ctr++), st);
+        if (e != cudaSuccess) return from_cuda(e);
+        if (si == ns - 1) {   // y rows m0..m1 of every output block ii (r_d = 1)
+          e = cudaEventRecord(ev[kChunks + c], st);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[kChunks + c], 0);
+          if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(y_host + m0, size_t(M) * sizeof(double), h->hy + m0, size_t(M) * sizeof(double),
+                                  size_t(m1 - m0) * sizeof(double), size_t(1) << L, cudaMemcpyDeviceToHost, cs);
+          if (e != cudaSuccess) return from_cuda(e);
+        }
+      }
+    } else {
+      e = launch_stage(h, S, false, in, out, M, 0, counters + si, st);
+      if (e != cudaSuccess) return from_cuda(e);
+    }
+    in = out;
+  }
+  e = cudaEventRecord(ev[2 * kChunks + 1], cs);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[2 * kChunks + 1], 0);
+  if (e == cudaSuccess) e = cudaEventRecord(h->last, st);
+  return from_cuda(e);
 }
 
 // enqueue() through a cached CUDA graph: captured once per (x, y, ws, nrhs) on
@@ -783,6 +868,29 @@ qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host
       if (e == cudaSuccess) e = cudaMalloc(&h->hy, elems * sizeof(double));
       if (e != cudaSuccess) return from_cuda(e);
       h->h_elems = elems;
+    }
+    // pipelined copies: one RHS, at least two stages, enough rows to chunk
+    if (nrhs == 1 && h->stages.size() >= 2 && h->shard_bits == 0 && !h->timing &&
+        (h->N >> (h->stages.front().plan.k1 - h->stages.front().plan.k0 + 1)) >= 8 * 64 &&
+        (h->N >> (h->stages.back().plan.k1 - h->stages.back().plan.k0 + 1)) >= 8 * 64) {
+      const size_t need = ws_bytes_for(h, 1);
+      if (need > h->ws_bytes) {
+        if (h->ws) cudaFreeAsync(h->ws, h->ws_stream);
+        h->ws = nullptr;
+        h->ws_bytes = 0;
+        for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+        h->graphs.clear();
+        cudaError_t e = cudaMallocAsync(&h->ws, need, st);
+        if (e != cudaSuccess) {
+          h->ws = nullptr;
+          return from_cuda(e);
+        }
+        h->ws_bytes = need;
+        h->ws_stream = st;
+      }
+      qtt_status_t s = apply_host_pipelined(h, x_host, y_host, st);
+      if (s != QTT_SUCCESS) return s;
+      return from_cuda(cudaStreamSynchronize(st));
     }
     cudaError_t e = cudaMemcpyAsync(h->hx, x_host, elems * sizeof(double), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return from_cuda(e);

@@ -64,7 +64,8 @@ struct LevelArgs {
   double* out = nullptr;
   const double* bpack = nullptr;   // DMMA: packed B fragments (KB*NB*32 double4)
   const double* core = nullptr;    // generic: raw core [a][i][j][b]
-  int64_t M = 0;                   // GEMM rows: nrhs * N / n_i
+  int64_t M = 0;                   // GEMM rows of this launch: nrhs * N / n_i, or a chunk of them
+                                   // (chunks: one RHS only; `in` and `out` are pre-offset)
   int64_t q = 0;                   // Q = N / n_i
   int log2_q = 0;                  // Q = 2^log2_q
   int n_i = 2;                     // 2^L output (and input) digit combinations

@@ -340,3 +340,24 @@ def test_graph_replay_matches_plain_enqueue(qtt):
                 assert torch.equal(yb, p)
     finally:
         op.close()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_apply_host_pipelined_bitwise(qtt, name):
+    """qtt_apply_host overlaps the H2D of x with the first stage and the D2H of y
+    with the last stage (chunked launches of the same kernels): bitwise equal
+    to the device apply."""
+    cfg, cores, x = generate(name)
+    op = qtt.QttOperator(cores)
+    try:
+        yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        xh = torch.from_numpy(x).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        for _ in range(2):
+            yh.zero_()
+            op.apply_host(xh.numpy(), out=yh.numpy())
+            np.testing.assert_array_equal(yh.numpy(), yd)
+        # pageable buffers too
+        np.testing.assert_array_equal(op.apply_host(x), yd)
+    finally:
+        op.close()
