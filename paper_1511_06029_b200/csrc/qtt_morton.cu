@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads) morton_tile_kernel(const double* __r
                                                                int levels, int64_t N) {
   constexpr int B = kTileBits / DIM;          // bits per axis inside the tile
   constexpr int R = 1 << B;                   // row length (x extent)
-  __shared__ double tile[kTile];
+  __shared__ __align__(16) double tile[kTile];
 
   const int64_t tiles_per_rhs = N >> kTileBits;
   const int64_t s = blockIdx.x / tiles_per_rhs;
@@ -105,27 +105,32 @@ __global__ void __launch_bounds__(kThreads) morton_tile_kernel(const double* __r
     slot = row * R + (x ^ swz<DIM>(row));
   };
 
+  // 16-byte accesses on both sides: x pairs (x even, x + 1) stay adjacent under
+  // the swizzle (it flips only bits 2-3 of x), and u pairs are x pairs.
+  double2* tile2 = reinterpret_cast<double2*>(tile);
   if (PACK) {
-#pragma unroll 4
-    for (int e = threadIdx.x; e < kTile; e += kThreads) {
+#pragma unroll
+    for (int e = 2 * threadIdx.x; e < kTile; e += 2 * kThreads) {
       int64_t goff;
       int slot;
       grid_of_e(e, goff, slot);
-      tile[slot] = __ldcs(in + gbase + goff);
+      tile2[slot >> 1] = __ldcs(reinterpret_cast<const double2*>(in + gbase + goff));
     }
     __syncthreads();
-#pragma unroll 4
-    for (int u = threadIdx.x; u < kTile; u += kThreads) __stcs(out + qbase + u, tile[slot_of_u(u)]);
+#pragma unroll
+    for (int u = 2 * threadIdx.x; u < kTile; u += 2 * kThreads)
+      __stcs(reinterpret_cast<double2*>(out + qbase + u), tile2[slot_of_u(u) >> 1]);
   } else {
-#pragma unroll 4
-    for (int u = threadIdx.x; u < kTile; u += kThreads) tile[slot_of_u(u)] = __ldcs(in + qbase + u);
+#pragma unroll
+    for (int u = 2 * threadIdx.x; u < kTile; u += 2 * kThreads)
+      tile2[slot_of_u(u) >> 1] = __ldcs(reinterpret_cast<const double2*>(in + qbase + u));
     __syncthreads();
-#pragma unroll 4
-    for (int e = threadIdx.x; e < kTile; e += kThreads) {
+#pragma unroll
+    for (int e = 2 * threadIdx.x; e < kTile; e += 2 * kThreads) {
       int64_t goff;
       int slot;
       grid_of_e(e, goff, slot);
-      __stcs(out + gbase + goff, tile[slot]);
+      __stcs(reinterpret_cast<double2*>(out + gbase + goff), tile2[slot >> 1]);
     }
   }
 }
@@ -136,7 +141,8 @@ cudaError_t launch_morton(const double* in, double* out, int dim, int levels, in
                           cudaStream_t st, int num_sms) {
   const int d = dim * levels;
   const int64_t N = int64_t(1) << d;
-  const bool tiled = (dim == 3 && levels >= 4) || (dim == 2 && levels >= 6);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const bool tiled = aligned && ((dim == 3 && levels >= 4) || (dim == 2 && levels >= 6));
   if (tiled) {
     const int64_t blocks = nrhs * (N >> kTileBits);
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;

@@ -79,3 +79,16 @@ def test_apply_grid(qtt, dim, levels, nrhs):
         op.close()
     ref = OM.unpack(oracle.apply_alg2(cores, OM.pack(g, dim, levels)), dim, levels)
     oracle.assert_close(y, ref)
+
+
+def test_pack_unaligned_pointers(qtt):
+    """8-byte aligned (not 16) pointers take the per-element kernel: same result."""
+    dim, levels = 3, 4
+    N = 1 << 12
+    base = torch.from_numpy(np.random.default_rng(2).standard_normal(N + 1)).cuda()
+    g = base[1:]                                     # 8-byte offset view
+    out = torch.empty(N + 1, dtype=torch.float64, device="cuda")[1:]
+    lib = qtt._lib.load()
+    assert lib.qtt_morton_pack(g.data_ptr(), out.data_ptr(), dim, levels, 1, None) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), OM.pack(g.cpu().numpy()[None, :], dim, levels)[0])

@@ -9,8 +9,8 @@ for sa, sb in zip(a["per_stage_roofline"]["stages"], b["per_stage_roofline"]["st
 ea, eb = a["other_configs_and_next_rows"], b["other_configs_and_next_rows"]
 for k in ea:
     va, vb = ea[k], eb.get(k, {})
-    ms_a = va.get("ms_median", va.get("pack_ms", va.get("ms_wall_median")))
-    ms_b = vb.get("ms_median", vb.get("pack_ms", vb.get("ms_wall_median")))
+    ms_a = va.get("ms_per_apply", va.get("pack_ms", va.get("ms_wall_median")))
+    ms_b = vb.get("ms_per_apply", vb.get("pack_ms", vb.get("ms_wall_median")))
     print(k, "A %.4f  B %.4f ms" % (ms_a, ms_b))
     if "stages" in va and len(va["stages"][0]) > 3:
         for x, y in zip(va["stages"], vb["stages"]):
