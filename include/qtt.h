@@ -25,8 +25,10 @@
  * no reduced precision).  NaN/Inf propagate per IEEE; nothing is checked.
  * Results are bitwise deterministic for a fixed (handle, nrhs): no split-K
  * and no atomic accumulation (the one atomic, the dynamic tile scheduler,
- * decides only which SM computes a tile, never the order of its arithmetic).  No exceptions cross this boundary; every entry point returns
- * a qtt_status_t.
+ * decides only which SM computes a tile, never the order of its arithmetic).
+ * No exceptions cross this boundary; every entry point returns a qtt_status_t.
+ * Threading: a handle (its cached workspace, graphs and staging buffers) must
+ * not be used by several host threads at once; separate handles are independent.
  */
 #ifndef QTT_B200_H
 #define QTT_B200_H
