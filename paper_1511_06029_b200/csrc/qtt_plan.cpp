@@ -32,10 +32,16 @@ namespace {
 
 // Cost model of one B200 (148 SMs, 1965 MHz): DMMA 148*64 FMA/clk, HBM copy
 // bandwidth as measured in MEASURED_PEAKS.json (~6.5 TB/s), launch ~3 us.
-constexpr double kFp64 = 37.2e12 * 0.95;
+constexpr double kFp64 = 37.2e12 * 0.955;     // DMMA rate of the resident kernel with 12 consumer warps
 constexpr double kHbm = 6.45e12 * 0.90;
 constexpr double kLaunch = 3.0e-6;
-constexpr double kFp64Wide = 37.2e12 * 0.88;   // streamed super-core: some issue slots go to TMA
+// measured (profiles/, c3-c5 stages): 8 consumer warps (NB <= 8) reach ~0.84
+// of nominal against 12 warps' ~0.955; a wide tile pays a fixed epilogue
+// against its k-chunks, ~nch / (nch + 0.3)
+double fp64_rate(int NB, double nchunks) {
+  const double warps = dmma_col_groups(NB) >= 3 ? 1.0 : 0.88;
+  return kFp64 * warps * (nchunks / (nchunks + 0.3));
+}
 constexpr double kL2 = 7.0e12;                   // L2 -> SM bytes the wide kernel may pull
 constexpr double kTileLatency = 1.5e-6;          // one tile: TMA round trip + epilogue
 constexpr double kChunkLatency = 0.4e-6;         // one more k-chunk of a wide tile
@@ -99,7 +105,7 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
     // each at least one TMA round trip
     const double tile_bytes = kDmmaRowsPerSubtile * sp->rep * 8.0 * sp->K;
     const double lat = std::ceil(tiles / kSms) * (kTileLatency + tile_bytes / kSmBw) + sp->KB * sp->NB * 1024.0 / kSmBw;
-    sp->est_seconds = std::max({flops / (kFp64 * u), bytes / (kHbm * u), lat}) + kLaunch;
+    sp->est_seconds = std::max({flops / (fp64_rate(sp->NB, 1e9) * u), bytes / (kHbm * u), lat}) + kLaunch;
     ok = true;
     // Near the ridge (HBM time >= 0.85 x FP64 time) two CTAs per SM with a
     // shallower ring keep more bytes in flight than one CTA with a deep one
@@ -133,7 +139,8 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
       const double nch = std::ceil(sp->K / double(kWideBK));
       const double tile_bytes = nch * kWideBK * 8.0 * (kDmmaRowsPerSubtile + 8.0 * NBw);
       const double lat = std::ceil(tiles / kSms) * (kTileLatency + nch * kChunkLatency + tile_bytes / kSmBw);
-      const double t = std::max({flops / (kFp64Wide * u), (bytes + wbytes) / (kHbm * u), l2 / kL2, lat}) + kLaunch;
+      const double t =
+          std::max({flops / (fp64_rate(NBw, nch) * u), (bytes + wbytes) / (kHbm * u), l2 / kL2, lat}) + kLaunch;
       if (!ok || t < sp->est_seconds) {
         sp->variant = kWide;
         sp->NB = NBw;
