@@ -109,7 +109,8 @@ qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem_optin, int
  *   x, y  : DEVICE pointers owned by the caller, column-major N x nrhs,
  *           16-byte aligned; the ranges [x, x+N*nrhs) and [y, y+N*nrhs)
  *           must not overlap (in-place is impossible, reading R13).
- *   nrhs  : number of right-hand sides, >= 1.
+ *   nrhs  : number of right-hand sides, >= 1, with N * nrhs <= 2^31
+ *           (QTT_ERROR_NOT_SUPPORTED beyond: 32-bit TMA row coordinates).
  * Argument errors return synchronously and enqueue nothing.  The handle
  * keeps a cached workspace of qtt_workspace_size() bytes, allocated on first
  * use with cudaMallocAsync on `stream`; concurrent applies on one handle

@@ -566,7 +566,8 @@ qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nr
 qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs) {
   if (!h || !x || !y || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
   if (h->shard_bits) return QTT_ERROR_INVALID_VALUE;   // shard handles use qtt_shard_apply
-  if (nrhs > (int64_t(1) << 40) / h->N) return QTT_ERROR_INVALID_VALUE;
+  // N * nrhs <= 2^31 keeps every GEMM row index a valid 32-bit TMA coordinate
+  if (nrhs > (int64_t(1) << 31) / h->N) return QTT_ERROR_NOT_SUPPORTED;
   const uintptr_t xs = reinterpret_cast<uintptr_t>(x), ys = reinterpret_cast<uintptr_t>(y);
   const uintptr_t bytes = uintptr_t(h->N) * uintptr_t(nrhs) * sizeof(double);
   if (xs < ys + bytes && ys < xs + bytes) return QTT_ERROR_INVALID_VALUE;
@@ -727,7 +728,7 @@ qtt_status_t qtt_create_shard(qtt_handle_t* out, int d, const int64_t* ranks, co
 
 static qtt_status_t check_shard_args(qtt_plan* h, const double* x, const double* send, int64_t nrhs) {
   if (!h || !x || !send || nrhs < 1 || h->shard_bits == 0) return QTT_ERROR_INVALID_VALUE;
-  if (nrhs > (int64_t(1) << 40) / (h->N << h->shard_bits)) return QTT_ERROR_INVALID_VALUE;
+  if (nrhs > (int64_t(1) << 31) / (h->N << h->shard_bits)) return QTT_ERROR_NOT_SUPPORTED;
   const uintptr_t xs = reinterpret_cast<uintptr_t>(x), ys = reinterpret_cast<uintptr_t>(send);
   const uintptr_t xb = uintptr_t(h->N) * uintptr_t(nrhs) * sizeof(double);
   const uintptr_t yb = xb << h->shard_bits;
