@@ -361,3 +361,20 @@ def test_apply_host_pipelined_bitwise(qtt, name):
         np.testing.assert_array_equal(op.apply_host(x), yd)
     finally:
         op.close()
+
+
+@pytest.mark.parametrize("d,s,nrhs", [(28, 123457, 1), (26, 1, 3)])
+def test_shift_large_d_bitwise(qtt, d, s, nrhs):
+    """Large N (2 GiB vectors at d = 28; 64-bit offsets, many tiles): the exact
+    rank-2 cyclic shift is np.roll / torch.roll bitwise."""
+    gen = torch.Generator(device="cuda").manual_seed(d)
+    x = torch.randn((nrhs, 1 << d), dtype=torch.float64, device="cuda", generator=gen)
+    op = qtt.QttOperator(CF.shift_cores(d, s))
+    try:
+        y = op.apply(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y, torch.roll(x, s, dims=1))
+    finally:
+        op.close()
+    del x, y
+    torch.cuda.empty_cache()
