@@ -57,6 +57,9 @@ struct qtt_plan {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   cudaStream_t ws_stream = nullptr;
+  // stream of the last apply that used the cached workspace (cross-stream ordering)
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
   // cached QTT-order staging vectors (qtt_apply_grid)
   double* gx = nullptr;
   double* gy = nullptr;
@@ -563,6 +566,19 @@ qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nr
   return from_cuda(e);
 }
 
+// The cached workspace is shared by every apply on the handle: order this one
+// after the previous one when that was enqueued on another stream (skipped
+// while `st` is being captured by the caller).
+qtt_status_t order_after_last(qtt_plan* h, cudaStream_t st) {
+  if (!h->has_last || h->last_stream == st) return QTT_SUCCESS;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return QTT_SUCCESS;
+  }
+  return from_cuda(cudaStreamWaitEvent(st, h->last, 0));
+}
+
 qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs) {
   if (!h || !x || !y || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
   if (h->shard_bits) return QTT_ERROR_INVALID_VALUE;   // shard handles use qtt_shard_apply
@@ -773,7 +789,13 @@ qtt_status_t qtt_shard_apply(qtt_handle_t h, const double* x_local, double* send
       h->ws_bytes = need;
       h->ws_stream = st;
     }
-    return enqueue(h, x_local, send, nrhs, h->ws, st);
+    qtt_status_t so = order_after_last(h, st);
+    if (so == QTT_SUCCESS) so = enqueue(h, x_local, send, nrhs, h->ws, st);
+    if (so == QTT_SUCCESS) {
+      h->last_stream = st;
+      h->has_last = true;
+    }
+    return so;
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
@@ -847,7 +869,14 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
       h->ws_bytes = need;
       h->ws_stream = st;
     }
-    return enqueue_graphed(h, x, y, nrhs, h->ws, st);
+    const qtt_status_t so = order_after_last(h, st);
+    if (so != QTT_SUCCESS) return so;
+    const qtt_status_t s2 = enqueue_graphed(h, x, y, nrhs, h->ws, st);
+    if (s2 == QTT_SUCCESS) {
+      h->last_stream = st;
+      h->has_last = true;
+    }
+    return s2;
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
@@ -889,8 +918,11 @@ qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host
         h->ws_bytes = need;
         h->ws_stream = st;
       }
-      qtt_status_t s = apply_host_pipelined(h, x_host, y_host, st);
+      qtt_status_t s = order_after_last(h, st);
+      if (s == QTT_SUCCESS) s = apply_host_pipelined(h, x_host, y_host, st);
       if (s != QTT_SUCCESS) return s;
+      h->last_stream = st;
+      h->has_last = true;
       return from_cuda(cudaStreamSynchronize(st));
     }
     cudaError_t e = cudaMemcpyAsync(h->hx, x_host, elems * sizeof(double), cudaMemcpyHostToDevice, st);

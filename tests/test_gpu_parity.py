@@ -378,3 +378,26 @@ def test_shift_large_d_bitwise(qtt, d, s, nrhs):
         op.close()
     del x, y
     torch.cuda.empty_cache()
+
+
+def test_back_to_back_applies_on_two_streams(qtt):
+    """The cached workspace is shared: an apply enqueued on stream B right after
+    one on stream A (no host sync between) is ordered after it by the library."""
+    cfg, cores, x = generate("c3")
+    x2 = np.ascontiguousarray(x[:, ::-1])
+    op = qtt.QttOperator(cores)
+    try:
+        ref1 = op.apply(torch.from_numpy(x).cuda())
+        ref2 = op.apply(torch.from_numpy(x2).cuda())
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Stream(), torch.cuda.Stream()
+        xa, xb = torch.from_numpy(x).cuda(), torch.from_numpy(x2).cuda()
+        torch.cuda.synchronize()
+        for _ in range(3):
+            ya = op.apply(xa, stream=a)
+            yb = op.apply(xb, stream=b)
+            a.synchronize()
+            b.synchronize()
+            assert torch.equal(ya, ref1) and torch.equal(yb, ref2)
+    finally:
+        op.close()
