@@ -82,6 +82,15 @@ struct LevelArgs {
   int nchunks = 1;                 // K / kWideBK
   int ncb = 1;                     // column blocks of 8*NB columns
   int nout = 0;                    // n_i * r_out real output columns (RP = r_out)
+  // wide variant, host-copy pipelining (qtt_apply_host): the producer waits for
+  // ready[m0 / ready_rows] >= ready_val (written by the copy stream after each
+  // H2D chunk) before loading a tile's A rows; each consumer warp adds 1 to
+  // done[m0 / done_rows] once its part of a tile is stored
+  const unsigned* ready = nullptr;
+  unsigned ready_val = 0;
+  int64_t ready_rows = 0;
+  unsigned* done = nullptr;
+  int64_t done_rows = 0;
 };
 
 // Host-side stage plan (qtt_plan.cpp): pure function of the rank profile and

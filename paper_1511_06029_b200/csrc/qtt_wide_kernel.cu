@@ -135,7 +135,13 @@ __device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const Leve
   }
 }
 
-template <int NB, int NBC>
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int NB, int NBC, bool HOOKS>
 __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uint64_t* empty, const int64_t* tile_id,
                                          unsigned char* ring, int rg, int nb0, int lane) {
   const int g = lane >> 2;
@@ -160,11 +166,16 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
       const int64_t rt = t / p.ncb;
       const int cb = int(t - rt * p.ncb);
       tile_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
+      if (HOOKS && p.done) {   // publish this warp's part of the tile to the D2H copy stream
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.done + (rt * kDmmaRowsPerSubtile) / p.done_rows, 1u);
+      }
     }
   }
 }
 
-template <int NB>
+template <int NB, bool HOOKS>
 __global__ void __launch_bounds__(dmma_threads(NB), 1)
 wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   constexpr int CG = dmma_col_groups(NB);
@@ -211,6 +222,10 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
         const int cb = int(t - rt * p.ncb);
         const int m0 = int(rt * kDmmaRowsPerSubtile);
         const double* bsrc = p.bpack + size_t(cb) * p.nchunks * (bbytes / 8);
+        if (HOOKS && p.ready) {   // this tile's rows of A must have arrived from the host
+          const unsigned* f = p.ready + m0 / p.ready_rows;
+          while (int(ld_acquire_u32(f) - p.ready_val) < 0) __nanosleep(200);
+        }
         for (int ch = 0; ch < p.nchunks; ++ch, ++it) {
           const int s = it % kWideStages;
           mbar_wait(&empty[s], (uint32_t(it / kWideStages) & 1u) ^ 1u);
@@ -229,11 +244,11 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   const int rg = warp % kDmmaRowGroups;
   const int cg = warp / kDmmaRowGroups;
   if (cg == 0) {
-    consumer<NB, NBW>(p, full, empty, tile_id, ring, rg, 0, lane);
+    consumer<NB, NBW, HOOKS>(p, full, empty, tile_id, ring, rg, 0, lane);
   } else if (cg == 1) {
-    if constexpr (NB_1 > 0) consumer<NB, NB_1>(p, full, empty, tile_id, ring, rg, NBW, lane);
+    if constexpr (NB_1 > 0) consumer<NB, NB_1, HOOKS>(p, full, empty, tile_id, ring, rg, NBW, lane);
   } else {
-    if constexpr (NB_2 > 0) consumer<NB, NB_2>(p, full, empty, tile_id, ring, rg, NBW + NB_1, lane);
+    if constexpr (NB_2 > 0) consumer<NB, NB_2, HOOKS>(p, full, empty, tile_id, ring, rg, NBW + NB_1, lane);
   }
 }
 
@@ -251,15 +266,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-KernelFn lookup(int NB) {
+template <bool H>
+KernelFn lookup_h(int NB) {
   switch (NB) {
-    case 4: return &wide_dmma_kernel<4>;
-    case 8: return &wide_dmma_kernel<8>;
-    case 12: return &wide_dmma_kernel<12>;
-    case 16: return &wide_dmma_kernel<16>;
+    case 4: return &wide_dmma_kernel<4, H>;
+    case 8: return &wide_dmma_kernel<8, H>;
+    case 12: return &wide_dmma_kernel<12, H>;
+    case 16: return &wide_dmma_kernel<16, H>;
     default: return nullptr;
   }
 }
+
+// the HOOKS instances carry the host-copy pipelining flags (qtt_apply_host)
+KernelFn lookup(int NB, bool hooks) { return hooks ? lookup_h<true>(NB) : lookup_h<false>(NB); }
 
 }  // namespace
 }  // namespace wide
@@ -267,14 +286,18 @@ KernelFn lookup(int NB) {
 size_t wide_smem_bytes(int NB) { return kBarBytes + 1024 + size_t(kWideStages) * wide::stage_bytes(NB); }
 
 cudaError_t wide_prepare(int NB, size_t smem) {
-  wide::KernelFn f = wide::lookup(NB);
-  if (!f) return cudaErrorInvalidValue;
-  return cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              int(smem));
+  for (bool hooks : {false, true}) {
+    wide::KernelFn f = wide::lookup(NB, hooks);
+    if (!f) return cudaErrorInvalidValue;
+    const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
-  wide::KernelFn f = wide::lookup(a.NB);
+  wide::KernelFn f = wide::lookup(a.NB, a.ready != nullptr || a.done != nullptr);
   auto encode = wide::encode_fn();
   if (!f || !encode) return cudaErrorInvalidValue;
   // A viewed as a 2-D tensor [M rows][K doubles], boxes of 64 rows x 16 doubles
