@@ -106,7 +106,7 @@ qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem_optin, int
 
 /*
  * qtt_apply -- y = A x on `stream` (asynchronous, stream-ordered).
- *   x, y  : DEVICE pointers owned by the caller, column-major N x nrhs,
+ *   x, y  : DEVICE pointers (on the handle's device) owned by the caller, column-major N x nrhs,
  *           16-byte aligned; the ranges [x, x+N*nrhs) and [y, y+N*nrhs)
  *           must not overlap (in-place is impossible, reading R13).
  *   nrhs  : number of right-hand sides, >= 1, with N * nrhs <= 2^31

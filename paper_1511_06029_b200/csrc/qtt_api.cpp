@@ -286,13 +286,16 @@ std::vector<double> shard_projection(int d, const int64_t* ranks, const double* 
   return Wp;
 }
 
-bool is_device_ptr(const void* p) {
+// Device (or managed) memory; with dev >= 0 also on that device (a kernel of a
+// handle on device A must not touch device B's memory).
+bool is_device_ptr(const void* p, int dev = -1) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+  if (at.type == cudaMemoryTypeManaged) return true;
+  return at.type == cudaMemoryTypeDevice && (dev < 0 || at.device == dev);
 }
 
 // Workspace layout: [256 B: per-stage tile counters of the dynamic scheduler]
@@ -724,7 +727,7 @@ qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int
   const uintptr_t bytes = uintptr_t(h->N) * uintptr_t(nrhs) * sizeof(double);
   if (xs < ys + bytes && ys < xs + bytes) return QTT_ERROR_INVALID_VALUE;
   if ((xs % 16) || (ys % 16)) return QTT_ERROR_NOT_SUPPORTED;
-  if (!is_device_ptr(x) || !is_device_ptr(y)) return QTT_ERROR_NOT_SUPPORTED;
+  if (!is_device_ptr(x, h->device) || !is_device_ptr(y, h->device)) return QTT_ERROR_NOT_SUPPORTED;
   return QTT_SUCCESS;
 }
 
@@ -886,7 +889,7 @@ static qtt_status_t check_shard_args(qtt_plan* h, const double* x, const double*
   const uintptr_t yb = xb << h->shard_bits;
   if (xs < ys + yb && ys < xs + xb) return QTT_ERROR_INVALID_VALUE;
   if ((xs % 16) || (ys % 16)) return QTT_ERROR_NOT_SUPPORTED;
-  if (!is_device_ptr(x) || !is_device_ptr(send)) return QTT_ERROR_NOT_SUPPORTED;
+  if (!is_device_ptr(x, h->device) || !is_device_ptr(send, h->device)) return QTT_ERROR_NOT_SUPPORTED;
   return QTT_SUCCESS;
 }
 
