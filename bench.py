@@ -202,7 +202,26 @@ def run_cpu_baseline(cfg, cores, x, budget_s=20.0):
     return {"value": flops / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"oracle.alg2_sweep (Alg. 2, numpy/BLAS) over levels 1..{cfg.d - s_bits} on 1 of "
                       f"2^{s_bits} top-bit blocks of x ({flops / 1e9:.1f} GFLOP, {dt:.1f} s)",
-            "seconds": dt, "blas": apis, "host_cpus": os.cpu_count()}
+            "seconds": dt, "blas": apis, "host_cpus": os.cpu_count(), "affinity_cpus": _affinity(),
+            "cpu_model": _cpu_model()}
+
+
+def _affinity():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return None
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def stage_table(stages, r, N, nrhs, stage_ms, n_timed, P, BW):
@@ -284,7 +303,14 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
             rows, sT, st_ = stage_table(op.stages(), cfg.ranks, cfg.N, cfg.nrhs, sms, nt, P, BW)
             F = op.flops_per_rhs * cfg.nrhs
             Fx = sum(rr["flops_executed"] for rr in rows)
-            out[name] = {"ms_per_apply": med, "ms_single_call_min": mn, "gflops_alg2": F / (med * 1e-3) / 1e9,
+            oracle_ms = None
+            if name in ("c1", "c2", "c3"):   # the CPU oracle (all host cores) on the same input, for scale
+                import oracle
+                t0 = time.perf_counter()
+                oracle.apply_alg2(cores, x_np)
+                oracle_ms = (time.perf_counter() - t0) * 1e3
+            out[name] = {"ms_per_apply": med, "ms_single_call_min": mn, "oracle_cpu_ms": oracle_ms,
+                         "gflops_alg2": F / (med * 1e-3) / 1e9,
                          "tflops_executed": Fx / (med * 1e-3) / 1e12, "launches": op.launches_per_apply,
                          "per_stage_frac": sT / st_ if st_ else None,
                          "per_stage_frac_executed": sum(
