@@ -16,9 +16,10 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.environ.get("QTT_OBJ_DIR", os.path.join(PKG, "build"))
 LIB = os.environ.get("QTT_LIB_OUT", os.path.join(PKG, "libqtt_b200.so"))
 
-SOURCES = ["qtt_dmma_inst_kb12.cu", "qtt_dmma_inst_kb34.cu", "qtt_dmma_inst_kb56.cu",
-           "qtt_dmma_inst_kb78.cu", "qtt_wide_kernel.cu", "qtt_morton.cu", "qtt_compressed.cu", "qtt_level_dmma.cu", "qtt_plan.cpp", "qtt_api.cpp"]
-HEADERS = ["qtt_internal.h", "qtt_dmma_kernel.cuh", os.path.join("..", "..", "include", "qtt.h")]
+SOURCES = ["qtt_dmma_inst_kb12.cu", "qtt_dmma_inst_kb34.cu", "qtt_dmma_inst_kb56.cu", "qtt_dmma_inst_kb78.cu",
+           "qtt_wide_kernel.cu", "qtt_morton.cu", "qtt_compressed.cu", "qtt_level_dmma.cu",
+           "qtt_plan.cpp", "qtt_runtime.cpp", "qtt_host_copy.cpp", "qtt_api.cpp", "qtt_api_ext.cpp"]
+HEADERS = ["qtt_internal.h", "qtt_runtime.h", "qtt_dmma_kernel.cuh", os.path.join("..", "..", "include", "qtt.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",

@@ -1,0 +1,408 @@
+// Runtime of libqtt_b200.so: super-core contraction and B-operand packing
+// (SURVEY B1), workspace layout, per-stage launches, the per-apply enqueue and
+// its CUDA-graph cache, argument checks.  The arithmetic of PAPER.md Alg. 2
+// runs entirely in the kernels; nothing here touches vector data.
+#include "qtt_runtime.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+namespace qtt {
+namespace rt {
+qtt_status_t from_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return QTT_SUCCESS;
+  if (std::getenv("QTT_DEBUG")) std::fprintf(stderr, "qtt: CUDA error %s\n", cudaGetErrorString(e));
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return QTT_ERROR_OUT_OF_MEMORY;
+  }
+  return QTT_ERROR_CUDA;
+}
+
+// Super-core of levels k0..k1 (PAPER Eq. TTdeccores P:519-523 restricted to the
+// stage's digits; qtt_plan.cpp): W[a][ii][jj][b], ii/jj = the stage's output /
+// input digits, first level least significant.  Contracted from the narrow
+// end of the stage (the rank-1 side of a boundary stage): left to right costs
+// sum_l r_in 4^l r_l r_{l+1}, right to left sum_l r_l r_{l+1} 4^(L-l) r_out
+// multiply-adds; fp64 accumulation (R17), inner loops contiguous.
+std::vector<double> super_core(const double* const* cores, const int64_t* ranks, int k0, int k1) {
+  const int L = k1 - k0 + 1;
+  const int64_t r_in = ranks[k0 - 1], r_out = ranks[k1];
+  double lr = 0, rl = 0;
+  for (int l = 1; l < L; ++l) {
+    lr += double(r_in) * std::ldexp(1.0, 2 * l) * double(ranks[k0 - 1 + l]) * double(ranks[k0 + l]);
+    rl += double(ranks[k1 - l - 1]) * double(ranks[k1 - l]) * std::ldexp(1.0, 2 * l) * double(r_out);
+  }
+  if (lr <= rl) {
+    // left to right: V[a][ii + n i][jj + n j][b] = sum_c W[a][ii][jj][c] G[c][i][j][b]
+    const int r0 = int(r_in);
+    std::vector<double> W(cores[k0 - 1], cores[k0 - 1] + size_t(r0) * 4 * ranks[k0]);
+    int n_i = 2;
+    int rc = int(ranks[k0]);
+    for (int k = k0 + 1; k <= k1; ++k) {
+      const double* G = cores[k - 1];
+      const int rb = int(ranks[k]);
+      const int n2 = 2 * n_i;
+      std::vector<double> V(size_t(r0) * n2 * n2 * rb, 0.0);
+      for (int a = 0; a < r0; ++a)
+        for (int ii = 0; ii < n_i; ++ii)
+          for (int jj = 0; jj < n_i; ++jj)
+            for (int c = 0; c < rc; ++c) {
+              const double w = W[((size_t(a) * n_i + ii) * n_i + jj) * rc + c];
+              if (w == 0.0) continue;
+              for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 2; ++j) {
+                  const double* g = G + ((size_t(c) * 2 + i) * 2 + j) * rb;
+                  double* v = &V[((size_t(a) * n2 + ii + n_i * i) * n2 + jj + n_i * j) * rb];
+                  for (int b = 0; b < rb; ++b) v[b] = std::fma(w, g[b], v[b]);
+                }
+            }
+      W.swap(V);
+      n_i = n2;
+      rc = rb;
+    }
+    return W;
+  }
+  // right to left: U[c][ii][jj][b] over levels k+1..k1; prepend level k as the
+  // least significant digit: V[a][i + 2 ii][j + 2 jj][b] = sum_c G_k[a][i][j][c] U[c][ii][jj][b]
+  const int ro = int(r_out);
+  std::vector<double> U(cores[k1 - 1], cores[k1 - 1] + size_t(ranks[k1 - 1]) * 4 * ro);
+  int n_i = 2;
+  for (int k = k1 - 1; k >= k0; --k) {
+    const double* G = cores[k - 1];
+    const int ra = int(ranks[k - 1]), rc = int(ranks[k]);
+    const int n2 = 2 * n_i;
+    std::vector<double> V(size_t(ra) * n2 * n2 * ro, 0.0);
+    for (int a = 0; a < ra; ++a)
+      for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j)
+          for (int c = 0; c < rc; ++c) {
+            const double g = G[((size_t(a) * 2 + i) * 2 + j) * rc + c];
+            if (g == 0.0) continue;
+            const double* u = &U[size_t(c) * n_i * n_i * ro];
+            for (int ii = 0; ii < n_i; ++ii)
+              for (int jj = 0; jj < n_i; ++jj) {
+                double* v = &V[((size_t(a) * n2 + i + 2 * ii) * n2 + j + 2 * jj) * ro];
+                const double* uu = u + (size_t(ii) * n_i + jj) * ro;
+                for (int b = 0; b < ro; ++b) v[b] = std::fma(g, uu[b], v[b]);
+              }
+          }
+    U.swap(V);
+    n_i = n2;
+  }
+  return U;
+}
+
+// Stage super-core W[a][ii][jj][b] as the DMMA B operand:
+//   Bmat[kk][n], kk = jj*r_in + a (the column-merged index of Alg. 2 line 6),
+//   n = ii*RP + b (the row-separated output, Alg. 2 line 8), value W[a,ii,jj,b].
+std::vector<double> pack_dmma(const double* W, const qtt::StagePlan& sp) {
+  const int RP = sp.RP, r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i, K = sp.K;
+  return pack_dmma_fn(sp, [=](int kk, int n) {
+    if (kk >= K) return 0.0;
+    const int jj = kk / r_in, a = kk % r_in;
+    const int ii = n / RP, b = n % RP;
+    return (ii < n_i && b < r_out) ? W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b] : 0.0;
+  });
+}
+
+// Wide stage: Bmat[jj*r_in + a][ii*r_out + b] = W[a,ii,jj,b] (no column padding per ii).
+std::vector<double> pack_wide(const double* W, const qtt::StagePlan& sp) {
+  const int r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i, K = sp.K, nout = sp.n_i * sp.r_out;
+  return pack_wide_fn(sp, [=](int kk, int n) {
+    if (kk >= K || n >= nout) return 0.0;
+    const int jj = kk / r_in, a = kk % r_in;
+    const int ii = n / r_out, b = n % r_out;
+    return W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b];
+  });
+}
+
+// Top-bit sharding: projection vectors of part g onto every
+// output block h, c_{h,g}[alpha] = [G_{d-s+1}(alpha, h_1, g_1, :) ... G_d(:, h_s, g_s, 0)],
+// written as Wp[h * r + alpha], r = ranks[d-s].
+std::vector<double> shard_projection(int d, const int64_t* ranks, const double* const* cores, int s, int g) {
+  const int P = 1 << s;
+  const int r = int(ranks[d - s]);
+  std::vector<double> Wp(size_t(P) * r, 0.0);
+  for (int h = 0; h < P; ++h) {
+    // right to left: v over the bond below level k
+    std::vector<double> v(1, 1.0);
+    for (int l = s; l >= 1; --l) {
+      const int k = d - s + l;                       // 1-based level
+      const int hb = (h >> (l - 1)) & 1, gb = (g >> (l - 1)) & 1;
+      const int ra = int(ranks[k - 1]), rb = int(ranks[k]);
+      const double* G = cores[k - 1];
+      std::vector<double> u(ra, 0.0);
+      for (int a = 0; a < ra; ++a) {
+        double acc = 0.0;
+        for (int b = 0; b < rb; ++b) acc = std::fma(G[((size_t(a) * 2 + hb) * 2 + gb) * rb + b], v[b], acc);
+        u[a] = acc;
+      }
+      v.swap(u);
+    }
+    for (int a = 0; a < r; ++a) Wp[size_t(h) * r + a] = v[a];
+  }
+  return Wp;
+}
+
+// Device (or managed) memory; with dev >= 0 also on that device (a kernel of a
+// handle on device A must not touch device B's memory).
+bool is_device_ptr(const void* p, int dev) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (at.type == cudaMemoryTypeManaged) return true;
+  return at.type == cudaMemoryTypeDevice && (dev < 0 || at.device == dev);
+}
+
+// Workspace layout: [256 B: per-stage tile counters of the dynamic scheduler]
+// [buffer 0][buffer 1], each buffer max stage-boundary rank * N * nrhs doubles
+// (the ping-pong intermediate y_k of Alg. 2 at the stage boundaries).
+
+size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs) {
+  if (h->stages.size() <= 1 && h->shard_bits == 0) return 0;
+  const size_t one = size_t(h->max_interior_rank) * size_t(h->N) * size_t(nrhs) * sizeof(double);
+  return (one + 255) / 256 * 256;
+}
+
+size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs) { return kWsHeader + 2 * ws_buf_bytes(h, nrhs); }
+
+void free_plan(qtt_plan* h) {
+  for (auto& S : h->stages) {
+    if (S.d_bpack) cudaFree(S.d_bpack);
+    if (S.d_core) cudaFree(S.d_core);
+  }
+  for (double* p : h->d_raw)
+    if (p) cudaFree(p);
+  if (h->proj.d_bpack) cudaFree(h->proj.d_bpack);
+  if (h->ws) cudaFree(h->ws);
+  if (h->gx) cudaFree(h->gx);
+  if (h->gy) cudaFree(h->gy);
+  if (h->hx) cudaFree(h->hx);
+  if (h->hy) cudaFree(h->hy);
+  for (auto& e : h->pending) {
+    cudaEventDestroy(e.start);
+    cudaEventDestroy(e.stop);
+  }
+  if (h->last) cudaEventDestroy(h->last);
+  for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+  if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  for (auto& e : h->pipe_events) cudaEventDestroy(e);
+  if (h->d_sync) cudaFree(h->d_sync);
+  delete h;
+}
+
+qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
+  const qtt::StagePlan& sp = S.plan;
+  if (sp.variant == qtt::kGeneric) {
+    const size_t core_elems = size_t(sp.r_in) * 4 * sp.r_out;
+    cudaError_t e = cudaMalloc(&S.d_core, core_elems * sizeof(double));
+    if (e != cudaSuccess) return from_cuda(e);
+    return from_cuda(cudaMemcpy(S.d_core, cores[sp.k0 - 1], core_elems * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (sp.variant == qtt::kWide) {
+    cudaError_t e = qtt::wide_prepare(sp.NB, h->smem_optin);
+    if (e != cudaSuccess) return from_cuda(e);
+    S.ctas_per_sm = 1;
+    const std::vector<double> W = super_core(cores, h->ranks.data(), sp.k0, sp.k1);
+    const std::vector<double> pk = pack_wide(W.data(), sp);
+    e = cudaMalloc(&S.d_bpack, pk.size() * sizeof(double));
+    if (e != cudaSuccess) return from_cuda(e);
+    return from_cuda(cudaMemcpy(S.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  // The attribute is per kernel instance and shared by every stage (and plan)
+  // that uses it, so raise it to the device maximum rather than this stage's need.
+  cudaError_t e = qtt::dmma_prepare(sp.KB, sp.NB, h->smem_optin);
+  if (e != cudaSuccess) return from_cuda(e);
+  int occ = 0;
+  e = qtt::dmma_occupancy(sp.KB, sp.NB, sp.smem, &occ);
+  if (e != cudaSuccess) return from_cuda(e);
+  S.ctas_per_sm = std::max(1, occ);
+  std::vector<double> pk;
+  if (sp.k0 == sp.k1) {
+    pk = pack_dmma(cores[sp.k0 - 1], sp);
+  } else {
+    const std::vector<double> W = super_core(cores, h->ranks.data(), sp.k0, sp.k1);
+    pk = pack_dmma(W.data(), sp);
+  }
+  e = cudaMalloc(&S.d_bpack, pk.size() * sizeof(double));
+  if (e != cudaSuccess) return from_cuda(e);
+  return from_cuda(cudaMemcpy(S.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+// One launch of stage S over GEMM rows [m_base, m_base + M) (all rows: m_base = 0,
+// M = nrhs * N / n_i).  `in` points at the stage input's row 0.  A chunk
+// (m_base > 0) must lie in the first RHS: there every output row is
+// m + Q ii, so offsetting `out` by m_base rows is exact.
+
+cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* in, double* out, int64_t M,
+                         int64_t m_base, int* counter, cudaStream_t st, const WideHooks* hooks) {
+  const qtt::StagePlan& sp = S.plan;
+  const int L = proj ? 0 : sp.k1 - sp.k0 + 1;
+  LevelArgs a;
+  a.in = in + m_base * sp.K;
+  a.out = out + m_base * sp.r_out;
+  a.bpack = S.d_bpack;
+  a.core = S.d_core;
+  a.n_i = sp.n_i;
+  a.log2_q = h->d - L;
+  a.q = int64_t(1) << a.log2_q;
+  a.M = M;
+  a.tile_counter = counter;
+  a.r_in = sp.r_in;
+  a.r_out = sp.r_out;
+  a.RP = sp.RP;
+  a.K = sp.K;
+  a.KB = sp.KB;
+  a.NB = sp.NB;
+  a.rep = sp.rep;
+  a.stages = sp.stages;
+  a.smem = sp.smem;
+  a.nchunks = sp.nchunks;
+  a.ncb = sp.ncb;
+  a.nout = sp.n_i * sp.r_out;
+  if (hooks) {
+    a.ready = hooks->ready;
+    a.ready_val = hooks->ready_val;
+    a.ready_rows = hooks->ready_rows;
+    a.done = hooks->done;
+    a.done_rows = hooks->done_rows;
+  }
+  cudaError_t e;
+  if (sp.variant == qtt::kWide) {
+    const int64_t tiles = (a.M + qtt::kDmmaRowsPerSubtile - 1) / qtt::kDmmaRowsPerSubtile * sp.ncb;
+    a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms)));
+    e = qtt::launch_wide(a, st);
+  } else if (sp.variant != qtt::kGeneric) {
+    const int64_t rows_per_stage = int64_t(qtt::kDmmaRowsPerSubtile) * sp.rep;
+    const int64_t tiles = (a.M + rows_per_stage - 1) / rows_per_stage;
+    a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms) * S.ctas_per_sm));
+    e = qtt::launch_level_dmma(a, st);
+  } else {
+    e = qtt::launch_level_generic(a, st, h->num_sms);
+  }
+  if (e != cudaSuccess && std::getenv("QTT_DEBUG"))
+    std::fprintf(stderr, "qtt: stage (levels %d-%d, variant %d, KB %d NB %d smem %zu grid %d) launch failed: %s\n",
+                 sp.k0, sp.k1, sp.variant, sp.KB, sp.NB, a.smem, a.grid, cudaGetErrorString(e));
+  return e;
+}
+
+qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st) {
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  int* counters = reinterpret_cast<int*>(base);
+  const size_t bb = ws_buf_bytes(h, nrhs);
+  double* buf[2] = {reinterpret_cast<double*>(base + kWsHeader), reinterpret_cast<double*>(base + kWsHeader + bb)};
+  cudaError_t me = cudaMemsetAsync(counters, 0, kWsHeader, st);
+  if (me != cudaSuccess) return from_cuda(me);
+  const double* in = x;
+  const int nloc = int(h->stages.size());
+  const int ns = nloc + (h->shard_bits ? 1 : 0);
+  for (int si = 0; si < ns; ++si) {
+    const bool proj = si == nloc;                  // shard projection stage
+    const Stage& S = proj ? h->proj : h->stages[si];
+    double* out = (si == ns - 1) ? y : buf[si & 1];
+    StageEvents ev{};
+    if (h->timing && !proj) {
+      ev.stage = si;
+      if (cudaEventCreate(&ev.start) != cudaSuccess || cudaEventCreate(&ev.stop) != cudaSuccess)
+        return QTT_ERROR_CUDA;
+      cudaEventRecord(ev.start, st);
+    }
+    const int L = proj ? 0 : S.plan.k1 - S.plan.k0 + 1;
+    const int64_t M = nrhs * (int64_t(1) << (h->d - L));
+    const cudaError_t e = launch_stage(h, S, proj, in, out, M, 0, counters + si, st);
+    if (e != cudaSuccess) return from_cuda(e);
+    if (h->timing && !proj) {
+      cudaEventRecord(ev.stop, st);
+      h->pending.push_back(ev);
+    }
+    in = out;
+  }
+  if (h->timing) h->timed_applies++;
+  if (st != h->capture_stream) cudaEventRecord(h->last, st);
+  return QTT_SUCCESS;
+}
+
+// enqueue() through a cached CUDA graph: captured once per (x, y, ws, nrhs) on
+// an internal stream, then replayed on `st` with one launch.  Falls back to a
+// plain enqueue while stage timing is on, when `st` is itself being captured,
+// or with QTT_NO_GRAPH set.
+qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st) {
+  static const bool no_graph = std::getenv("QTT_NO_GRAPH") != nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (no_graph || h->timing || cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return enqueue(h, x, y, nrhs, ws, st);
+  }
+  for (auto& g : h->graphs)
+    if (g.x == x && g.y == y && g.ws == ws && g.nrhs == nrhs) {
+      cudaError_t e = cudaGraphLaunch(g.exec, st);
+      if (e == cudaSuccess) e = cudaEventRecord(h->last, st);
+      return from_cuda(e);
+    }
+  if (!h->capture_stream && cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return QTT_ERROR_CUDA;
+  cudaError_t e = cudaStreamBeginCapture(h->capture_stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return from_cuda(e);
+  const qtt_status_t s = enqueue(h, x, y, nrhs, ws, h->capture_stream);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(h->capture_stream, &graph);
+  if (s != QTT_SUCCESS) {
+    if (graph) cudaGraphDestroy(graph);
+    return s;
+  }
+  if (e != cudaSuccess) return from_cuda(e);
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return from_cuda(e);
+  if (h->graphs.size() >= 8) {
+    cudaGraphExecDestroy(h->graphs.front().exec);
+    h->graphs.erase(h->graphs.begin());
+  }
+  h->graphs.push_back({x, y, ws, nrhs, exec});
+  e = cudaGraphLaunch(exec, st);
+  if (e == cudaSuccess) e = cudaEventRecord(h->last, st);
+  return from_cuda(e);
+}
+
+// The cached workspace is shared by every apply on the handle: order this one
+// after the previous one when that was enqueued on another stream (skipped
+// while `st` is being captured by the caller).
+qtt_status_t order_after_last(qtt_plan* h, cudaStream_t st) {
+  if (!h->has_last || h->last_stream == st) return QTT_SUCCESS;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return QTT_SUCCESS;
+  }
+  return from_cuda(cudaStreamWaitEvent(st, h->last, 0));
+}
+
+qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs) {
+  if (!h || !x || !y || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  if (h->shard_bits) return QTT_ERROR_INVALID_VALUE;   // shard handles use qtt_shard_apply
+  // N * nrhs <= 2^31 keeps every GEMM row index a valid 32-bit TMA coordinate
+  if (nrhs > (int64_t(1) << 31) / h->N) return QTT_ERROR_NOT_SUPPORTED;
+  const uintptr_t xs = reinterpret_cast<uintptr_t>(x), ys = reinterpret_cast<uintptr_t>(y);
+  const uintptr_t bytes = uintptr_t(h->N) * uintptr_t(nrhs) * sizeof(double);
+  if (xs < ys + bytes && ys < xs + bytes) return QTT_ERROR_INVALID_VALUE;
+  if ((xs % 16) || (ys % 16)) return QTT_ERROR_NOT_SUPPORTED;
+  if (!is_device_ptr(x, h->device) || !is_device_ptr(y, h->device)) return QTT_ERROR_NOT_SUPPORTED;
+  return QTT_SUCCESS;
+}
+
+}  // namespace rt
+}  // namespace qtt
