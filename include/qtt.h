@@ -119,6 +119,18 @@ qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem_optin, int
 qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
                        qtt_stream_t stream);
 
+/*
+ * qtt_stage_super_core -- HOST only (no GPU): the super-core a merged stage of
+ * levels [k_first, k_last] applies (at most 12 levels), i.e. the QTT definition
+ * restricted to those digits, contracted over the inner bonds:
+ *   W[a][ii][jj][b] = sum G_k_first(a, i_1 j_1, :) ... G_k_last(:, i_L j_L, b),
+ *   ii = sum_l i_l 2^{l-1}, jj = sum_l j_l 2^{l-1}   (l = 1 is level k_first)
+ * written as ranks[k_first-1] * 2^L * 2^L * ranks[k_last] doubles, row-major.
+ * cores/ranks as qtt_create (only levels k_first..k_last are read).
+ */
+qtt_status_t qtt_stage_super_core(int d, const int64_t* ranks, const double* const* cores, int k_first,
+                                  int k_last, double* W);
+
 /* Bytes of device workspace one apply with `nrhs` right-hand sides needs
  * (256 bytes of scheduler counters plus two ping-pong buffers of max
  * stage-boundary rank * N * nrhs doubles; absent for a one-stage plan). */

@@ -109,6 +109,18 @@ def qtt_plan_stages(ranks, smem_optin: int = 0, max_stage_levels: int = MAX_STAG
     return [(a[i], b[i], v[i]) for i in range(n.value)]
 
 
+def stage_super_core(cores, k_first: int, k_last: int) -> np.ndarray:
+    """Host-only: the super-core W[a][ii][jj][b] of levels k_first..k_last (1-based)."""
+    arrs, ranks = _marshal_cores(cores, None)
+    d = len(arrs)
+    L = k_last - k_first + 1
+    W = np.empty((ranks[k_first - 1], 1 << L, 1 << L, ranks[k_last]), dtype=np.float64)
+    _lib.check("qtt_stage_super_core", _lib.load().qtt_stage_super_core(
+        d, (C.c_int64 * (d + 1))(*ranks), (C.c_void_p * d)(*[a.ctypes.data for a in arrs]),
+        int(k_first), int(k_last), W.ctypes.data))
+    return W
+
+
 def plan_stages(ranks, max_stage_levels: int = MAX_STAGE_LEVELS):
     """Like qtt_plan_stages with variant names: [{'k_first', 'k_last', 'variant'}]."""
     return [dict(k_first=a, k_last=b, variant=VARIANT_NAMES.get(v, str(v)))

@@ -26,6 +26,7 @@ SYMBOLS = (
     "qtt_product_create", "qtt_product_workspace_size", "qtt_product_apply", "qtt_product_apply_ws",
     "qtt_product_destroy", "qtt_compressed_matvec", "qtt_compressed_matvec_cores",
     "qtt_create_shard", "qtt_shard_apply", "qtt_shard_apply_ws", "qtt_shard_projection",
+    "qtt_stage_super_core",
 )
 
 _lib = None
@@ -99,6 +100,8 @@ def load():
     lib.qtt_shard_apply_ws.argtypes = [h, dp, dp, i64, dp, C.c_size_t, C.c_void_p]
     lib.qtt_shard_projection.restype = st
     lib.qtt_shard_projection.argtypes = [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.c_int, C.c_int, dp]
+    lib.qtt_stage_super_core.restype = st
+    lib.qtt_stage_super_core.argtypes = [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.c_int, C.c_int, dp]
     lib.qtt_destroy.restype = st
     lib.qtt_destroy.argtypes = [h]
     _lib = lib

@@ -244,6 +244,24 @@ qtt_status_t qtt_shard_projection(int d, const int64_t* ranks, const double* con
   return QTT_SUCCESS;
 }
 
+qtt_status_t qtt_stage_super_core(int d, const int64_t* ranks, const double* const* cores, int k_first,
+                                  int k_last, double* W) {
+  if (d < 1 || d > 30 || !ranks || !cores || !W || k_first < 1 || k_last > d || k_first > k_last ||
+      k_last - k_first + 1 > 12)
+    return QTT_ERROR_INVALID_VALUE;
+  for (int k = k_first - 1; k <= k_last; ++k)
+    if (ranks[k] < 1 || ranks[k] > 4096) return QTT_ERROR_INVALID_VALUE;
+  for (int k = k_first - 1; k < k_last; ++k)
+    if (!cores[k]) return QTT_ERROR_INVALID_VALUE;
+  try {
+    const std::vector<double> w = super_core(cores, ranks, k_first, k_last);
+    std::copy(w.begin(), w.end(), W);
+  } catch (...) {
+    return QTT_ERROR_OUT_OF_MEMORY;
+  }
+  return QTT_SUCCESS;
+}
+
 qtt_status_t qtt_workspace_size(qtt_handle_t h, int64_t nrhs, size_t* bytes) {
   if (!h || !bytes || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
   *bytes = ws_bytes_for(h, nrhs);

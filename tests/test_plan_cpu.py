@@ -94,3 +94,32 @@ def test_plan_validation(q):
         q.qtt_plan_stages([1, 2, 1], 0, 0)
     with pytest.raises(QttError):
         q.qtt_plan_stages([1] * 32)
+
+
+# --- super-cores (host logic of merged stages) --------------------------------
+@pytest.mark.parametrize("ranks,k0,k1", [
+    ([1, 3, 5, 2, 1], 1, 4),          # whole operator: W = dense A (r_0 = r_d = 1)
+    ([1, 2, 4, 8, 16, 32, 6, 1], 1, 5),   # bottom stage, contracted left to right
+    ([1, 6, 32, 16, 8, 4, 2, 1], 3, 7),   # top stage, contracted right to left
+    ([1, 4, 7, 9, 3, 1], 2, 4),       # interior stage with open bonds at both ends
+])
+def test_super_core_is_the_qtt_definition(q, ranks, k0, k1):
+    """W[a][ii][jj][b] from the library equals the product of core slices over
+    the stage's digits (Eq. TTdeccores), i.e. the oracle's dense
+    matrix of the sub-train with the open bonds fixed."""
+    import numpy as np
+    import oracle
+    rng = np.random.default_rng(sum(ranks))
+    d = len(ranks) - 1
+    cores = [rng.standard_normal((ranks[k], 2, 2, ranks[k + 1])) for k in range(d)]
+    W = q.stage_super_core(cores, k0, k1)
+    sub = cores[k0 - 1:k1]
+    L = k1 - k0 + 1
+    assert W.shape == (ranks[k0 - 1], 1 << L, 1 << L, ranks[k1])
+    for a in range(ranks[k0 - 1]):
+        for b in range(ranks[k1]):
+            # close the open bonds with unit vectors -> an ordinary QTT (r = 1 ends)
+            first = sub[0][a:a + 1]
+            last = sub[-1][..., b:b + 1]
+            closed = [first] + sub[1:-1] + [last] if L > 1 else [sub[0][a:a + 1, :, :, b:b + 1]]
+            np.testing.assert_allclose(W[a, :, :, b], oracle.dense_matrix(closed), rtol=1e-12, atol=1e-12)
