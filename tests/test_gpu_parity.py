@@ -401,3 +401,27 @@ def test_back_to_back_applies_on_two_streams(qtt):
             assert torch.equal(ya, ref1) and torch.equal(yb, ref2)
     finally:
         op.close()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_plan_fuzz(qtt, seed):
+    """Random depth, rank profile (tapered, flat, spiky, odd) and RHS count
+    through the default plan (whatever mix of resident / merged / wide /
+    generic stages the scheduler picks) against the oracle."""
+    rng = np.random.default_rng(9000 + seed)
+    d = int(rng.integers(2, 17))
+    kind = seed % 4
+    if kind == 0:     # tapered like c4
+        cap = int(rng.integers(2, 60))
+        ranks = [min(2 ** k, 2 ** (d - k), cap) for k in range(d + 1)]
+    elif kind == 1:   # flat
+        r = int(rng.integers(1, 70))
+        ranks = [1] + [r] * (d - 1) + [1]
+    elif kind == 2:   # spiky
+        ranks = [1] + [int(v) for v in rng.choice([1, 2, 3, 17, 40, 64, 96], d - 1)] + [1]
+    else:             # uniform random
+        ranks = [1] + [int(v) for v in rng.integers(1, 50, d - 1)] + [1]
+    nrhs = int(rng.choice([1, 1, 2, 3, 5]))
+    _, cores, x = random_case(9000 + seed, d, max(ranks), nrhs, ranks=ranks)
+    y, st = gpu_apply(qtt, cores, x)
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
