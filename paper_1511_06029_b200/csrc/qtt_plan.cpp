@@ -51,6 +51,12 @@ constexpr size_t kTwoCtaSmem = 113 * 1024;      // two resident-kernel CTAs per 
 
 uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
+// Fraction of the SM-waves a stage keeps busy: its tiles fill ceil(tiles / slots)
+// waves of `slots` CTAs (the last one partly), e.g. 256 tiles on 148 SMs -> 86%.
+double wave_efficiency(double tiles, double slots) {
+  return tiles / (std::ceil(tiles / slots) * slots);
+}
+
 }  // namespace
 
 size_t dmma_smem_bytes(int KB, int NB, int K, int rep, int stages) {
@@ -100,7 +106,7 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
     const double tiles = std::ceil(M / (kDmmaRowsPerSubtile * sp->rep));
     // padded tensor-pipe work: whole tiles of 64 * rep rows, K and N to fragment blocks
     const double flops = 2.0 * tiles * kDmmaRowsPerSubtile * sp->rep * 16.0 * sp->KB * 8.0 * sp->NB;
-    const double u = std::min(1.0, tiles / kSms);                   // fraction of SMs busy
+    const double u = wave_efficiency(tiles, kSms);                   // busy fraction of the SM-waves
     // latency floor of tiny problems: each CTA's tiles run one after another,
     // each at least one TMA round trip
     const double tile_bytes = kDmmaRowsPerSubtile * sp->rep * 8.0 * sp->K;
@@ -136,7 +142,7 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
       const int ncb = (nout + 8 * NBw - 1) / (8 * NBw);
       const double tiles = std::ceil(M / kDmmaRowsPerSubtile) * ncb;
       const double flops = 2.0 * tiles * kDmmaRowsPerSubtile * std::ceil(sp->K / double(kWideBK)) * kWideBK * 8.0 * NBw;
-      const double u = std::min(1.0, tiles / kSms);
+      const double u = wave_efficiency(tiles, kSms);
       const double l2 = tiles * (kDmmaRowsPerSubtile * 8.0 * sp->K + 8.0 * sp->K * 8.0 * NBw);
       // a wide tile streams its k-chunks one after another
       const double nch = std::ceil(sp->K / double(kWideBK));
