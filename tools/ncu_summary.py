@@ -11,6 +11,7 @@ import subprocess
 
 KEYS = {
     "gpu__time_duration.sum": "duration",
+    "sm__ops_path_tensor_src_fp64.sum": "fp64_tensor_ops",
     "dram__bytes_read.sum": "dram_read",
     "dram__bytes_write.sum": "dram_write",
     "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active": "dmma_pipe_pct_active",
@@ -71,6 +72,9 @@ def main():
     if a.algorithmic_flops and "duration" in first:
         out["algorithmic_flops_per_launch"] = a.algorithmic_flops
         out["achieved_tflops_under_ncu"] = a.algorithmic_flops / first["duration"] / 1e12
+        if "fp64_tensor_ops" in first:
+            # FP64 ops the tensor pipe executed (ncu) over the flops this repo claims for the launch
+            out["tensor_fp64_ops_over_claimed_flops"] = first["fp64_tensor_ops"] / a.algorithmic_flops
     with open(a.out, "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "launches"}, indent=1))
