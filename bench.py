@@ -59,7 +59,11 @@ def load_traffic(config):
     ncu --set full capture summary (profiles/*_ncu_full_summary.json), or None."""
     import glob
     best = None
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*summary.json"))):
+    # tags run r01a .. r01z, r01aa, r01ab, ...: order by (length, tag) so the latest wins
+    def tag_key(path):
+        tag = os.path.basename(path).split("_")[0]
+        return (len(tag), tag)
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*summary.json")), key=tag_key):
         try:
             with open(p) as f:
                 d = json.load(f)

@@ -1,0 +1,47 @@
+"""bench.py host logic (-m "not gpu"): the per-stage roofline arithmetic and the
+peak / traffic lookups the JSON line is assembled from."""
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+def test_stage_table_single_and_merged():
+    r = [1, 2, 4, 4, 1]                       # d = 4
+    N, P, BW = 16, 1e12, 1e12
+    stages = [{"k_first": 1, "k_last": 2, "variant": "merged"}, {"k_first": 3, "k_last": 3, "variant": "dmma"},
+              {"k_first": 4, "k_last": 4, "variant": "dmma"}]
+    rows, sT, st = bench.stage_table(stages, r, N, 1, [2.0, 1.0, 1.0], 2, P, BW)
+    # stage 1-2: Alg. 2 flops 4 (1*2 + 2*4) N; executed 2^(L+1) r_in r_out N = 8 * 1 * 4 * N
+    assert rows[0]["flops_alg2"] == 4 * (2 + 8) * N
+    assert rows[0]["flops_executed"] == 8 * 4 * N
+    assert rows[0]["ms"] == pytest.approx(1.0)          # 2.0 ms over 2 timed applies
+    # single level: executed == Alg. 2; bytes 8 N (r_in + r_out) + 32 r_in r_out
+    assert rows[1]["flops_executed"] == rows[1]["flops_alg2"] == 4 * 4 * 4 * N
+    B = 8 * N * (4 + 4) + 32 * 16
+    assert rows[1]["gbs"] == pytest.approx(B / 0.5e-3 / 1e9)
+    T = max(4 * 16 * N / P, B / BW)
+    assert rows[1]["roofline_frac"] == pytest.approx(T / 0.5e-3)
+    assert st == pytest.approx(2e-3)
+
+
+def test_peaks_from_measured_files():
+    hbm, hbm_src, fp64, fp64_src = bench.load_peaks()
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            assert hbm == pytest.approx(float(json.load(f)["hbm_gbs"]))
+        assert "measured" in hbm_src
+    assert 30.0 < fp64 < 45.0                              # DMMA probe (37.08) or the nominal 37.2
+
+
+def test_traffic_lookup_picks_latest_c4_summary():
+    tr = bench.load_traffic("c4")
+    assert tr is not None
+    nbytes, name = tr
+    assert 1.2e10 < nbytes < 1.4e10                        # one r = 48 level: ~12.9 GB
+    assert name.startswith("r01ap")                      # the latest capture (tags ordered by length, then name)
