@@ -59,10 +59,11 @@ def load_traffic(config):
     ncu --set full capture summary (profiles/*_ncu_full_summary.json), or None."""
     import glob
     best = None
-    # tags run r01a .. r01z, r01aa, r01ab, ...: order by (length, tag) so the latest wins
+    # tags r<round><suffix>, suffixes a .. z, aa, ab, ...: latest round, then latest suffix wins
     def tag_key(path):
-        tag = os.path.basename(path).split("_")[0]
-        return (len(tag), tag)
+        import re
+        m = re.match(r"r(\d+)([a-z]*)", os.path.basename(path))
+        return (int(m.group(1)), len(m.group(2)), m.group(2)) if m else (-1, 0, "")
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*summary.json")), key=tag_key):
         try:
             with open(p) as f:

@@ -44,4 +44,11 @@ def test_traffic_lookup_picks_latest_c4_summary():
     assert tr is not None
     nbytes, name = tr
     assert 1.2e10 < nbytes < 1.4e10                        # one r = 48 level: ~12.9 GB
-    assert name.startswith("r01ap")                      # the latest capture (tags ordered by length, then name)
+    import glob
+    import re
+    def key(n):
+        m = re.match(r"r(\d+)([a-z]*)", n)
+        return (int(m.group(1)), len(m.group(2)), m.group(2))
+    c4 = [os.path.basename(p) for p in glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*summary.json"))
+          if json.load(open(p)).get("config") == "c4"]
+    assert name == max(c4, key=key)                       # the latest capture by round, then suffix
