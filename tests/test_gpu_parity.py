@@ -425,3 +425,28 @@ def test_random_plan_fuzz(qtt, seed):
     _, cores, x = random_case(9000 + seed, d, max(ranks), nrhs, ranks=ranks)
     y, st = gpu_apply(qtt, cores, x)
     oracle.assert_close(y, oracle.apply_alg2(cores, x))
+
+
+def test_graph_cache_eviction_and_workspace_growth(qtt):
+    """More (x, y) pairs than the 8 cached graphs, and growing nrhs (the cached
+    workspace is reallocated and graphs on the old one dropped): every result
+    stays bitwise equal to the plain enqueue."""
+    _, cores, x = random_case(41, 13, 20, 4)
+    op = qtt.QttOperator(cores)
+    try:
+        xs = [torch.from_numpy(np.ascontiguousarray(np.roll(x, k, axis=1))).cuda() for k in range(11)]
+        op.set_stage_timing(True)
+        refs = [op.apply(t) for t in xs]
+        torch.cuda.synchronize()
+        op.stage_times()
+        op.set_stage_timing(False)
+        for rep in range(2):
+            for t, ref in zip(xs, refs):
+                assert torch.equal(op.apply(t), ref)
+        # growing nrhs: 1 -> 4 -> 2 RHS through the cached workspace
+        for n in (1, 4, 2):
+            y = op.apply(xs[0][:n].contiguous())
+            torch.cuda.synchronize()
+            assert torch.equal(y, refs[0][:n])
+    finally:
+        op.close()
