@@ -293,6 +293,10 @@ def time_applies(fn, steps, warmup, stream):
     return batch, min(single)
 
 
+def op_flops_c4(cfg):
+    return 4 * sum(cfg.ranks[k] * cfg.ranks[k + 1] for k in range(cfg.d)) * cfg.N
+
+
 def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
     """The other BASELINE configs and the NEXT rows, timed after the headline
     (not part of `value`): per config ms/apply, Alg. 2 and executed rates and
@@ -381,6 +385,49 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
                                         "note": "host wall time of the synchronous call: b cores H2D, "
                                                 "product cores, GPU densify of the 2^24-entry result"}
         del c
+    # B12: same-box library comparator -- Alg. 2 level by level on
+    # the same rotating layout with two cuBLAS DGEMMs per level (one per output
+    # half i_k), through torch.matmul; and cuBLAS DGEMM 8192^3 as the library's
+    # FP64 ceiling on this box.  Not the product; a number to beat.
+    cfg4, c4cores, x4 = generate("c4")
+    N4 = cfg4.N
+    rmax = max(cfg4.ranks)
+    bufs = [torch.empty(N4 * rmax, dtype=torch.float64, device=dev) for _ in range(2)]
+    xg = torch.from_numpy(x4).to(dev).view(-1)
+    Bs = []
+    for k, G in enumerate(c4cores):
+        ri, ro = G.shape[0], G.shape[3]
+        Gt = torch.from_numpy(np.ascontiguousarray(G)).to(dev)            # [a][i][j][b]
+        # Bmat_i[j*ri + a][b] = G[a, i, j, b]
+        Bs.append([Gt[:, i, :, :].permute(1, 0, 2).reshape(2 * ri, ro).contiguous() for i in range(2)])
+
+    def cublas_apply():
+        src = xg
+        for k, G in enumerate(c4cores):
+            ri, ro = G.shape[0], G.shape[3]
+            A = src[: N4 * ri].view(N4 // 2, 2 * ri)
+            dst = bufs[k & 1][: N4 * ro].view(2, N4 // 2, ro)
+            for i in range(2):
+                torch.matmul(A, Bs[k][i], out=dst[i])
+            src = bufs[k & 1][: N4 * ro]
+        return src
+    cb_ms, _ = time_applies(cublas_apply, 3, 1, stream)
+    yk = cublas_apply()[:N4].clone()
+    a8 = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    b8 = torch.randn_like(a8)
+    c8 = torch.empty_like(a8)
+    gemm_ms, _ = time_applies(lambda: torch.matmul(a8, b8, out=c8), 3, 1, stream)
+    with q.QttOperator(c4cores) as A4:
+        yq = A4.apply(xg.view(1, -1)).view(-1)
+    rel = float((yq - yk).norm() / yk.norm())
+    out["cublas_comparator"] = {
+        "c4_alg2_two_dgemm_per_level_ms": cb_ms,
+        "c4_alg2_gflops": op_flops_c4(cfg4) / (cb_ms * 1e-3) / 1e9,
+        "rel_l2_vs_library_apply": rel,
+        "dgemm_8192_tflops": 2 * 8192 ** 3 / (gemm_ms * 1e-3) / 1e12,
+        "note": "torch.matmul fp64 (cuBLAS DGEMM) on the same rotating layout as the library's level kernel"}
+    del bufs, xg, Bs, a8, b8, c8, yk, yq
+    torch.cuda.empty_cache()
     # NEXT-1: product of two c4-profile operators, and the grid apply
     _, cM, xg = generate("c4")
     _, cY, _ = generate("c4", seed=1, with_x=False)
