@@ -385,6 +385,21 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
                                         "note": "host wall time of the synchronous call: b cores H2D, "
                                                 "product cores, GPU densify of the 2^24-entry result"}
         del c
+    # SPEC acceptance #9: apply time ~ N log N -- fit the exponent of
+    # time vs N at constant rank 16 over d = 18..24 (per level it is ~N^1)
+    ts, ns = [], []
+    for d_ in (18, 20, 22, 24):
+        ranks = [1] + [16] * (d_ - 1) + [1]
+        _, cores, x_np = random_case(77, d_, 16, 1, ranks=ranks)
+        with q.QttOperator(cores) as op:
+            x = torch.from_numpy(x_np).to(dev)
+            y = torch.empty_like(x)
+            ms, _ = time_applies(lambda: op.apply(x, out=y, stream=stream), 10, 3, stream)
+        ts.append(ms)
+        ns.append(1 << d_)
+    slope = float(np.polyfit(np.log(ns), np.log(ts), 1)[0])
+    out["time_vs_N_rank16"] = {"d": [18, 20, 22, 24], "ms": ts, "loglog_slope": slope,
+                               "note": "Alg. 2 is O(r^2 N log N); slope ~1 (log factor + fixed launch costs)"}
     # B12: same-box library comparator -- Alg. 2 level by level on
     # the same rotating layout with two cuBLAS DGEMMs per level (one per output
     # half i_k), through torch.matmul; and cuBLAS DGEMM 8192^3 as the library's
