@@ -443,6 +443,30 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
         "note": "torch.matmul fp64 (cuBLAS DGEMM) on the same rotating layout as the library's level kernel"}
     del bufs, xg, Bs, a8, b8, c8, yk, yq
     torch.cuda.empty_cache()
+    # NEXT-4 top-bit shards, emulated on this one GPU: the local kernel time of each
+    # part's shard plan (levels 1..d-s on its block + projection) for c4 at P = 2, 4, 8
+    from paper_1511_06029_b200 import parallel as par
+    _, c4c, x4s = generate("c4")
+    xs_full = torch.from_numpy(x4s).to(dev)
+    shard_out = {}
+    for s_ in (1, 2, 3):
+        P_ = 1 << s_
+        per = []
+        for g_ in range(P_):
+            with par.QttShard(c4c, s_, g_) as sh:
+                xb = par.block_of(xs_full, g_, P_).contiguous()
+                send = torch.empty((1, P_, sh.n), dtype=torch.float64, device=dev)
+                ws_ = torch.empty(sh.workspace_size(1) // 8 + 64, dtype=torch.float64, device=dev)
+                ms_g, _ = time_applies(lambda: sh.apply(xb, send=send, workspace=ws_, stream=stream), 3, 1, stream)
+                per.append(ms_g)
+                del xb, send, ws_
+        xfer = (P_ - 1) / P_ * (1 << 24) * 8 / 770e9 * 1e3      # reduce-scatter bytes / measured NVLink 770 GB/s
+        shard_out[f"P{P_}"] = {"local_ms_max": max(per), "local_ms_mean": sum(per) / P_,
+                               "exchange_ms_est": xfer, "projected_ms": max(per) + xfer,
+                               "projected_speedup_vs_1gpu": None}
+    out["sharded_c4_emulated"] = shard_out
+    del xs_full
+    torch.cuda.empty_cache()
     # NEXT-1: product of two c4-profile operators, and the grid apply
     _, cM, xg = generate("c4")
     _, cY, _ = generate("c4", seed=1, with_x=False)
@@ -691,6 +715,9 @@ def main(argv=None):
         del x, y, ws
         torch.cuda.empty_cache()
         extra = extra_measurements(dev, stream, P, BW, args.max_stage_levels)
+        for v in extra.get("sharded_c4_emulated", {}).values():
+            if args.config == "c4":
+                v["projected_speedup_vs_1gpu"] = ms_step / v["projected_ms"]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
