@@ -113,7 +113,7 @@ qtt_status_t apply_host_flagged(qtt_plan* h, const double* x_host, double* y_hos
     in = out;
   }
   // y chunks: rows [m0, m1) of every output block ii, once all their tiles are stored
-  const int cw = 4 * qtt::dmma_col_groups(SL.plan.NB);        // consumer warps per CTA
+  const int cw = 4 * qtt::wide_col_groups(SL.plan.NB);        // consumer warps per CTA
   for (int64_t m0 = 0; m0 < ML; m0 += cl) {
     const int64_t m1 = std::min(ML, m0 + cl);
     const unsigned target = unsigned(((m1 - m0 + 63) / 64) * SL.plan.ncb * cw);

@@ -116,7 +116,16 @@ cudaError_t dmma_occupancy(int KB, int NB, size_t smem, int* ctas_per_sm);
 cudaError_t launch_level_dmma(const LevelArgs& a, cudaStream_t st);
 cudaError_t launch_level_generic(const LevelArgs& a, cudaStream_t st, int num_sms);
 size_t wide_smem_bytes(int NB);
-QTT_HD constexpr int wide_threads(int NB) { return dmma_threads(NB); }
+#ifndef QTT_WIDE_CG4_MIN_NB
+#define QTT_WIDE_CG4_MIN_NB 16
+#endif
+// column groups of the wide kernel's consumer warps: 4 (16 warps, 4 n-blocks
+// each, 96 registers, no spills) for NB = 16 -- measured 1-3.5% faster than
+// 3 groups of 6/5/5 n-blocks (c3 stages, c4 top, large ranks; A/B r01ay)
+QTT_HD constexpr int wide_col_groups(int NB) {
+  return (NB >= QTT_WIDE_CG4_MIN_NB && NB % 4 == 0) ? 4 : dmma_col_groups(NB);
+}
+QTT_HD constexpr int wide_threads(int NB) { return (kDmmaRowGroups * wide_col_groups(NB) + 1) * 32; }
 cudaError_t wide_prepare(int NB, size_t smem);
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st);
 // QTT-compressed matvec cores and TT-vector densification, qtt_compressed.cu

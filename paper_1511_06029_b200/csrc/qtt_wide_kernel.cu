@@ -176,9 +176,9 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
 }
 
 template <int NB, bool HOOKS>
-__global__ void __launch_bounds__(dmma_threads(NB), 1)
+__global__ void __launch_bounds__(wide_threads(NB), 1)
 wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
-  constexpr int CG = dmma_col_groups(NB);
+  constexpr int CG = wide_col_groups(NB);
   constexpr int CW = kDmmaRowGroups * CG;
   constexpr int NBW = (NB + CG - 1) / CG;
   constexpr int NB_1 = (NB - NBW) < NBW ? (NB - NBW) : NBW;
@@ -243,7 +243,10 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   }
   const int rg = warp % kDmmaRowGroups;
   const int cg = warp / kDmmaRowGroups;
-  if (cg == 0) {
+  if constexpr (CG == 4) {
+    static_assert(NB % 4 == 0, "4 column groups need NB % 4 == 0");
+    consumer<NB, NB / 4, HOOKS>(p, full, empty, tile_id, ring, rg, cg * (NB / 4), lane);
+  } else if (cg == 0) {
     consumer<NB, NBW, HOOKS>(p, full, empty, tile_id, ring, rg, 0, lane);
   } else if (cg == 1) {
     if constexpr (NB_1 > 0) consumer<NB, NB_1, HOOKS>(p, full, empty, tile_id, ring, rg, NBW, lane);
@@ -310,7 +313,7 @@ cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  f<<<a.grid, dmma_threads(a.NB), a.smem, st>>>(a, map);
+  f<<<a.grid, wide_threads(a.NB), a.smem, st>>>(a, map);
   return cudaGetLastError();
 }
 
