@@ -133,10 +133,9 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
   // (K need not be a multiple of the k-chunk: the TMA unit zero-fills the A
   // columns past K and the packed W rows past K are zero.)
   if (wbytes <= double(kWideMaxCoreBytes)) {
-    int NBw = nout <= 32 ? 4 : nout <= 64 ? 8 : nout <= 96 ? 12 : 16;
-    // a column block of whole ii blocks when 128 columns cannot hold them but 96
-    // can (r_out = 48 / 24 / 12 ...): measured faster (c4 levels 1-7: 6.15 -> 6.04 ms)
-    if (NBw == 16 && r_out > 1 && 128 % r_out != 0 && 96 % r_out == 0) NBw = 12;
+    // widest column block that the output needs (NB = 16 runs 16 consumer warps;
+    // it beats 96-column blocks of whole ii blocks too: c4 levels 1-7 5.96 vs 6.04 ms)
+    const int NBw = nout <= 32 ? 4 : nout <= 64 ? 8 : nout <= 96 ? 12 : 16;
     const size_t smem = wide_smem_bytes(NBw);
     if (smem <= smem_optin) {
       const int ncb = (nout + 8 * NBw - 1) / (8 * NBw);
