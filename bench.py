@@ -133,6 +133,9 @@ def dist_setup(n_gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: several ranks on one GPU (gloo barriers only; no kernel waits on another rank)
+    if os.environ.get("QTT_BENCH_DEVICE") is not None:
+        local = int(os.environ["QTT_BENCH_DEVICE"])
     if world > 1:
         import torch.distributed as dist
         backend = os.environ.get("QTT_DIST_BACKEND", "nccl")
@@ -523,7 +526,7 @@ def run_sharded(args, world, rank, local, dev, cfg, cores, x_np):
     import torch
     from paper_1511_06029_b200 import parallel as par
     nrhs = cfg.nrhs
-    op = par.ShardedQttOperator(cores)
+    op = par.ShardedQttOperator(cores, fused=(args.exchange == "fused"), max_nrhs=nrhs)
     xb = torch.from_numpy(np.ascontiguousarray(par.block_of(x_np, rank, world))).to(dev)
     send = torch.empty((nrhs, world, op.n), dtype=torch.float64, device=dev)
     yb = torch.empty((nrhs, op.n), dtype=torch.float64, device=dev)
@@ -565,7 +568,8 @@ def run_sharded(args, world, rank, local, dev, cfg, cores, x_np):
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded; random cores with the config's rank profile)",
-           "config": dict(config_desc(cfg, nrhs), parallelism=f"top-bit shards x{world} + NCCL reduce-scatter"),
+           "config": dict(config_desc(cfg, nrhs), parallelism=f"top-bit shards x{world} + "
+                          + ("fused peer-store exchange" if args.exchange == "fused" else "NCCL reduce-scatter")),
            "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                    "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8)},
            "gpu_launches": (len(op._shard.stages())) * args.steps,
@@ -591,6 +595,9 @@ def main(argv=None):
     ap.add_argument("--no-extra", action="store_true", help="skip the other configs / NEXT-row measurements")
     ap.add_argument("--max-stage-levels", type=int, default=None,
                     help="cap on levels per launch (1 = Alg. 2 level by level); default: the library's")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="sharded mode: NCCL reduce-scatter of a send buffer, or the fused projection "
+                         "storing into the other GPUs' receive buffers (CUDA IPC over NVLink)")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
                     help="N>1: independent replicas (weak scaling, default) or one apply sharded by the "
                          "top index bits with one NCCL reduce-scatter (strong scaling; DESIGN.md 9)")

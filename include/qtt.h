@@ -259,6 +259,37 @@ qtt_status_t qtt_shard_apply_ws(qtt_handle_t h, const double* x_local, double* s
 qtt_status_t qtt_shard_projection(int d, const int64_t* ranks, const double* const* cores, int log2_parts,
                                   int part, double* W);
 
+/*
+ * Fused exchange (the compute + collective step in one kernel): instead of a
+ * send buffer and a ReduceScatter, the projection stage stores output block h
+ * of part g straight into part h's receive buffer -- over NVLink when `recv`
+ * holds peer mappings (cudaIpcOpenMemHandle) of the other GPUs' buffers.
+ *   qtt_shard_set_peers  : recv[h] = part h's receive buffer as seen from this
+ *                          device ([P][nrhs][n] doubles, 16-byte aligned), h = 0..P-1
+ *                          (recv[part] is this part's own buffer).
+ *   qtt_shard_apply_fused: local stages + scatter projection; writes slot `part`
+ *                          of every part's buffer.  The caller then makes sure all
+ *                          P parts have finished (e.g. stream sync + a process barrier)
+ *                          before reducing.
+ *   qtt_shard_reduce     : y_local[i] = sum_{g=0..P-1} recv[g * count + i] in that fixed
+ *                          order (count = nrhs * n, even; deterministic).
+ */
+qtt_status_t qtt_shard_set_peers(qtt_handle_t h, double* const* recv, int parts);
+qtt_status_t qtt_shard_apply_fused(qtt_handle_t h, const double* x_local, int64_t nrhs, qtt_stream_t stream);
+qtt_status_t qtt_shard_reduce(const double* recv, double* y_local, int parts, int64_t count, qtt_stream_t stream);
+
+/*
+ * Receive buffers shared between the processes of a node (CUDA IPC): allocate
+ * with qtt_ipc_alloc (a whole cudaMalloc allocation, so the IPC mapping starts
+ * at the pointer), export its 64-byte handle, open the other processes'
+ * handles (peer access enabled lazily), close / free at the end.
+ */
+qtt_status_t qtt_ipc_alloc(size_t bytes, void** ptr);
+qtt_status_t qtt_ipc_free(void* ptr);
+qtt_status_t qtt_ipc_get_handle(void* ptr, unsigned char* handle64);
+qtt_status_t qtt_ipc_open(const unsigned char* handle64, void** ptr);
+qtt_status_t qtt_ipc_close(void* ptr);
+
 /* Plan facts: d, N, max rank, algorithmic flops per right-hand side
  * (4 * sum_k r_{k-1} r_k * N) and the number of kernel
  * launches one apply enqueues.  Any output pointer may be NULL. */

@@ -26,7 +26,8 @@ SYMBOLS = (
     "qtt_product_create", "qtt_product_workspace_size", "qtt_product_apply", "qtt_product_apply_ws",
     "qtt_product_destroy", "qtt_compressed_matvec", "qtt_compressed_matvec_cores",
     "qtt_create_shard", "qtt_shard_apply", "qtt_shard_apply_ws", "qtt_shard_projection",
-    "qtt_stage_super_core",
+    "qtt_stage_super_core", "qtt_shard_set_peers", "qtt_shard_apply_fused", "qtt_shard_reduce",
+    "qtt_ipc_alloc", "qtt_ipc_free", "qtt_ipc_get_handle", "qtt_ipc_open", "qtt_ipc_close",
 )
 
 _lib = None
@@ -102,6 +103,23 @@ def load():
     lib.qtt_shard_projection.argtypes = [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.c_int, C.c_int, dp]
     lib.qtt_stage_super_core.restype = st
     lib.qtt_stage_super_core.argtypes = [C.c_int, C.POINTER(i64), C.POINTER(C.c_void_p), C.c_int, C.c_int, dp]
+    lib.qtt_shard_set_peers.restype = st
+    lib.qtt_shard_set_peers.argtypes = [h, C.POINTER(C.c_void_p), C.c_int]
+    lib.qtt_shard_apply_fused.restype = st
+    lib.qtt_shard_apply_fused.argtypes = [h, dp, i64, C.c_void_p]
+    lib.qtt_shard_reduce.restype = st
+    lib.qtt_shard_reduce.argtypes = [dp, dp, C.c_int, i64, C.c_void_p]
+    vpp = C.POINTER(C.c_void_p)
+    lib.qtt_ipc_alloc.restype = st
+    lib.qtt_ipc_alloc.argtypes = [C.c_size_t, vpp]
+    lib.qtt_ipc_free.restype = st
+    lib.qtt_ipc_free.argtypes = [dp]
+    lib.qtt_ipc_get_handle.restype = st
+    lib.qtt_ipc_get_handle.argtypes = [dp, dp]
+    lib.qtt_ipc_open.restype = st
+    lib.qtt_ipc_open.argtypes = [dp, vpp]
+    lib.qtt_ipc_close.restype = st
+    lib.qtt_ipc_close.argtypes = [dp]
     lib.qtt_destroy.restype = st
     lib.qtt_destroy.argtypes = [h]
     _lib = lib

@@ -112,6 +112,7 @@ static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, 
         st = QTT_ERROR_NOT_SUPPORTED;
       } else {
         const std::vector<double> Wp = shard_projection(d, full_ranks, full_cores, shard_bits, shard_part);
+        h->proj_W = Wp;
         std::vector<double> pk;
         cudaError_t e;
         if (pp.variant == qtt::kWide) {
@@ -224,6 +225,107 @@ qtt_status_t qtt_shard_apply(qtt_handle_t h, const double* x_local, double* send
     return QTT_ERROR_CUDA;
   }
 }
+
+qtt_status_t qtt_shard_set_peers(qtt_handle_t h, double* const* recv, int parts) {
+  if (!h || !recv || h->shard_bits == 0 || parts != (1 << h->shard_bits)) return QTT_ERROR_INVALID_VALUE;
+  for (int g = 0; g < parts; ++g)
+    if (!recv[g] || (reinterpret_cast<uintptr_t>(recv[g]) % 16)) return QTT_ERROR_INVALID_VALUE;
+  try {
+    DeviceGuard gd(h->device);
+    if (!h->proj_fused.d_bpack) {   // the projection as a wide stage with the scatter epilogue
+      qtt::StagePlan& pp = h->proj_fused.plan;
+      const int rp = int(h->ranks[h->d]), r = int(h->proj_W.size() / size_t(parts));
+      if (!qtt::projection_plan_wide(rp, h->shard_bits, h->smem_optin, &pp)) return QTT_ERROR_NOT_SUPPORTED;
+      const std::vector<double>& Wp = h->proj_W;
+      const std::vector<double> pk =
+          pack_wide_fn(pp, [&](int kk, int n) { return (kk < r && n < parts) ? Wp[size_t(n) * r + kk] : 0.0; });
+      cudaError_t e = qtt::wide_prepare(pp.NB, h->smem_optin);
+      if (e == cudaSuccess) e = cudaMalloc(&h->proj_fused.d_bpack, pk.size() * sizeof(double));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(h->proj_fused.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return from_cuda(e);
+      h->proj_fused.ctas_per_sm = 1;
+    }
+    if (!h->d_peers) {
+      cudaError_t e = cudaMalloc(&h->d_peers, size_t(parts) * sizeof(double*));
+      if (e != cudaSuccess) return from_cuda(e);
+    }
+    return from_cuda(cudaMemcpy(h->d_peers, recv, size_t(parts) * sizeof(double*), cudaMemcpyHostToDevice));
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_shard_apply_fused(qtt_handle_t h, const double* x_local, int64_t nrhs, qtt_stream_t stream) {
+  if (!h || !x_local || nrhs < 1 || h->shard_bits == 0 || !h->d_peers) return QTT_ERROR_INVALID_VALUE;
+  if (nrhs > (int64_t(1) << 31) / (h->N << h->shard_bits)) return QTT_ERROR_NOT_SUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(x_local) % 16) || !is_device_ptr(x_local, h->device))
+    return QTT_ERROR_NOT_SUPPORTED;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  try {
+    DeviceGuard g(h->device);
+    const size_t need = ws_bytes_for(h, nrhs);
+    if (need > h->ws_bytes) {
+      if (h->ws) cudaFreeAsync(h->ws, h->ws_stream);
+      h->ws = nullptr;
+      h->ws_bytes = 0;
+      cudaError_t e = cudaMallocAsync(&h->ws, need, st);
+      if (e != cudaSuccess) {
+        h->ws = nullptr;
+        return from_cuda(e);
+      }
+      h->ws_bytes = need;
+      h->ws_stream = st;
+    }
+    qtt_status_t so = order_after_last(h, st);
+    if (so == QTT_SUCCESS) so = enqueue(h, x_local, nullptr, nrhs, h->ws, st, true);
+    if (so == QTT_SUCCESS) {
+      h->last_stream = st;
+      h->has_last = true;
+    }
+    return so;
+  } catch (...) {
+    return QTT_ERROR_CUDA;
+  }
+}
+
+qtt_status_t qtt_shard_reduce(const double* recv, double* y_local, int parts, int64_t count, qtt_stream_t stream) {
+  if (!recv || !y_local || parts < 1 || count < 2 || (count % 2)) return QTT_ERROR_INVALID_VALUE;
+  if ((reinterpret_cast<uintptr_t>(recv) % 16) || (reinterpret_cast<uintptr_t>(y_local) % 16))
+    return QTT_ERROR_NOT_SUPPORTED;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return QTT_ERROR_CUDA;
+  return from_cuda(qtt::launch_shard_reduce(recv, y_local, parts, count, reinterpret_cast<cudaStream_t>(stream), sms));
+}
+
+qtt_status_t qtt_ipc_alloc(size_t bytes, void** ptr) {
+  if (!ptr || bytes == 0) return QTT_ERROR_INVALID_VALUE;
+  *ptr = nullptr;
+  return from_cuda(cudaMalloc(ptr, bytes));
+}
+
+qtt_status_t qtt_ipc_free(void* ptr) { return ptr ? from_cuda(cudaFree(ptr)) : QTT_SUCCESS; }
+
+qtt_status_t qtt_ipc_get_handle(void* ptr, unsigned char* handle64) {
+  if (!ptr || !handle64) return QTT_ERROR_INVALID_VALUE;
+  cudaIpcMemHandle_t hd;
+  const cudaError_t e = cudaIpcGetMemHandle(&hd, ptr);
+  if (e != cudaSuccess) return from_cuda(e);
+  static_assert(sizeof(hd) == 64, "CUDA IPC handles are 64 bytes");
+  std::memcpy(handle64, &hd, 64);
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_ipc_open(const unsigned char* handle64, void** ptr) {
+  if (!handle64 || !ptr) return QTT_ERROR_INVALID_VALUE;
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle64, 64);
+  *ptr = nullptr;
+  return from_cuda(cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+}
+
+qtt_status_t qtt_ipc_close(void* ptr) { return ptr ? from_cuda(cudaIpcCloseMemHandle(ptr)) : QTT_SUCCESS; }
 
 qtt_status_t qtt_shard_projection(int d, const int64_t* ranks, const double* const* cores, int log2_parts,
                                   int part, double* W) {

@@ -91,6 +91,11 @@ struct LevelArgs {
   int64_t ready_rows = 0;
   unsigned* done = nullptr;
   int64_t done_rows = 0;
+  // wide variant, fused shard exchange: output column ii (r_out = 1) of row m is
+  // stored at peers[ii][m] -- part ii's receive slot for this part (NVLink
+  // peer memory on a multi-GPU node)
+  double* const* peers = nullptr;
+  int64_t peer_offset = 0;         // added to every peers[ii] (this part's slot: part * M)
 };
 
 // Host-side stage plan (qtt_plan.cpp): pure function of the rank profile and
@@ -110,6 +115,7 @@ size_t dmma_smem_bytes(int KB, int NB, int K, int rep, int stages);
 bool dmma_tiling(int K, int KB, int NB, size_t smem_optin, int* rep, int* stages, size_t* smem);
 std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels);
 bool projection_plan(int r, int s, size_t smem_optin, StagePlan* sp);
+bool projection_plan_wide(int r, int s, size_t smem_optin, StagePlan* sp);   // fused exchange
 
 cudaError_t dmma_prepare(int KB, int NB, size_t smem);   // sets the max dynamic smem attribute
 cudaError_t dmma_occupancy(int KB, int NB, size_t smem, int* ctas_per_sm);
@@ -128,6 +134,9 @@ QTT_HD constexpr int wide_col_groups(int NB) {
 QTT_HD constexpr int wide_threads(int NB) { return (kDmmaRowGroups * wide_col_groups(NB) + 1) * 32; }
 cudaError_t wide_prepare(int NB, size_t smem);
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st);
+// y[s][c] = sum_g recv[g][s][c] (fixed order g = 0..parts-1), qtt_wide_kernel.cu
+cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,
+                                int num_sms);
 // QTT-compressed matvec cores and TT-vector densification, qtt_compressed.cu
 cudaError_t compressed_cores(int d, const int64_t* ra, const double* const* dG, const int64_t* rb,
                              const double* const* dV, double* const* dC, cudaStream_t st, int num_sms);

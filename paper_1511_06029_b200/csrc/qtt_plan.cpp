@@ -202,6 +202,26 @@ std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_opti
 
 // Projection stage of a shard (top-bit sharding): T[m][alpha]
 // (n rows, K = r) times Wp[alpha][h] (P = 2^s columns), out row m + n (s' (P-1) + h).
+bool projection_plan_wide(int r, int s, size_t smem_optin, StagePlan* sp) {
+  const int P = 1 << s;
+  if (r % 2) return false;                      // TMA tensor map row stride must be 16-byte aligned
+  sp->k0 = sp->k1 = 0;
+  sp->r_in = r;
+  sp->r_out = 1;
+  sp->n_i = P;
+  sp->K = r;
+  sp->variant = kWide;
+  sp->RP = 1;
+  sp->NB = P <= 32 ? 4 : P <= 64 ? 8 : P <= 96 ? 12 : 16;
+  sp->KB = kWideKBC;
+  sp->ncb = (P + 8 * sp->NB - 1) / (8 * sp->NB);
+  sp->nchunks = (r + kWideBK - 1) / kWideBK;
+  sp->rep = 1;
+  sp->stages = kWideStages;
+  sp->smem = wide_smem_bytes(sp->NB);
+  return sp->smem <= smem_optin;
+}
+
 bool projection_plan(int r, int s, size_t smem_optin, StagePlan* sp) {
   const int P = 1 << s;
   sp->k0 = sp->k1 = 0;

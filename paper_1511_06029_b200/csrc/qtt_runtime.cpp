@@ -186,6 +186,8 @@ void free_plan(qtt_plan* h) {
   for (double* p : h->d_raw)
     if (p) cudaFree(p);
   if (h->proj.d_bpack) cudaFree(h->proj.d_bpack);
+  if (h->proj_fused.d_bpack) cudaFree(h->proj_fused.d_bpack);
+  if (h->d_peers) cudaFree(h->d_peers);
   if (h->ws) cudaFree(h->ws);
   if (h->gx) cudaFree(h->gx);
   if (h->gy) cudaFree(h->gy);
@@ -274,6 +276,8 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
   a.ncb = sp.ncb;
   a.nout = sp.n_i * sp.r_out;
   if (hooks) {
+    a.peers = hooks->peers;
+    a.peer_offset = hooks->peer_offset;
     a.ready = hooks->ready;
     a.ready_val = hooks->ready_val;
     a.ready_rows = hooks->ready_rows;
@@ -299,7 +303,8 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
   return e;
 }
 
-qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st) {
+qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
+                     bool fused) {
   unsigned char* base = static_cast<unsigned char*>(ws);
   int* counters = reinterpret_cast<int*>(base);
   const size_t bb = ws_buf_bytes(h, nrhs);
@@ -311,7 +316,7 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
   const int ns = nloc + (h->shard_bits ? 1 : 0);
   for (int si = 0; si < ns; ++si) {
     const bool proj = si == nloc;                  // shard projection stage
-    const Stage& S = proj ? h->proj : h->stages[si];
+    const Stage& S = proj ? (fused ? h->proj_fused : h->proj) : h->stages[si];
     double* out = (si == ns - 1) ? y : buf[si & 1];
     StageEvents ev{};
     if (h->timing && !proj) {
@@ -322,7 +327,12 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
     }
     const int L = proj ? 0 : S.plan.k1 - S.plan.k0 + 1;
     const int64_t M = nrhs * (int64_t(1) << (h->d - L));
-    const cudaError_t e = launch_stage(h, S, proj, in, out, M, 0, counters + si, st);
+    WideHooks fh;
+    if (proj && fused) {   // write each output block straight into its part's receive slot
+      fh.peers = h->d_peers;
+      fh.peer_offset = int64_t(h->shard_part) * M;
+    }
+    const cudaError_t e = launch_stage(h, S, proj, in, out, M, 0, counters + si, st, (proj && fused) ? &fh : nullptr);
     if (e != cudaSuccess) return from_cuda(e);
     if (h->timing && !proj) {
       cudaEventRecord(ev.stop, st);

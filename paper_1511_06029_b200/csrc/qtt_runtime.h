@@ -49,6 +49,9 @@ struct qtt_plan {
   int shard_bits = 0;
   int shard_part = 0;
   Stage proj;
+  std::vector<double> proj_W;      // c_{h,part}[alpha] (P x r), kept for the fused exchange
+  Stage proj_fused;                // the projection as a wide stage writing into peers
+  double** d_peers = nullptr;      // device table of the P receive buffers (qtt_shard_set_peers)
   int64_t max_interior_rank = 0;
   // cached workspace (qtt_apply)
   void* ws = nullptr;
@@ -120,6 +123,8 @@ struct DeviceGuard {
 constexpr size_t kWsHeader = 256;
 
 struct WideHooks {
+  double* const* peers = nullptr;
+  int64_t peer_offset = 0;
   const unsigned* ready = nullptr;
   unsigned ready_val = 0;
   int64_t ready_rows = 0;
@@ -172,7 +177,8 @@ void free_plan(qtt_plan* h);
 qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores);
 cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* in, double* out, int64_t M,
                          int64_t m_base, int* counter, cudaStream_t st, const WideHooks* hooks = nullptr);
-qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st);
+qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
+                     bool fused = false);
 qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st);
 qtt_status_t order_after_last(qtt_plan* h, cudaStream_t st);
 qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs);

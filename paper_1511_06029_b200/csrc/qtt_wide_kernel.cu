@@ -141,7 +141,25 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
-template <int NB, int NBC, bool HOOKS>
+// Fused shard exchange (r_out = 1): column n of GEMM row m goes to peers[n][m].
+template <int NBC>
+__device__ __forceinline__ void scatter_store(const double (&c)[NBC][4], const LevelArgs& p, int64_t m_first,
+                                              int n_first, int lane) {
+  const int g = lane >> 2, t0 = lane & 3;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t m = m_first + g + 8 * h;
+    if (m >= p.M) continue;
+#pragma unroll
+    for (int nb = 0; nb < NBC; ++nb) {
+      const int n = n_first + nb * 8 + 2 * t0;
+      if (n < p.nout) p.peers[n][p.peer_offset + m] = c[nb][2 * h];
+      if (n + 1 < p.nout) p.peers[n + 1][p.peer_offset + m] = c[nb][2 * h + 1];
+    }
+  }
+}
+
+template <int NB, int NBC, int MODE>
 __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uint64_t* empty, const int64_t* tile_id,
                                          unsigned char* ring, int rg, int nb0, int lane) {
   const int g = lane >> 2;
@@ -165,8 +183,9 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
       chunk = 0;
       const int64_t rt = t / p.ncb;
       const int cb = int(t - rt * p.ncb);
-      tile_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
-      if (HOOKS && p.done) {   // publish this warp's part of the tile to the D2H copy stream
+      if (MODE == 2) scatter_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
+      else tile_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
+      if (MODE == 1 && p.done) {   // publish this warp's part of the tile to the D2H copy stream
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(p.done + (rt * kDmmaRowsPerSubtile) / p.done_rows, 1u);
@@ -175,7 +194,8 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
   }
 }
 
-template <int NB, bool HOOKS>
+// MODE 0: plain; 1: host-copy hooks (qtt_apply_host); 2: fused shard exchange
+template <int NB, int MODE>
 __global__ void __launch_bounds__(wide_threads(NB), 1)
 wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   constexpr int CG = wide_col_groups(NB);
@@ -222,7 +242,7 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
         const int cb = int(t - rt * p.ncb);
         const int m0 = int(rt * kDmmaRowsPerSubtile);
         const double* bsrc = p.bpack + size_t(cb) * p.nchunks * (bbytes / 8);
-        if (HOOKS && p.ready) {   // this tile's rows of A must have arrived from the host
+        if (MODE == 1 && p.ready) {   // this tile's rows of A must have arrived from the host
           const unsigned* f = p.ready + m0 / p.ready_rows;
           while (int(ld_acquire_u32(f) - p.ready_val) < 0) __nanosleep(200);
         }
@@ -245,13 +265,13 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   const int cg = warp / kDmmaRowGroups;
   if constexpr (CG == 4) {
     static_assert(NB % 4 == 0, "4 column groups need NB % 4 == 0");
-    consumer<NB, NB / 4, HOOKS>(p, full, empty, tile_id, ring, rg, cg * (NB / 4), lane);
+    consumer<NB, NB / 4, MODE>(p, full, empty, tile_id, ring, rg, cg * (NB / 4), lane);
   } else if (cg == 0) {
-    consumer<NB, NBW, HOOKS>(p, full, empty, tile_id, ring, rg, 0, lane);
+    consumer<NB, NBW, MODE>(p, full, empty, tile_id, ring, rg, 0, lane);
   } else if (cg == 1) {
-    if constexpr (NB_1 > 0) consumer<NB, NB_1, HOOKS>(p, full, empty, tile_id, ring, rg, NBW, lane);
+    if constexpr (NB_1 > 0) consumer<NB, NB_1, MODE>(p, full, empty, tile_id, ring, rg, NBW, lane);
   } else {
-    if constexpr (NB_2 > 0) consumer<NB, NB_2, HOOKS>(p, full, empty, tile_id, ring, rg, NBW + NB_1, lane);
+    if constexpr (NB_2 > 0) consumer<NB, NB_2, MODE>(p, full, empty, tile_id, ring, rg, NBW + NB_1, lane);
   }
 }
 
@@ -269,19 +289,35 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <bool H>
-KernelFn lookup_h(int NB) {
+template <int MODE>
+KernelFn lookup_m(int NB) {
   switch (NB) {
-    case 4: return &wide_dmma_kernel<4, H>;
-    case 8: return &wide_dmma_kernel<8, H>;
-    case 12: return &wide_dmma_kernel<12, H>;
-    case 16: return &wide_dmma_kernel<16, H>;
+    case 4: return &wide_dmma_kernel<4, MODE>;
+    case 8: return &wide_dmma_kernel<8, MODE>;
+    case 12: return &wide_dmma_kernel<12, MODE>;
+    case 16: return &wide_dmma_kernel<16, MODE>;
     default: return nullptr;
   }
 }
 
-// the HOOKS instances carry the host-copy pipelining flags (qtt_apply_host)
-KernelFn lookup(int NB, bool hooks) { return hooks ? lookup_h<true>(NB) : lookup_h<false>(NB); }
+// MODE 1 instances carry the host-copy pipelining flags (qtt_apply_host),
+// MODE 2 the fused shard exchange
+KernelFn lookup(int NB, int mode) {
+  return mode == 2 ? lookup_m<2>(NB) : mode == 1 ? lookup_m<1>(NB) : lookup_m<0>(NB);
+}
+
+__global__ void shard_reduce_kernel(const double2* __restrict__ recv, double2* __restrict__ y, int parts,
+                                    int64_t count2) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < count2; t += int64_t(gridDim.x) * blockDim.x) {
+    double2 acc = recv[t];
+    for (int g = 1; g < parts; ++g) {
+      const double2 v = recv[int64_t(g) * count2 + t];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    y[t] = acc;
+  }
+}
 
 }  // namespace
 }  // namespace wide
@@ -289,8 +325,8 @@ KernelFn lookup(int NB, bool hooks) { return hooks ? lookup_h<true>(NB) : lookup
 size_t wide_smem_bytes(int NB) { return kBarBytes + 1024 + size_t(kWideStages) * wide::stage_bytes(NB); }
 
 cudaError_t wide_prepare(int NB, size_t smem) {
-  for (bool hooks : {false, true}) {
-    wide::KernelFn f = wide::lookup(NB, hooks);
+  for (int mode : {0, 1, 2}) {
+    wide::KernelFn f = wide::lookup(NB, mode);
     if (!f) return cudaErrorInvalidValue;
     const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -300,7 +336,7 @@ cudaError_t wide_prepare(int NB, size_t smem) {
 }
 
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
-  wide::KernelFn f = wide::lookup(a.NB, a.ready != nullptr || a.done != nullptr);
+  wide::KernelFn f = wide::lookup(a.NB, a.peers ? 2 : (a.ready != nullptr || a.done != nullptr) ? 1 : 0);
   auto encode = wide::encode_fn();
   if (!f || !encode) return cudaErrorInvalidValue;
   // A viewed as a 2-D tensor [M rows][K doubles], boxes of 64 rows x 16 doubles
@@ -314,6 +350,17 @@ cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   f<<<a.grid, wide_threads(a.NB), a.smem, st>>>(a, map);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,
+                                int num_sms) {
+  if (count % 2) return cudaErrorInvalidValue;
+  const int64_t c2 = count / 2;
+  int64_t blocks = (c2 + 255) / 256;
+  blocks = blocks > int64_t(num_sms) * 8 ? int64_t(num_sms) * 8 : (blocks < 1 ? 1 : blocks);
+  wide::shard_reduce_kernel<<<int(blocks), 256, 0, st>>>(reinterpret_cast<const double2*>(recv),
+                                                         reinterpret_cast<double2*>(y), parts, c2);
   return cudaGetLastError();
 }
 

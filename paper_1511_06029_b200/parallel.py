@@ -110,6 +110,33 @@ class QttShard:
                 workspace.numel() * workspace.element_size(), _stream_handle(stream)))
         return send
 
+    # ---- fused exchange: projection stores straight into the parts' receive buffers
+    def set_peers(self, recv_ptrs):
+        """recv_ptrs[h]: device pointer (this process's mapping) of part h's receive
+        buffer, [P][nrhs][n] doubles."""
+        if len(recv_ptrs) != self.P:
+            raise ValueError(f"need {self.P} receive buffers")
+        arr = (C.c_void_p * self.P)(*[int(p) for p in recv_ptrs])
+        _lib.check("qtt_shard_set_peers", _lib.load().qtt_shard_set_peers(self._h, arr, self.P))
+
+    def apply_fused(self, x_local, stream=None):
+        import torch
+        xl = x_local if x_local.dim() == 2 else x_local.view(1, -1)
+        if xl.dtype != torch.float64 or not xl.is_cuda or not xl.is_contiguous() or xl.shape[-1] != self.n:
+            raise ValueError(f"x_local must be a contiguous float64 CUDA tensor with {self.n} columns")
+        _lib.check("qtt_shard_apply_fused", _lib.load().qtt_shard_apply_fused(
+            self._h, _ptr(xl), xl.shape[0], _stream_handle(stream)))
+
+    @staticmethod
+    def reduce(recv, out, stream=None, parts=None):
+        """out = sum over the P slots of recv ([P][nrhs][n] tensor, or a raw device
+        pointer with `parts` given), fixed order."""
+        P = recv.shape[0] if parts is None else int(parts)
+        src = _ptr(recv) if parts is None else int(recv)
+        _lib.check("qtt_shard_reduce", _lib.load().qtt_shard_reduce(
+            src, _ptr(out), P, int(out.numel()), _stream_handle(stream)))
+        return out
+
     def close(self):
         if self._h is not None:
             h, self._h = self._h, None
@@ -128,6 +155,25 @@ class QttShard:
         self.close()
 
 
+def ipc_alloc(nbytes: int) -> int:
+    p = C.c_void_p()
+    _lib.check("qtt_ipc_alloc", _lib.load().qtt_ipc_alloc(int(nbytes), C.byref(p)))
+    return int(p.value)
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = C.create_string_buffer(64)
+    _lib.check("qtt_ipc_get_handle", _lib.load().qtt_ipc_get_handle(int(ptr), C.addressof(buf)))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    buf = C.create_string_buffer(bytes(handle), 64)
+    p = C.c_void_p()
+    _lib.check("qtt_ipc_open", _lib.load().qtt_ipc_open(C.addressof(buf), C.byref(p)))
+    return int(p.value)
+
+
 class ShardedQttOperator:
     """y = A x with x, y sharded by the top index bits over the ranks of `group`.
 
@@ -135,7 +181,7 @@ class ShardedQttOperator:
     returns this rank's block of y.  World size must be a power of two; with
     one rank it is a plain QttOperator."""
 
-    def __init__(self, cores, group=None):
+    def __init__(self, cores, group=None, fused: bool = False, max_nrhs: int = 1):
         import torch.distributed as dist
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -150,10 +196,28 @@ class ShardedQttOperator:
         self.flops_per_rhs = 4.0 * sum(ranks[k] * ranks[k + 1] for k in range(self.d)) * self.N
         self._op = None
         self._shard = None
+        self.fused = bool(fused) and self.s > 0
+        self.max_nrhs = int(max_nrhs)
+        self._recv = None
+        self._peers = []
         if self.s == 0:
             self._op = QttOperator(arrs)
         else:
             self._shard = QttShard(arrs, self.s, self.rank)
+        if self.fused:
+            # every part's receive buffer [P][max_nrhs][n], mapped into every process (CUDA IPC)
+            self._recv = ipc_alloc(self.world * self.max_nrhs * self.n * 8)
+            handles = [None] * self.world
+            dist.all_gather_object(handles, ipc_handle(self._recv), group=group)
+            ptrs = []
+            for r, hd in enumerate(handles):
+                if r == self.rank:
+                    ptrs.append(self._recv)
+                else:
+                    p = ipc_open(hd)
+                    self._peers.append(p)
+                    ptrs.append(p)
+            self._shard.set_peers(ptrs)
 
     def workspace_size(self, nrhs: int = 1) -> int:
         return (self._op or self._shard).workspace_size(nrhs)
@@ -166,9 +230,31 @@ class ShardedQttOperator:
         import torch
         if self._op is not None:
             return self._op.apply(x_local, out=out, stream=stream, workspace=workspace)
+        if self.fused:
+            return self._apply_fused(x_local, out, stream)
         send = self.local_apply(x_local, send=send, stream=stream, workspace=workspace)
         y = torch.empty((send.shape[0], self.n), dtype=torch.float64, device=send.device) if out is None else out
         exchange(send, y.view(send.shape[0], self.n), self.group)
+        return y if x_local.dim() == 2 else y.view(-1)
+
+    def _apply_fused(self, x_local, out, stream):
+        """Projection stores into every part's receive slot (peer memory), then --
+        once all parts are done (stream sync + process barrier) -- each part
+        sums its P slots.  A second barrier keeps the next apply's stores off
+        buffers a slower part is still reducing."""
+        import torch
+        import torch.distributed as dist
+        xl = x_local if x_local.dim() == 2 else x_local.view(1, -1)
+        nrhs = xl.shape[0]
+        if nrhs > self.max_nrhs:
+            raise ValueError(f"nrhs {nrhs} > max_nrhs {self.max_nrhs} given at construction")
+        y = torch.empty((nrhs, self.n), dtype=torch.float64, device=xl.device) if out is None else out
+        self._shard.apply_fused(xl, stream=stream)
+        torch.cuda.synchronize(xl.device)
+        dist.barrier(group=self.group)
+        QttShard.reduce(self._recv, y.view(nrhs, self.n), stream=stream, parts=self.world)
+        torch.cuda.synchronize(xl.device)
+        dist.barrier(group=self.group)
         return y if x_local.dim() == 2 else y.view(-1)
 
     def close(self):
@@ -176,6 +262,13 @@ class ShardedQttOperator:
             if o is not None:
                 o.close()
         self._op = self._shard = None
+        lib = _lib.load()
+        for p in self._peers:
+            lib.qtt_ipc_close(p)
+        self._peers = []
+        if self._recv:
+            lib.qtt_ipc_free(self._recv)
+            self._recv = None
 
     def __del__(self):
         try:

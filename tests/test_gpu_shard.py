@@ -66,3 +66,73 @@ def test_shard_errors(par):
         assert lib.qtt_apply(sh._h, xb.data_ptr(), y.data_ptr(), 1, None) == q._lib.QTT_ERROR_INVALID_VALUE
         with pytest.raises(ValueError):
             sh.apply(torch.zeros(64, dtype=torch.float64, device="cuda"))
+
+
+# ------------------------------------------------------------------ fused exchange
+@pytest.mark.parametrize("d,maxr,s,nrhs", [(10, 12, 1, 1), (12, 24, 2, 2), (13, 33, 3, 1), (11, 48, 2, 3)])
+def test_fused_exchange_emulated(par, d, maxr, s, nrhs):
+    """The projection stores every output block straight into its part's receive
+    slot (the fused compute + exchange); here all P parts' buffers live on this
+    one GPU and the parts run one after another (no kernel waits on another)."""
+    _, cores, x = random_case(1600 + d + s, d, maxr, nrhs)
+    P = 1 << s
+    n = (1 << d) // P
+    recv = [torch.empty((P, nrhs, n), dtype=torch.float64, device="cuda") for _ in range(P)]
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    for g in range(P):
+        with par.QttShard(cores, s, g) as sh:
+            sh.set_peers([r.data_ptr() for r in recv])
+            sh.apply_fused(par.block_of(xt, g, P).contiguous())
+    torch.cuda.synchronize()
+    y = torch.empty((nrhs, 1 << d), dtype=torch.float64, device="cuda")
+    for h in range(P):
+        yh = torch.empty((nrhs, n), dtype=torch.float64, device="cuda")
+        par.QttShard.reduce(recv[h], yh)
+        y[:, h * n:(h + 1) * n] = yh
+    torch.cuda.synchronize()
+    oracle.assert_close(y.cpu().numpy(), oracle.apply_alg2(cores, x))
+
+
+def _fused_worker(rank, world, port, q):
+    import os
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1511_06029_b200 import parallel as par
+        _, cores, x = random_case(1700, 12, 20, 2)
+        op = par.ShardedQttOperator(cores, fused=True, max_nrhs=2)
+        xb = par.block_of(torch.from_numpy(np.ascontiguousarray(x)).cuda(), rank, world).contiguous()
+        errs = []
+        for _ in range(2):
+            y = op.apply(xb)
+            ref = par.block_of(oracle.apply_alg2(cores, x), rank, world)
+            errs.append(float(np.abs(y.cpu().numpy() - ref).max() / np.abs(ref).max()))
+        op.close()
+        q.put((rank, max(errs)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_exchange_two_processes_ipc(par):
+    """Two processes on this one GPU: receive buffers shared through CUDA IPC,
+    host barriers (gloo) between the fused apply and the reduction -- no kernel
+    waits on another process's kernel."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fused_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert max(res.values()) <= 1e-12, res
