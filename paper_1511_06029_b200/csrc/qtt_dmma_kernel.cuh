@@ -16,6 +16,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+// Programmatic dependent launch.  Every stage kernel is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so it may start while the
+// previous kernel on the stream drains its last tiles; pdl_wait() (before the
+// first access to any buffer another kernel writes or reads: activations, tile
+// counters, flags) blocks until that kernel has completed and its stores are
+// visible.  Only static operands (the packed cores) are read before it.
+// pdl_trigger() lets the next kernel launch once every CTA has issued it (or
+// exited): issued when a CTA's scheduler runs out of tiles.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -207,7 +217,8 @@ level_dmma_kernel(const LevelArgs p) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // B operand (the packed core) -> smem, once per CTA.
+  // B operand (the packed core) -> smem, once per CTA.  Read before pdl_wait():
+  // bpack is written once at qtt_create, never by a kernel on the stream.
   {
     const double4* gB = reinterpret_cast<const double4*>(p.bpack);
     for (int i = threadIdx.x; i < KB * NB * 32; i += blockDim.x) sB[i] = gB[i];
@@ -219,6 +230,7 @@ level_dmma_kernel(const LevelArgs p) {
     }
     fence_mbar_init();
   }
+  pdl_wait();
   __syncthreads();
 
   if (warp == CW) {
@@ -232,6 +244,7 @@ level_dmma_kernel(const LevelArgs p) {
         mbar_wait(&empty[s], ph ^ 1u);
         const int64_t t = atomicAdd(p.tile_counter, 1);
         if (t >= nstage_tiles) {
+          pdl_trigger();
           tile_id[s] = -1;
           mbar_arrive(&full[s]);
           break;

@@ -84,8 +84,17 @@ cudaError_t dmma_occupancy(int KB, int NB, size_t smem, int* ctas_per_sm) {
 cudaError_t launch_level_dmma(const LevelArgs& a, cudaStream_t st) {
   KernelFn f = lookup(a.KB, a.NB);
   if (!f) return cudaErrorInvalidValue;
-  f<<<a.grid, dmma_threads(a.NB), a.smem, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.grid);
+  cfg.blockDim = dim3(dmma_threads(a.NB));
+  cfg.dynamicSmemBytes = a.smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, f, a);
 }
 
 cudaError_t launch_level_generic(const LevelArgs& a, cudaStream_t st, int num_sms) {

@@ -42,6 +42,8 @@ using dmma::mbar_arrive;
 using dmma::mbar_arrive_expect_tx;
 using dmma::mbar_init;
 using dmma::mbar_wait;
+using dmma::pdl_trigger;
+using dmma::pdl_wait;
 
 // A chunk in smem: kWideKBC boxes of [64 rows][16 doubles] = 8 KiB each, 128-byte
 // swizzled (16-byte granule c of row r stored at granule c ^ (r % 8)).
@@ -220,6 +222,7 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
     }
     fence_mbar_init();
   }
+  pdl_wait();
   __syncthreads();
 
   if (warp == CW) {
@@ -232,6 +235,7 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
       for (;;) {
         const int64_t t = atomicAdd(p.tile_counter, 1);
         if (t >= ntiles) {
+          pdl_trigger();
           const int s = it % kWideStages;
           mbar_wait(&empty[s], (uint32_t(it / kWideStages) & 1u) ^ 1u);
           tile_id[s] = -1;
@@ -349,8 +353,17 @@ cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  f<<<a.grid, wide_threads(a.NB), a.smem, st>>>(a, map);
-  return cudaGetLastError();
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.grid);
+  cfg.blockDim = dim3(wide_threads(a.NB));
+  cfg.dynamicSmemBytes = a.smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, f, a, map);
 }
 
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,
