@@ -190,6 +190,7 @@ void free_plan(qtt_plan* h) {
   if (h->d_peers) cudaFree(h->d_peers);
   if (h->ws) cudaFree(h->ws);
   if (h->gx) cudaFree(h->gx);
+  if (h->cmv) cudaFree(h->cmv);
   if (h->gy) cudaFree(h->gy);
   if (h->hx) cudaFree(h->hx);
   if (h->hy) cudaFree(h->hy);

@@ -65,6 +65,9 @@ struct qtt_plan {
   double* gy = nullptr;
   size_t g_elems = 0;
   cudaStream_t g_stream = nullptr;
+  // cached scratch of the compressed matvec (b's cores, product cores, densify workspace)
+  void* cmv = nullptr;
+  size_t cmv_bytes = 0;
   // cached staging buffers (qtt_apply_host)
   double* hx = nullptr;
   double* hy = nullptr;
