@@ -24,7 +24,7 @@ def qtt():
 
 
 @pytest.mark.parametrize("dim,levels,nrhs", [(1, 7, 2), (2, 3, 1), (2, 6, 2), (2, 7, 1), (3, 2, 3), (3, 3, 1),
-                                             (3, 4, 2), (3, 5, 1), (3, 6, 1)])
+                                             (3, 4, 2), (3, 5, 1), (3, 6, 1), (3, 5, 2), (2, 8, 3)])
 def test_pack_unpack_bitwise(qtt, dim, levels, nrhs):
     N = 1 << (dim * levels)
     g = np.random.default_rng(dim * 100 + levels).standard_normal((nrhs, N))
