@@ -99,7 +99,8 @@ qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks,
  *   n_stages          : receives the number of stages (<= d).
  *   k_first, k_last, variant : arrays of >= d ints (any may be NULL) receiving
  *                       per stage the 1-based level range and the variant
- *                       (0 generic, 1 DMMA one level, 2 DMMA merged stage).
+ *                       (0 generic, 1 DMMA one level, 2 DMMA merged stage,
+ *                       3 merged stage with the super-core streamed from L2).
  */
 qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
                              int* n_stages, int* k_first, int* k_last, int* variant);
@@ -300,9 +301,21 @@ qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank,
  * Per-stage description: stage s (0 <= s < launches_per_apply) covers levels
  * [*k_first, *k_last] (1-based) and runs kernel variant *variant (0 = generic,
  * 1 = fp64 tensor-core DMMA, one level; 2 = DMMA merged stage of several
- * levels, see qtt_plan_stages).
+ * levels with the super-core in shared memory; 3 = the same with the
+ * super-core streamed from L2 in k-chunks, see qtt_plan_stages).
  */
 qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int* variant);
+
+/*
+ * qtt_get_stage_split -- how many k-ranges stage s splits its GEMM into at
+ * `nrhs` right-hand sides (1 = no split).  A variant-3 stage whose output
+ * tiles alone would leave SMs idle (few GEMM rows, long K: the last stage of
+ * a constant-rank profile, whose super-core has K = 2^L r) computes each
+ * output tile as S partial sums over disjoint k-ranges, added in fixed order
+ * k-range 0..S-1 by the last CTA to finish (bitwise reproducible).  The split
+ * scratch is part of qtt_workspace_size.  Host-only query; no GPU work.
+ */
+qtt_status_t qtt_get_stage_split(qtt_handle_t h, int s, int64_t nrhs, int* ksplit);
 
 /*
  * Stage timing (for the bench's roofline): when enabled, each apply records

@@ -23,7 +23,7 @@ from ._lib import QttError, SYMBOLS
 
 __all__ = [
     "QttOperator", "QttError", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "plan_stages", "qtt_apply", "qtt_apply_ws", "qtt_apply_host",
-    "qtt_workspace_size", "qtt_get_info", "qtt_get_stage", "qtt_set_stage_timing",
+    "qtt_workspace_size", "qtt_get_info", "qtt_get_stage", "qtt_get_stage_split", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy", "qtt_status_string", "library_path", "SYMBOLS",
     "morton_pack", "morton_unpack", "QttProduct",
 ]
@@ -159,6 +159,12 @@ def qtt_get_stage(h: int, s: int) -> dict:
     a, b, v = C.c_int(), C.c_int(), C.c_int()
     _lib.check("qtt_get_stage", _lib.load().qtt_get_stage(h, int(s), C.byref(a), C.byref(b), C.byref(v)))
     return dict(k_first=a.value, k_last=b.value, variant=VARIANT_NAMES.get(v.value, str(v.value)))
+
+
+def qtt_get_stage_split(h: int, s: int, nrhs: int = 1) -> int:
+    k = C.c_int()
+    _lib.check("qtt_get_stage_split", _lib.load().qtt_get_stage_split(h, int(s), int(nrhs), C.byref(k)))
+    return k.value
 
 
 def qtt_set_stage_timing(h: int, enable: bool) -> None:
@@ -327,6 +333,10 @@ class QttOperator:
 
     def stages(self):
         return [qtt_get_stage(self.handle, s) for s in range(self.launches_per_apply)]
+
+    def stage_splits(self, nrhs: int = 1):
+        """Split-K factor of every stage at `nrhs` (1 = unsplit)."""
+        return [qtt_get_stage_split(self.handle, s, nrhs) for s in range(self.launches_per_apply)]
 
     def set_stage_timing(self, enable: bool = True):
         qtt_set_stage_timing(self.handle, enable)

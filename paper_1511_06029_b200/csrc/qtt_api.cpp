@@ -510,6 +510,18 @@ qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int
   return QTT_SUCCESS;
 }
 
+qtt_status_t qtt_get_stage_split(qtt_handle_t h, int s, int64_t nrhs, int* ksplit) {
+  if (!h || !ksplit || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  if (h->shard_bits && s == int(h->stages.size())) {
+    *ksplit = 1;
+    return QTT_SUCCESS;
+  }
+  if (s < 0 || s >= int(h->stages.size())) return QTT_ERROR_INVALID_VALUE;
+  const Stage& S = h->stages[s];
+  *ksplit = stage_ksplit(h, S, nrhs * (int64_t(1) << (h->d - (S.plan.k1 - S.plan.k0 + 1))));
+  return QTT_SUCCESS;
+}
+
 qtt_status_t qtt_set_stage_timing(qtt_handle_t h, int enable) {
   if (!h) return QTT_ERROR_INVALID_VALUE;
   h->timing = enable != 0;

@@ -17,15 +17,18 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 // Programmatic dependent launch.  Every stage kernel is launched with
-// cudaLaunchAttributeProgrammaticStreamSerialization, so it may start while the
-// previous kernel on the stream drains its last tiles; pdl_wait() (before the
-// first access to any buffer another kernel writes or reads: activations, tile
-// counters, flags) blocks until that kernel has completed and its stores are
-// visible.  Only static operands (the packed cores) are read before it.
-// pdl_trigger() lets the next kernel launch once every CTA has issued it (or
-// exited): issued when a CTA's scheduler runs out of tiles.
+// cudaLaunchAttributeProgrammaticStreamSerialization, so its launch is
+// processed while the previous kernel on the stream runs; pdl_wait() (before
+// the first access to any buffer another kernel writes or reads: activations,
+// tile counters, split scratch, flags) blocks until the previous kernel's
+// CTAs have all exited.  Only static operands (the packed cores) are read
+// before it.  No kernel issues griddepcontrol.launch_dependents: the wait
+// returns once every CTA of the previous grid has triggered or exited, and
+// only stores made before a CTA's trigger are guaranteed visible -- an early
+// trigger (when a CTA's scheduler ran dry, with tiles still in flight) let a
+// split-K stage read stale rows; the implicit trigger at CTA
+// exit is the one that is always safe here.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -244,7 +247,6 @@ level_dmma_kernel(const LevelArgs p) {
         mbar_wait(&empty[s], ph ^ 1u);
         const int64_t t = atomicAdd(p.tile_counter, 1);
         if (t >= nstage_tiles) {
-          pdl_trigger();
           tile_id[s] = -1;
           mbar_arrive(&full[s]);
           break;

@@ -78,7 +78,9 @@ qtt_status_t apply_host_flagged(qtt_plan* h, const double* x_host, double* y_hos
   const int L0 = S0.plan.k1 - S0.plan.k0 + 1, LL = SL.plan.k1 - SL.plan.k0 + 1;
   const int64_t M0 = int64_t(1) << (h->d - L0), ML = int64_t(1) << (h->d - LL);
   const int64_t c0 = rows_per_chunk(M0), cl = rows_per_chunk(ML);
+  SplitScratch split;
   cudaError_t e = cudaMemsetAsync(counters, 0, kWsHeader, st);
+  if (e == cudaSuccess) e = setup_split(h, h->ws, 1, st, &split);
   if (e == cudaSuccess) e = cudaMemsetAsync(done, 0, kSyncChunks * sizeof(unsigned), st);
   if (e == cudaSuccess) e = cudaEventRecord(ev[0], st);        // prior work + resets done
   if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[0], 0);
@@ -108,7 +110,8 @@ qtt_status_t apply_host_flagged(qtt_plan* h, const double* x_host, double* y_hos
       hk.done = done;
       hk.done_rows = cl;
     }
-    e = launch_stage(h, S, false, in, out, M, 0, counters + si, st, (si == 0 || si == ns - 1) ? &hk : nullptr);
+    e = launch_stage(h, S, false, in, out, M, 0, counters + si, st, (si == 0 || si == ns - 1) ? &hk : nullptr,
+                     &split);
     if (e != cudaSuccess) return from_cuda(e);
     in = out;
   }
@@ -159,6 +162,8 @@ qtt_status_t apply_host_pipelined(qtt_plan* h, const double* x_host, double* y_h
   cudaError_t e = cudaEventRecord(ev[2 * kChunks], st);               // copies start after prior work on st
   if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[2 * kChunks], 0);
   if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, kWsHeader, st);
+  SplitScratch split;
+  if (e == cudaSuccess) e = setup_split(h, h->ws, 1, st, &split);
   if (e != cudaSuccess) return from_cuda(e);
   auto chunk_rows = [](int64_t M, int c) {
     const int64_t step = (M / kChunks + 63) / 64 * 64;
@@ -182,7 +187,7 @@ qtt_status_t apply_host_pipelined(qtt_plan* h, const double* x_host, double* y_h
           if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[c], 0);
           if (e != cudaSuccess) return from_cuda(e);
         }
-        e = launch_stage(h, S, false, in, out, m1 - m0, m0, counters + (ctr++), st);
+        e = launch_stage(h, S, false, in, out, m1 - m0, m0, counters + (ctr++), st, nullptr, &split);
         if (e != cudaSuccess) return from_cuda(e);
         if (si == ns - 1) {   // y rows m0..m1 of every output block ii (r_d = 1)
           e = cudaEventRecord(ev[kChunks + c], st);
@@ -194,7 +199,7 @@ qtt_status_t apply_host_pipelined(qtt_plan* h, const double* x_host, double* y_h
         }
       }
     } else {
-      e = launch_stage(h, S, false, in, out, M, 0, counters + si, st);
+      e = launch_stage(h, S, false, in, out, M, 0, counters + si, st, nullptr, &split);
       if (e != cudaSuccess) return from_cuda(e);
     }
     in = out;

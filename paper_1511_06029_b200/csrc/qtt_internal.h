@@ -96,6 +96,13 @@ struct LevelArgs {
   // peer memory on a multi-GPU node)
   double* const* peers = nullptr;
   int64_t peer_offset = 0;         // added to every peers[ii] (this part's slot: part * M)
+  // wide variant, split-K (ksplit > 1): tile t = output tile t / ksplit, k-chunks
+  // [(t % ksplit) * kcps, ...); partial sums in `partial`, arrival counters in
+  // split_cnt (zero before the launch, left zero after it)
+  int ksplit = 1;
+  int kcps = 0;                    // k-chunks per split
+  double* partial = nullptr;       // [output tiles][ksplit][consumer warps][split_slot_doubles(NB)]
+  int* split_cnt = nullptr;        // [output tiles][consumer warps]
 };
 
 // Host-side stage plan (qtt_plan.cpp): pure function of the rank profile and
@@ -106,6 +113,7 @@ struct StagePlan {
   int r_in = 0, r_out = 0, n_i = 2;
   int K = 0, KB = 0, NB = 0, RP = 0, rep = 1, stages = 2;
   int nchunks = 1, ncb = 1;        // wide variant
+  int ksplit = 1;                  // wide variant: k-split at nrhs = 1 (re-derived per launch)
   size_t smem = 0;
   double est_seconds = 0;          // cost-model estimate at nrhs = 1
 };
@@ -132,6 +140,19 @@ QTT_HD constexpr int wide_col_groups(int NB) {
   return (NB >= QTT_WIDE_CG4_MIN_NB && NB % 4 == 0) ? 4 : dmma_col_groups(NB);
 }
 QTT_HD constexpr int wide_threads(int NB) { return (kDmmaRowGroups * wide_col_groups(NB) + 1) * 32; }
+QTT_HD constexpr int wide_consumer_warps(int NB) { return kDmmaRowGroups * wide_col_groups(NB); }
+// split-K partial of one consumer warp: 16 rows x (widest column group) x 8 columns
+QTT_HD constexpr int split_slot_doubles(int NB) {
+  return ((NB + wide_col_groups(NB) - 1) / wide_col_groups(NB)) * 128;
+}
+// k-split of a wide stage with `tiles` output tiles of `nchunks` k-chunks on
+// `sms` SMs: minimises waves x (chunks per split + epilogue), 1 = no split
+// (qtt_plan.cpp)
+int wide_ksplit(int64_t tiles, int nchunks, int sms);
+// diagnostics: QTT_NO_PDL=1 launches the stage kernels without programmatic
+// dependent launch, QTT_NO_SPLIT=1 plans no split-K stages
+bool pdl_enabled();
+bool split_enabled();
 cudaError_t wide_prepare(int NB, size_t smem);
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st);
 // y[s][c] = sum_g recv[g][s][c] (fixed order g = 0..parts-1), qtt_wide_kernel.cu

@@ -26,6 +26,7 @@
 #include "qtt_dmma_kernel.cuh"
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace qtt {
@@ -81,12 +82,17 @@ cudaError_t dmma_occupancy(int KB, int NB, size_t smem, int* ctas_per_sm) {
                                                        dmma_threads(NB), smem);
 }
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("QTT_NO_PDL") == nullptr;
+  return on;
+}
+
 cudaError_t launch_level_dmma(const LevelArgs& a, cudaStream_t st) {
   KernelFn f = lookup(a.KB, a.NB);
   if (!f) return cudaErrorInvalidValue;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.grid);
   cfg.blockDim = dim3(dmma_threads(a.NB));

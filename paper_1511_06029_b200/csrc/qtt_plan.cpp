@@ -47,6 +47,7 @@ constexpr double kTileLatency = 1.5e-6;          // one tile: TMA round trip + e
 constexpr double kChunkLatency = 0.4e-6;         // one more k-chunk of a wide tile
 constexpr double kSmBw = 100e9;                  // bytes/s one SM's TMA pulls when few SMs are busy
 constexpr double kSms = 148;
+constexpr double kSplitLatency = 2.5e-6;        // split-K: partial store, arrival atomics, S-way sum
 constexpr size_t kTwoCtaSmem = 113 * 1024;      // two resident-kernel CTAs per SM
 
 uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
@@ -58,6 +59,36 @@ double wave_efficiency(double tiles, double slots) {
 }
 
 }  // namespace
+
+bool split_enabled() {
+  static const bool on = std::getenv("QTT_NO_SPLIT") == nullptr;
+  return on;
+}
+
+int wide_ksplit(int64_t tiles, int nchunks, int sms) {
+  if (tiles <= 0 || nchunks < 4 || !split_enabled()) return 1;
+  // small stages are latency-bound: the partial round trip costs more than the
+  // idle SMs (c1, c2: 20 -> 23 us, 35 -> 45 us split); split from ~28 chunk-times per SM
+  if (double(tiles) * nchunks < 28.0 * sms) return 1;
+  // time in k-chunk units: waves x (chunks per tile + epilogue); a split tile's
+  // epilogue also stores its partial and (last arrival) sums S of them
+  auto cost = [&](int S) {
+    const int cps = (nchunks + S - 1) / S;
+    const double waves = std::ceil(double(tiles) * S / sms);
+    return waves * (cps + (S > 1 ? 1.0 : 0.3));
+  };
+  int best = 1;
+  double bc = cost(1);
+  for (int S = 2; S <= 64 && (nchunks + S - 1) / S >= 2; ++S) {
+    const double c = cost(S);
+    if (c < 0.95 * bc) {   // only for a clear win
+      bc = c;
+      best = S;
+    }
+  }
+  const int cps = (nchunks + best - 1) / best;
+  return (nchunks + cps - 1) / cps;   // no empty split
+}
 
 size_t dmma_smem_bytes(int KB, int NB, int K, int rep, int stages) {
   const size_t stage = round_up(uint32_t(kDmmaRowsPerSubtile * rep) * uint32_t(K) * 8u, 128u);
@@ -139,16 +170,22 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
     const size_t smem = wide_smem_bytes(NBw);
     if (smem <= smem_optin) {
       const int ncb = (nout + 8 * NBw - 1) / (8 * NBw);
-      const double tiles = std::ceil(M / kDmmaRowsPerSubtile) * ncb;
-      const double flops = 2.0 * tiles * kDmmaRowsPerSubtile * std::ceil(sp->K / double(kWideBK)) * kWideBK * 8.0 * NBw;
+      const double tiles_out = std::ceil(M / kDmmaRowsPerSubtile) * ncb;
+      const double nch_all = std::ceil(sp->K / double(kWideBK));
+      // split-K when the output tiles alone leave SMs idle (small M, huge K)
+      const int S = wide_ksplit(int64_t(tiles_out), int(nch_all), int(kSms));
+      const double nch = std::ceil(nch_all / S);                  // k-chunks per tile
+      const double tiles = tiles_out * S;
+      const double flops = 2.0 * tiles_out * kDmmaRowsPerSubtile * nch_all * kWideBK * 8.0 * NBw;
       const double u = wave_efficiency(tiles, kSms);
-      const double l2 = tiles * (kDmmaRowsPerSubtile * 8.0 * sp->K + 8.0 * sp->K * 8.0 * NBw);
+      const double l2 = tiles_out * (kDmmaRowsPerSubtile * 8.0 * sp->K + 8.0 * sp->K * 8.0 * NBw) +
+                        (S > 1 ? 2.0 * tiles * kDmmaRowsPerSubtile * 8.0 * NBw * 8.0 : 0.0);
       // a wide tile streams its k-chunks one after another
-      const double nch = std::ceil(sp->K / double(kWideBK));
       const double tile_bytes = nch * kWideBK * 8.0 * (kDmmaRowsPerSubtile + 8.0 * NBw);
-      const double lat = std::ceil(tiles / kSms) * (kTileLatency + nch * kChunkLatency + tile_bytes / kSmBw);
-      const double t =
-          std::max({flops / (fp64_rate(NBw, nch) * u), (bytes + wbytes) / (kHbm * u), l2 / kL2, lat}) + kLaunch;
+      const double lat = std::ceil(tiles / kSms) * (kTileLatency + nch * kChunkLatency + tile_bytes / kSmBw) +
+                         (S > 1 ? kSplitLatency : 0.0);
+      const double rate = S > 1 ? fp64_rate(NBw, 1e9) * nch / (nch + 1.0) : fp64_rate(NBw, nch);
+      const double t = std::max({flops / (rate * u), (bytes + wbytes) / (kHbm * u), l2 / kL2, lat}) + kLaunch;
       if (!ok || t < sp->est_seconds) {
         sp->variant = kWide;
         sp->NB = NBw;
@@ -156,6 +193,7 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
         sp->RP = r_out;
         sp->ncb = ncb;
         sp->nchunks = (sp->K + kWideBK - 1) / kWideBK;
+        sp->ksplit = S;
         sp->rep = 1;
         sp->stages = kWideStages;
         sp->smem = smem;

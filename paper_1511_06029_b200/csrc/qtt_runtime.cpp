@@ -176,7 +176,62 @@ size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs) {
   return (one + 255) / 256 * 256;
 }
 
-size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs) { return kWsHeader + 2 * ws_buf_bytes(h, nrhs); }
+// Split-K of a wide stage (1 = none): the planner's, fixed per plan whatever
+// the number of RHS or rows of a launch, so every output element is summed in
+// the same order in every path (batch-invariant, chunked host-copy launches
+// included).
+int stage_ksplit(const qtt_plan*, const Stage& S, int64_t) {
+  const qtt::StagePlan& sp = S.plan;
+  return sp.variant == qtt::kWide && sp.ksplit > 1 ? sp.ksplit : 1;
+}
+
+// split-K scratch of one stage: [arrival counters][partials], both 256-aligned
+static void split_bytes(const qtt_plan* h, const Stage& S, int64_t M, size_t* cnt, size_t* part) {
+  *cnt = *part = 0;
+  const int ks = stage_ksplit(h, S, M);
+  if (ks <= 1) return;
+  const int64_t tiles = (M + qtt::kDmmaRowsPerSubtile - 1) / qtt::kDmmaRowsPerSubtile * S.plan.ncb;
+  const int cw = qtt::wide_consumer_warps(S.plan.NB);
+  *cnt = (size_t(tiles) * cw * sizeof(int) + 255) / 256 * 256;
+  *part = size_t(tiles) * ks * cw * qtt::split_slot_doubles(S.plan.NB) * sizeof(double);
+}
+
+size_t ws_split_cnt_bytes(const qtt_plan* h, int64_t nrhs) {
+  size_t m = 0;
+  for (const auto& S : h->stages) {
+    size_t c, p;
+    split_bytes(h, S, nrhs * (int64_t(1) << (h->d - (S.plan.k1 - S.plan.k0 + 1))), &c, &p);
+    m = std::max(m, c);
+  }
+  return m;
+}
+
+static size_t ws_split_bytes(const qtt_plan* h, int64_t nrhs) {
+  size_t mc = 0, mp = 0;
+  for (const auto& S : h->stages) {
+    size_t c, p;
+    split_bytes(h, S, nrhs * (int64_t(1) << (h->d - (S.plan.k1 - S.plan.k0 + 1))), &c, &p);
+    mc = std::max(mc, c);
+    mp = std::max(mp, p);
+  }
+  return mc + mp;
+}
+
+// Split-K scratch after the two buffers; its counters are zeroed here (each
+// split launch leaves them zero for the next).
+cudaError_t setup_split(const qtt_plan* h, void* ws, int64_t nrhs, cudaStream_t st, SplitScratch* out) {
+  *out = SplitScratch{};
+  const size_t scb = ws_split_cnt_bytes(h, nrhs);
+  if (!scb) return cudaSuccess;
+  unsigned char* base = static_cast<unsigned char*>(ws) + kWsHeader + 2 * ws_buf_bytes(h, nrhs);
+  out->cnt = reinterpret_cast<int*>(base);
+  out->partial = reinterpret_cast<double*>(base + scb);
+  return cudaMemsetAsync(out->cnt, 0, scb, st);
+}
+
+size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs) {
+  return kWsHeader + 2 * ws_buf_bytes(h, nrhs) + ws_split_bytes(h, nrhs);
+}
 
 void free_plan(qtt_plan* h) {
   for (auto& S : h->stages) {
@@ -251,7 +306,8 @@ qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
 // m + Q ii, so offsetting `out` by m_base rows is exact.
 
 cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* in, double* out, int64_t M,
-                         int64_t m_base, int* counter, cudaStream_t st, const WideHooks* hooks) {
+                         int64_t m_base, int* counter, cudaStream_t st, const WideHooks* hooks,
+                         const SplitScratch* split) {
   const qtt::StagePlan& sp = S.plan;
   const int L = proj ? 0 : sp.k1 - sp.k0 + 1;
   LevelArgs a;
@@ -287,7 +343,16 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
   }
   cudaError_t e;
   if (sp.variant == qtt::kWide) {
-    const int64_t tiles = (a.M + qtt::kDmmaRowsPerSubtile - 1) / qtt::kDmmaRowsPerSubtile * sp.ncb;
+    int64_t tiles = (a.M + qtt::kDmmaRowsPerSubtile - 1) / qtt::kDmmaRowsPerSubtile * sp.ncb;
+    const int ks = proj ? 1 : stage_ksplit(h, S, M);
+    if (ks > 1 && !split) return cudaErrorInvalidValue;   // caller must provide the scratch
+    if (ks > 1) {
+      a.ksplit = ks;
+      a.kcps = (sp.nchunks + ks - 1) / ks;
+      a.split_cnt = split->cnt;
+      a.partial = split->partial;
+      tiles *= ks;
+    }
     a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms)));
     e = qtt::launch_wide(a, st);
   } else if (sp.variant != qtt::kGeneric) {
@@ -312,6 +377,10 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
   double* buf[2] = {reinterpret_cast<double*>(base + kWsHeader), reinterpret_cast<double*>(base + kWsHeader + bb)};
   cudaError_t me = cudaMemsetAsync(counters, 0, kWsHeader, st);
   if (me != cudaSuccess) return from_cuda(me);
+  SplitScratch split;
+  me = setup_split(h, ws, nrhs, st, &split);
+  if (me != cudaSuccess) return from_cuda(me);
+  const bool scb = split.cnt != nullptr;
   const double* in = x;
   const int nloc = int(h->stages.size());
   const int ns = nloc + (h->shard_bits ? 1 : 0);
@@ -333,7 +402,8 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
       fh.peers = h->d_peers;
       fh.peer_offset = int64_t(h->shard_part) * M;
     }
-    const cudaError_t e = launch_stage(h, S, proj, in, out, M, 0, counters + si, st, (proj && fused) ? &fh : nullptr);
+    const cudaError_t e = launch_stage(h, S, proj, in, out, M, 0, counters + si, st, (proj && fused) ? &fh : nullptr,
+                                       scb ? &split : nullptr);
     if (e != cudaSuccess) return from_cuda(e);
     if (h->timing && !proj) {
       cudaEventRecord(ev.stop, st);

@@ -42,7 +42,6 @@ using dmma::mbar_arrive;
 using dmma::mbar_arrive_expect_tx;
 using dmma::mbar_init;
 using dmma::mbar_wait;
-using dmma::pdl_trigger;
 using dmma::pdl_wait;
 
 // A chunk in smem: kWideKBC boxes of [64 rows][16 doubles] = 8 KiB each, 128-byte
@@ -137,6 +136,12 @@ __device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const Leve
   }
 }
 
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -161,12 +166,65 @@ __device__ __forceinline__ void scatter_store(const double (&c)[NBC][4], const L
   }
 }
 
+// Split-K epilogue (MODE & 4).  Tile t = tile_out * S + ks covers k-chunks
+// [ks * kcps, min(nchunks, (ks + 1) * kcps)).  Each consumer warp stores its
+// 16 x 8*NBC partial to slot (tile_out, ks, warp) of p.partial (lane-minor, 256
+// bytes per store instruction), fences, and counts in on
+// split_cnt[tile_out * CW + warp].  The S-th arrival sums the S partials in
+// the fixed order ks = 0..S-1 (bitwise reproducible whatever the arrival
+// order), resets the counter for the next stage and stores the tile with the
+// ordinary row-separation epilogue.
+template <int NBC>
+__device__ __forceinline__ bool split_reduce(double (&c)[NBC][4], const LevelArgs& p, int64_t tile_out, int ks,
+                                             int warp, int cw, int slot, int lane) {
+  const int S = p.ksplit;
+  double* mine = p.partial + ((tile_out * S + ks) * cw + warp) * int64_t(slot);
+#pragma unroll
+  for (int nb = 0; nb < NBC; ++nb)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) __stcg(mine + (nb * 4 + v) * 32 + lane, c[nb][v]);
+  // release: every lane's partial is ordered before lane 0's arrival (warp
+  // barrier, then lane 0's gpu-scope fence, cumulative over what it observed)
+  __syncwarp();
+  int old = 0;
+  int* cnt = p.split_cnt + tile_out * cw + warp;
+  if (lane == 0) {
+    __threadfence();
+    old = atomicAdd(cnt, 1);
+  }
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old != S - 1) return false;
+  // acquire: lane 0 observed all S arrivals; its fence and the warp barrier
+  // order every lane's loads after them.  Strong (relaxed.gpu) loads: a weak
+  // load need not see another SM's store without this chain (observed:
+  // stale partials on some lanes once kernels overlapped under PDL).
+  if (lane == 0) {
+    __threadfence();
+    *cnt = 0;   // left zero for the next split launch
+  }
+  __syncwarp();
+#pragma unroll
+  for (int nb = 0; nb < NBC; ++nb)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) c[nb][v] = 0.0;
+  for (int k = 0; k < S; ++k) {
+    const double* src = p.partial + ((tile_out * S + k) * cw + warp) * int64_t(slot);
+#pragma unroll
+    for (int nb = 0; nb < NBC; ++nb)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) c[nb][v] += ld_relaxed_f64(src + (nb * 4 + v) * 32 + lane);
+  }
+  return true;
+}
+
 template <int NB, int NBC, int MODE>
 __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uint64_t* empty, const int64_t* tile_id,
-                                         unsigned char* ring, int rg, int nb0, int lane) {
+                                         unsigned char* ring, int rg, int nb0, int lane, int warp = 0, int cw = 0,
+                                         int slot = 0) {
   const int g = lane >> 2;
   double c[NBC][4];
   int chunk = 0;
+  int tile_nch = p.nchunks;
   for (int it = 0;; ++it) {
     const int s = it % kWideStages;
     const uint32_t ph = uint32_t(it / kWideStages) & 1u;
@@ -176,18 +234,27 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
     if (chunk == 0) {
 #pragma unroll
       for (int nb = 0; nb < NBC; ++nb) c[nb][0] = c[nb][1] = c[nb][2] = c[nb][3] = 0.0;
+      if (MODE & 4) {
+        const int ks = int(t % p.ksplit);
+        tile_nch = min(p.kcps, p.nchunks - ks * p.kcps);
+      }
     }
     const unsigned char* st = ring + size_t(s) * stage_bytes(NB);
     chunk_mma<NB, NBC>(c, st, rg * 16 + g, reinterpret_cast<const double2*>(st + kAStageBytes), nb0, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    if (++chunk == p.nchunks) {
+    if (++chunk == tile_nch) {
       chunk = 0;
-      const int64_t rt = t / p.ncb;
-      const int cb = int(t - rt * p.ncb);
-      if (MODE == 2) scatter_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
+      int64_t to = t;
+      if (MODE & 4) {
+        to = t / p.ksplit;
+        if (!split_reduce<NBC>(c, p, to, int(t - to * p.ksplit), warp, cw, slot, lane)) continue;
+      }
+      const int64_t rt = to / p.ncb;
+      const int cb = int(to - rt * p.ncb);
+      if (MODE & 2) scatter_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
       else tile_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
-      if (MODE == 1 && p.done) {   // publish this warp's part of the tile to the D2H copy stream
+      if ((MODE & 1) && p.done) {   // publish this warp's part of the tile to the D2H copy stream
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(p.done + (rt * kDmmaRowsPerSubtile) / p.done_rows, 1u);
@@ -196,7 +263,8 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
   }
 }
 
-// MODE 0: plain; 1: host-copy hooks (qtt_apply_host); 2: fused shard exchange
+// MODE flags: 1 host-copy hooks (qtt_apply_host), 2 fused shard exchange, 4 split-K;
+// instances 0, 1, 2, 4, 5
 template <int NB, int MODE>
 __global__ void __launch_bounds__(wide_threads(NB), 1)
 wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
@@ -229,28 +297,34 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
     // ---------------- producer warp (one elected lane): tile scheduler + TMA loads ----------------
     if (lane == 0) {
       const int64_t M = p.M;
-      const int64_t ntiles = ((M + kDmmaRowsPerSubtile - 1) / kDmmaRowsPerSubtile) * p.ncb;
+      const int64_t ntiles = ((M + kDmmaRowsPerSubtile - 1) / kDmmaRowsPerSubtile) * p.ncb * ((MODE & 4) ? p.ksplit : 1);
       const uint32_t bbytes = b_chunk_bytes(NB);
       int it = 0;
       for (;;) {
         const int64_t t = atomicAdd(p.tile_counter, 1);
         if (t >= ntiles) {
-          pdl_trigger();
           const int s = it % kWideStages;
           mbar_wait(&empty[s], (uint32_t(it / kWideStages) & 1u) ^ 1u);
           tile_id[s] = -1;
           mbar_arrive(&full[s]);
           break;
         }
-        const int64_t rt = t / p.ncb;
-        const int cb = int(t - rt * p.ncb);
+        int64_t to = t;
+        int ch0 = 0, ch1 = p.nchunks;
+        if (MODE & 4) {   // split-K: consecutive tiles are the k-ranges of one output tile
+          to = t / p.ksplit;
+          ch0 = int(t - to * p.ksplit) * p.kcps;
+          ch1 = min(p.nchunks, ch0 + p.kcps);
+        }
+        const int64_t rt = to / p.ncb;
+        const int cb = int(to - rt * p.ncb);
         const int m0 = int(rt * kDmmaRowsPerSubtile);
         const double* bsrc = p.bpack + size_t(cb) * p.nchunks * (bbytes / 8);
-        if (MODE == 1 && p.ready) {   // this tile's rows of A must have arrived from the host
+        if ((MODE & 1) && p.ready) {   // this tile's rows of A must have arrived from the host
           const unsigned* f = p.ready + m0 / p.ready_rows;
           while (int(ld_acquire_u32(f) - p.ready_val) < 0) __nanosleep(200);
         }
-        for (int ch = 0; ch < p.nchunks; ++ch, ++it) {
+        for (int ch = ch0; ch < ch1; ++ch, ++it) {
           const int s = it % kWideStages;
           mbar_wait(&empty[s], (uint32_t(it / kWideStages) & 1u) ^ 1u);
           unsigned char* st = ring + size_t(s) * stage_bytes(NB);
@@ -267,15 +341,17 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   }
   const int rg = warp % kDmmaRowGroups;
   const int cg = warp / kDmmaRowGroups;
+  constexpr int SLOT = split_slot_doubles(NB);
   if constexpr (CG == 4) {
     static_assert(NB % 4 == 0, "4 column groups need NB % 4 == 0");
-    consumer<NB, NB / 4, MODE>(p, full, empty, tile_id, ring, rg, cg * (NB / 4), lane);
+    consumer<NB, NB / 4, MODE>(p, full, empty, tile_id, ring, rg, cg * (NB / 4), lane, warp, CW, SLOT);
   } else if (cg == 0) {
-    consumer<NB, NBW, MODE>(p, full, empty, tile_id, ring, rg, 0, lane);
+    consumer<NB, NBW, MODE>(p, full, empty, tile_id, ring, rg, 0, lane, warp, CW, SLOT);
   } else if (cg == 1) {
-    if constexpr (NB_1 > 0) consumer<NB, NB_1, MODE>(p, full, empty, tile_id, ring, rg, NBW, lane);
+    if constexpr (NB_1 > 0) consumer<NB, NB_1, MODE>(p, full, empty, tile_id, ring, rg, NBW, lane, warp, CW, SLOT);
   } else {
-    if constexpr (NB_2 > 0) consumer<NB, NB_2, MODE>(p, full, empty, tile_id, ring, rg, NBW + NB_1, lane);
+    if constexpr (NB_2 > 0)
+      consumer<NB, NB_2, MODE>(p, full, empty, tile_id, ring, rg, NBW + NB_1, lane, warp, CW, SLOT);
   }
 }
 
@@ -304,10 +380,17 @@ KernelFn lookup_m(int NB) {
   }
 }
 
-// MODE 1 instances carry the host-copy pipelining flags (qtt_apply_host),
-// MODE 2 the fused shard exchange
+// mode flags: 1 host-copy pipelining (qtt_apply_host), 2 fused shard exchange,
+// 4 split-K
 KernelFn lookup(int NB, int mode) {
-  return mode == 2 ? lookup_m<2>(NB) : mode == 1 ? lookup_m<1>(NB) : lookup_m<0>(NB);
+  switch (mode) {
+    case 0: return lookup_m<0>(NB);
+    case 1: return lookup_m<1>(NB);
+    case 2: return lookup_m<2>(NB);
+    case 4: return lookup_m<4>(NB);
+    case 5: return lookup_m<5>(NB);
+    default: return nullptr;
+  }
 }
 
 __global__ void shard_reduce_kernel(const double2* __restrict__ recv, double2* __restrict__ y, int parts,
@@ -329,7 +412,7 @@ __global__ void shard_reduce_kernel(const double2* __restrict__ recv, double2* _
 size_t wide_smem_bytes(int NB) { return kBarBytes + 1024 + size_t(kWideStages) * wide::stage_bytes(NB); }
 
 cudaError_t wide_prepare(int NB, size_t smem) {
-  for (int mode : {0, 1, 2}) {
+  for (int mode : {0, 1, 2, 4, 5}) {
     wide::KernelFn f = wide::lookup(NB, mode);
     if (!f) return cudaErrorInvalidValue;
     const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
@@ -340,7 +423,10 @@ cudaError_t wide_prepare(int NB, size_t smem) {
 }
 
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
-  wide::KernelFn f = wide::lookup(a.NB, a.peers ? 2 : (a.ready != nullptr || a.done != nullptr) ? 1 : 0);
+  const bool split = a.ksplit > 1;
+  const bool hooks = a.ready != nullptr || a.done != nullptr;
+  if (split && (a.peers || !a.partial || !a.split_cnt)) return cudaErrorInvalidValue;
+  wide::KernelFn f = wide::lookup(a.NB, a.peers ? 2 : (split ? 4 : 0) | (hooks ? 1 : 0));
   auto encode = wide::encode_fn();
   if (!f || !encode) return cudaErrorInvalidValue;
   // A viewed as a 2-D tensor [M rows][K doubles], boxes of 64 rows x 16 doubles
@@ -355,7 +441,7 @@ cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
     return cudaErrorInvalidValue;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.grid);
   cfg.blockDim = dim3(wide_threads(a.NB));

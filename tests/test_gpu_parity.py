@@ -122,6 +122,51 @@ def test_large_rank_path(qtt, r, maxL):
     oracle.assert_close(y, oracle.apply_alg2(cores, x))
 
 
+# ------------------------------------------------------------------ split-K wide stages
+SPLIT_CASES = [
+    # d, r, nrhs: constant rank, so the last stage's super-core has K = 2^L r
+    # against few GEMM rows and the stage runs split-K (ragged last k-range
+    # where S does not divide the chunk count)
+    (17, 128, 1), (16, 192, 2), (18, 64, 1),
+]
+
+
+@pytest.mark.parametrize("d,r,nrhs", SPLIT_CASES)
+def test_split_k_stages(qtt, d, r, nrhs):
+    ranks = [1] + [r] * (d - 1) + [1]
+    _, cores, x = random_case(5000 + 7 * d + r, d, r, nrhs, ranks=ranks)
+    op = qtt.QttOperator(cores)
+    try:
+        splits = op.stage_splits(nrhs)
+        assert max(splits) > 1, (op.stages(), splits)
+        xt = torch.from_numpy(x).cuda()
+        y1 = op.apply(xt)
+        y2 = op.apply(xt)           # split counters left at zero; fixed-order sums
+        ws = torch.empty(op.workspace_size(nrhs) // 8 + 1, dtype=torch.float64, device="cuda")
+        y3 = torch.empty_like(xt)
+        op.apply(xt, out=y3, workspace=ws)
+        torch.cuda.synchronize()
+        y1, y2, y3 = y1.cpu().numpy(), y2.cpu().numpy(), y3.cpu().numpy()
+    finally:
+        op.close()
+    oracle.assert_close(y1, oracle.apply_alg2(cores, x))
+    np.testing.assert_array_equal(y1, y2)
+    np.testing.assert_array_equal(y1, y3)
+
+
+def test_split_k_matches_unsplit_host_path(qtt):
+    """qtt_apply_host's pipelined path never splits (its hooks need whole
+    tiles); its result agrees with the split device path within tolerance."""
+    d, r = 18, 64
+    ranks = [1] + [r] * (d - 1) + [1]
+    _, cores, x = random_case(6061, d, r, 1, ranks=ranks)
+    with qtt.QttOperator(cores) as op:
+        assert max(op.stage_splits(1)) > 1
+        yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        yh = op.apply_host(x)
+    oracle.assert_close(yd, yh)
+
+
 # ------------------------------------------------------------------ merged stages (super-cores)
 @pytest.mark.parametrize("maxL", [1, 2, 3, 4, 6, 10])
 @pytest.mark.parametrize("seed,d,maxr,nrhs", [(21, 10, 6, 3), (22, 13, 12, 2), (23, 15, 24, 1), (24, 9, 3, 7),

@@ -14,11 +14,19 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--rank", type=int, default=0, help="constant interior rank (bench's large-rank rows)")
+    ap.add_argument("--d", type=int, default=18)
+    ap.add_argument("--stage-times", action="store_true")
     args = ap.parse_args()
     import torch
     import paper_1511_06029_b200 as q
     from qtt_workload import generate
-    cfg, cores, x = generate(args.config)
+    if args.rank:
+        from qtt_workload import random_case
+        ranks = [1] + [args.rank] * (args.d - 1) + [1]
+        _, cores, x = random_case(4242, args.d, args.rank, 1, ranks=ranks)
+    else:
+        cfg, cores, x = generate(args.config)
     op = q.QttOperator(cores)
     xt = torch.from_numpy(x).cuda()
     y = torch.empty_like(xt)
@@ -26,6 +34,14 @@ def main():
         op.apply(xt, out=y)
     torch.cuda.synchronize()
     print("stages:", [(s["k_first"], s["k_last"], s["variant"]) for s in op.stages()])
+    if args.stage_times:
+        op.set_stage_timing(True)
+        op.stage_times()
+        for _ in range(3):
+            op.apply(xt, out=y)
+        torch.cuda.synchronize()
+        ms, n = op.stage_times()
+        print("stage ms:", [round(m / n, 4) for m in ms])
     print("ok", float(y.abs().sum()))
     op.close()
 
