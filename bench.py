@@ -54,9 +54,11 @@ def load_peaks():
     return hbm, hbm_src, fp64, fp64_src
 
 
-def load_traffic(config):
+def load_traffic(config, flops=None):
     """dram read+write bytes per launch of the dominant kernel from the committed
-    ncu --set full capture summary (profiles/*_ncu_full_summary.json), or None."""
+    ncu --set full capture summary (profiles/*_ncu_full_summary.json), or None.
+    With `flops`, only a summary of a launch of that many algorithmic flops
+    (the dominant kernel's shape, not another stage of the same config) counts."""
     import glob
     best = None
     # tags r<round><suffix>, suffixes a .. z, aa, ab, ...: latest round, then latest suffix wins
@@ -68,6 +70,8 @@ def load_traffic(config):
         try:
             with open(p) as f:
                 d = json.load(f)
+            if flops is not None and d.get("algorithmic_flops_per_launch") != flops:
+                continue
             if d.get("config") == config and d.get("dram_bytes_per_launch"):
                 best = (float(d["dram_bytes_per_launch"]), os.path.basename(p))
         except Exception:
@@ -214,16 +218,27 @@ def run_cpu_baseline(cfg, cores, x, budget_s=20.0):
             "cpu_model": _cpu_model()}
 
 
-def small_config_oracle_ms():
-    """cpu_baseline leg: the oracle's Alg. 2 sweep timed on c1, c2, c3 (whole applies)."""
+def small_config_oracle_ms(threads=None):
+    """cpu_baseline leg: the oracle's Alg. 2 sweep timed on c1, c2, c3 (whole
+    applies); threads=1 limits BLAS to one thread (comparable to
+    the paper's serial Xeon)."""
+    import contextlib
     import oracle
     from qtt_workload import generate
+    ctx = contextlib.nullcontext()
+    if threads is not None:
+        try:
+            from threadpoolctl import threadpool_limits
+            ctx = threadpool_limits(limits=threads)
+        except Exception:
+            return None
     out = {}
-    for name in ("c1", "c2", "c3"):
-        _, cores, x = generate(name)
-        t0 = time.perf_counter()
-        oracle.apply_alg2(cores, x)
-        out[name] = (time.perf_counter() - t0) * 1e3
+    with ctx:
+        for name in ("c1", "c2", "c3"):
+            _, cores, x = generate(name)
+            t0 = time.perf_counter()
+            oracle.apply_alg2(cores, x)
+            out[name] = (time.perf_counter() - t0) * 1e3
     return out
 
 
@@ -685,7 +700,7 @@ def main(argv=None):
     rin, rout = dom_key[1], dom_key[2]
     dom_flops = dom[0]["flops_executed"]
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12
-    tr = load_traffic(args.config)
+    tr = load_traffic(args.config, dom_flops)
     roofline = {"bound": "tensor", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
                 "frac": achieved / fp64, "traffic": tr[0] if tr else None,
                 "kernel": f"level_dmma_kernel r_in={rin} r_out={rout} levels/launch={dom_key[3]} "
@@ -732,6 +747,7 @@ def main(argv=None):
         cpu.pop("seconds", None)
         # the same CPU baseline (the oracle, all host cores) on the small configs, whole applies
         cpu["other_configs_ms"] = small_config_oracle_ms()
+        cpu["other_configs_ms_1thread"] = small_config_oracle_ms(threads=1)
 
     clocks = clk.summary()
     out = {
