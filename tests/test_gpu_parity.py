@@ -154,6 +154,27 @@ def test_split_k_stages(qtt, d, r, nrhs):
     np.testing.assert_array_equal(y1, y3)
 
 
+def test_repeated_applies_alternating_inputs_bitwise(qtt):
+    """Race check (found the early-PDL-trigger bug): c3, whose
+    last stage runs split-K behind a PDL launch, applied 40 times to two
+    alternating inputs; every result bitwise equal to the first of its input."""
+    cfg, cores, x = generate("c3")
+    x2 = np.ascontiguousarray(x[:, ::-1])
+    with qtt.QttOperator(cores) as op:
+        assert max(op.stage_splits(1)) > 1
+        xs = [torch.from_numpy(x).cuda(), torch.from_numpy(x2).cuda()]
+        refs = [op.apply(v).clone() for v in xs]
+        torch.cuda.synchronize()
+        bad = []
+        for i in range(40):
+            y = op.apply(xs[i % 2])
+            torch.cuda.synchronize()
+            if not torch.equal(y, refs[i % 2]):
+                bad.append((i, int((y != refs[i % 2]).sum())))
+    assert not bad, bad
+    oracle.assert_close(refs[0].cpu().numpy(), oracle.apply_alg2(cores, x))
+
+
 def test_split_k_matches_unsplit_host_path(qtt):
     """qtt_apply_host's pipelined path never splits (its hooks need whole
     tiles); its result agrees with the split device path within tolerance."""
