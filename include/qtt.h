@@ -105,6 +105,11 @@ qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks,
 qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
                              int* n_stages, int* k_first, int* k_last, int* variant);
 
+/* qtt_plan_stages plus, per stage, the split-K factor (array of >= d ints,
+ * may be NULL; 1 = unsplit; see qtt_get_stage_split).  Host only. */
+qtt_status_t qtt_plan_stages_split(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
+                                   int* n_stages, int* k_first, int* k_last, int* variant, int* ksplit);
+
 /*
  * qtt_apply -- y = A x on `stream` (asynchronous, stream-ordered).
  *   x, y  : DEVICE pointers (on the handle's device) owned by the caller, column-major N x nrhs,

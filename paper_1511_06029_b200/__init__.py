@@ -122,9 +122,19 @@ def stage_super_core(cores, k_first: int, k_last: int) -> np.ndarray:
 
 
 def plan_stages(ranks, max_stage_levels: int = MAX_STAGE_LEVELS):
-    """Like qtt_plan_stages with variant names: [{'k_first', 'k_last', 'variant'}]."""
-    return [dict(k_first=a, k_last=b, variant=VARIANT_NAMES.get(v, str(v)))
-            for a, b, v in qtt_plan_stages(ranks, 0, max_stage_levels)]
+    """Like qtt_plan_stages with variant names and split-K factors:
+    [{'k_first', 'k_last', 'variant', 'ksplit'}] (host only)."""
+    lib = _lib.load()
+    ranks = [int(r) for r in ranks]
+    d = len(ranks) - 1
+    if d < 1:
+        raise ValueError("need d >= 1")
+    n = C.c_int()
+    a, b, v, k = (C.c_int * d)(), (C.c_int * d)(), (C.c_int * d)(), (C.c_int * d)()
+    _lib.check("qtt_plan_stages_split", lib.qtt_plan_stages_split(
+        d, (C.c_int64 * (d + 1))(*ranks), 0, int(max_stage_levels), C.byref(n), a, b, v, k))
+    return [dict(k_first=a[i], k_last=b[i], variant=VARIANT_NAMES.get(v[i], str(v[i])), ksplit=k[i])
+            for i in range(n.value)]
 
 
 def qtt_apply(h: int, x, y, nrhs: int, stream=None) -> None:

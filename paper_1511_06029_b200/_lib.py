@@ -20,7 +20,7 @@ QTT_ERROR_CUDA = 4
 
 # every symbol include/qtt.h declares
 SYMBOLS = (
-    "qtt_status_string", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "qtt_apply", "qtt_workspace_size", "qtt_apply_ws",
+    "qtt_status_string", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "qtt_plan_stages_split", "qtt_apply", "qtt_workspace_size", "qtt_apply_ws",
     "qtt_apply_host", "qtt_get_info", "qtt_get_stage", "qtt_get_stage_split", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy", "qtt_morton_pack", "qtt_morton_unpack", "qtt_apply_grid",
     "qtt_product_create", "qtt_product_workspace_size", "qtt_product_apply", "qtt_product_apply_ws",
@@ -55,6 +55,8 @@ def load():
     ip = C.POINTER(C.c_int)
     lib.qtt_plan_stages.restype = st
     lib.qtt_plan_stages.argtypes = [C.c_int, C.POINTER(i64), C.c_size_t, C.c_int, ip, ip, ip, ip]
+    lib.qtt_plan_stages_split.restype = st
+    lib.qtt_plan_stages_split.argtypes = [C.c_int, C.POINTER(i64), C.c_size_t, C.c_int, ip, ip, ip, ip, ip]
     lib.qtt_apply.restype = st
     lib.qtt_apply.argtypes = [h, dp, dp, i64, C.c_void_p]
     lib.qtt_workspace_size.restype = st

@@ -289,8 +289,16 @@ bool projection_plan(int r, int s, size_t smem_optin, StagePlan* sp) {
 
 }  // namespace qtt
 
+extern "C" qtt_status_t qtt_plan_stages_split(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
+                                              int* n_stages, int* k_first, int* k_last, int* variant, int* ksplit);
+
 extern "C" qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
                                         int* n_stages, int* k_first, int* k_last, int* variant) {
+  return qtt_plan_stages_split(d, ranks, smem_optin, max_stage_levels, n_stages, k_first, k_last, variant, nullptr);
+}
+
+extern "C" qtt_status_t qtt_plan_stages_split(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
+                                              int* n_stages, int* k_first, int* k_last, int* variant, int* ksplit) {
   if (d < 1 || d > 30 || !ranks || !n_stages || max_stage_levels < 1) return QTT_ERROR_INVALID_VALUE;
   if (ranks[0] != 1 || ranks[d] != 1) return QTT_ERROR_INVALID_VALUE;
   for (int k = 0; k <= d; ++k)
@@ -303,6 +311,7 @@ extern "C" qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem
       if (k_first) k_first[s] = p[s].k0;
       if (k_last) k_last[s] = p[s].k1;
       if (variant) variant[s] = p[s].variant;
+      if (ksplit) ksplit[s] = p[s].variant == qtt::kWide ? p[s].ksplit : 1;
     }
   } catch (...) {
     return QTT_ERROR_OUT_OF_MEMORY;

@@ -78,6 +78,29 @@ def test_huge_rank_falls_back_to_generic(q):
     assert [v for _, _, v in plan] == [1, 3, 0, 3, 1]
 
 
+def test_split_k_only_for_few_tiles_and_long_k(q):
+    """Split-K is planned only for wide stages whose output
+    tiles leave SMs idle and whose work is large: the last stage of long
+    constant-rank profiles.  Never for c4/c5 or the latency-bound c1/c2."""
+    for name in ("c1", "c2", "c4", "c5"):
+        assert all(s["ksplit"] == 1 for s in q.plan_stages(configs.make_config(name).ranks)), name
+    c3 = q.plan_stages(configs.make_config("c3").ranks)
+    assert [s["ksplit"] for s in c3][:-1] == [1] * (len(c3) - 1) and c3[-1]["ksplit"] > 1
+    d, r = 18, 256
+    plan = q.plan_stages([1] + [r] * (d - 1) + [1])
+    last = plan[-1]
+    assert last["variant"] == "wide" and last["k_last"] == d and last["ksplit"] > 1
+    # every split is a non-empty k-range: S <= chunks, ceil(chunks / ceil(chunks / S)) == S
+    L = last["k_last"] - last["k_first"] + 1
+    chunks = -(-(2 ** L) * r // 32)
+    S = last["ksplit"]
+    cps = -(-chunks // S)
+    assert -(-chunks // cps) == S
+    # the split never changes which levels a stage covers
+    check_cover([(s["k_first"], s["k_last"], 3 if s["variant"] == "wide" else 1 if s["variant"] == "dmma"
+                  else 2 if s["variant"] == "merged" else 0) for s in plan], d, 10)
+
+
 def test_rank_one_and_d1(q):
     assert q.qtt_plan_stages([1, 1]) == [(1, 1, 1)]
     plan = q.qtt_plan_stages([1] * 11)
