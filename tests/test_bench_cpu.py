@@ -40,7 +40,11 @@ def test_peaks_from_measured_files():
 
 
 def test_traffic_lookup_picks_latest_c4_summary():
-    tr = bench.load_traffic("c4")
+    """The dominant kernel's traffic comes from the latest capture of THAT
+    kernel shape (an r = 48 level, 4*48*48*N flops), not from another c4 stage
+    captured in the same round."""
+    level_flops = 4 * 48 * 48 * (1 << 24)
+    tr = bench.load_traffic("c4", level_flops)
     assert tr is not None
     nbytes, name = tr
     assert 1.2e10 < nbytes < 1.4e10                        # one r = 48 level: ~12.9 GB
@@ -50,5 +54,6 @@ def test_traffic_lookup_picks_latest_c4_summary():
         m = re.match(r"r(\d+)([a-z]*)", n)
         return (int(m.group(1)), len(m.group(2)), m.group(2))
     c4 = [os.path.basename(p) for p in glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*summary.json"))
-          if json.load(open(p)).get("config") == "c4"]
+          if json.load(open(p)).get("config") == "c4"
+          and json.load(open(p)).get("algorithmic_flops_per_launch") == level_flops]
     assert name == max(c4, key=key)                       # the latest capture by round, then suffix
