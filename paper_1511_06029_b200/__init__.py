@@ -342,7 +342,9 @@ class QttOperator:
         return qtt_workspace_size(self.handle, nrhs)
 
     def stages(self):
-        return [qtt_get_stage(self.handle, s) for s in range(self.launches_per_apply)]
+        """Per launch: {'k_first', 'k_last', 'variant', 'ksplit'} (as plan_stages)."""
+        return [dict(qtt_get_stage(self.handle, s), ksplit=qtt_get_stage_split(self.handle, s, 1))
+                for s in range(self.launches_per_apply)]
 
     def stage_splits(self, nrhs: int = 1):
         """Split-K factor of every stage at `nrhs` (1 = unsplit)."""

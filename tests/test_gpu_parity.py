@@ -429,6 +429,42 @@ def test_apply_host_pipelined_bitwise(qtt, name):
         op.close()
 
 
+_CHUNKED_HOST_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1511_06029_b200 as q
+from qtt_workload import generate, random_case
+cases = [("c3", None), ("split", (18, 64))]
+for name, dr in cases:
+    if dr is None:
+        _, cores, x = generate(name)
+    else:
+        d, r = dr
+        _, cores, x = random_case(6061, d, r, 1, ranks=[1] + [r] * (d - 1) + [1])
+    with q.QttOperator(cores) as op:
+        yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        for _ in range(2):
+            yh = op.apply_host(x)
+            assert np.array_equal(yh, yd), name
+print("ok")
+"""
+
+
+def test_apply_host_chunked_launches_bitwise():
+    """QTT_NO_COPY_FLAGS=1 selects qtt_apply_host's other pipeline: the first
+    and last stages run as 8 chunked launches each (split-K included, c3's and
+    a constant-rank last stage); bitwise equal to the device apply.  Run in a
+    subprocess because the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QTT_NO_COPY_FLAGS="1")
+    r = subprocess.run([sys.executable, "-c", _CHUNKED_HOST_SCRIPT, root], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("d,s,nrhs", [(28, 123457, 1), (26, 1, 3)])
 def test_shift_large_d_bitwise(qtt, d, s, nrhs):
     """Large N (2 GiB vectors at d = 28; 64-bit offsets, many tiles): the exact
