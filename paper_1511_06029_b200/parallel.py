@@ -7,7 +7,10 @@ levels 1..d-s on its own block (they never pair bits across blocks,
 PAPER.md P:1487-1496) and a projection of the result onto all P output
 blocks with the top s cores, all in the library's kernels.  The one exchange
 is a sum ReduceScatter of the [P][n] send buffers (NCCL over NVLink through
-torch.distributed; plumbing only).
+torch.distributed; plumbing only) -- or, with ``fused=True``, the projection
+kernel stores each block straight into its owner's receive buffer (CUDA IPC
+peer memory) and the owner sums the P slots in fixed order, ordered across
+processes by interprocess CUDA events.
 
 This module holds argument marshalling and the collective call; every flop
 runs in libqtt_b200.so.
@@ -200,6 +203,9 @@ class ShardedQttOperator:
         self.max_nrhs = int(max_nrhs)
         self._recv = None
         self._peers = []
+        self._ev_proj = self._ev_red = None
+        self._peer_proj, self._peer_red = [], []
+        self._hgroup = None
         if self.s == 0:
             self._op = QttOperator(arrs)
         else:
@@ -218,6 +224,24 @@ class ShardedQttOperator:
                     self._peers.append(p)
                     ptrs.append(p)
             self._shard.set_peers(ptrs)
+            # stream-ordered cross-process sync: interprocess CUDA events, one
+            # "projection stored" and one "reduction done" per part
+            import torch
+            self._ev_proj = torch.cuda.Event(interprocess=True)
+            self._ev_red = torch.cuda.Event(interprocess=True)
+            evh = [None] * self.world
+            dist.all_gather_object(evh, (self._ev_proj.ipc_handle(), self._ev_red.ipc_handle()), group=group)
+            dev = torch.cuda.current_device()
+            for r, (hp, hr) in enumerate(evh):
+                if r != self.rank:
+                    self._peer_proj.append(torch.cuda.Event.from_ipc_handle(dev, hp))
+                    self._peer_red.append(torch.cuda.Event.from_ipc_handle(dev, hr))
+            # host-only barriers (they order event records before the peers' waits)
+            if dist.get_backend(group) == "gloo":
+                self._hgroup = group
+            else:
+                ranks = list(range(dist.get_world_size())) if group is None else dist.get_process_group_ranks(group)
+                self._hgroup = dist.new_group(ranks=ranks, backend="gloo")
 
     def workspace_size(self, nrhs: int = 1) -> int:
         return (self._op or self._shard).workspace_size(nrhs)
@@ -238,26 +262,49 @@ class ShardedQttOperator:
         return y if x_local.dim() == 2 else y.view(-1)
 
     def _apply_fused(self, x_local, out, stream):
-        """Projection stores into every part's receive slot (peer memory), then --
-        once all parts are done (stream sync + process barrier) -- each part
-        sums its P slots.  A second barrier keeps the next apply's stores off
-        buffers a slower part is still reducing."""
+        """Projection stores into every part's receive slot (peer memory), then
+        each part sums its P slots in fixed order -- all stream-ordered, no
+        device synchronisation:
+
+          host barrier (every peer has recorded its previous "reduced" event)
+          wait on the peers' "reduced" events (their previous reduction has
+            read the slots this projection overwrites)
+          fused local stages + projection; record "projected"
+          host barrier (every peer has recorded "projected" for this apply)
+          wait on the peers' "projected" events; reduce; record "reduced"
+
+        The barriers are host-only (gloo): a stream wait captures an event's
+        latest record at call time, so each wait must follow the peer's record
+        call.  No kernel waits on another process's kernel."""
         import torch
         import torch.distributed as dist
         xl = x_local if x_local.dim() == 2 else x_local.view(1, -1)
         nrhs = xl.shape[0]
         if nrhs > self.max_nrhs:
             raise ValueError(f"nrhs {nrhs} > max_nrhs {self.max_nrhs} given at construction")
+        st = torch.cuda.current_stream(xl.device) if stream is None else stream
         y = torch.empty((nrhs, self.n), dtype=torch.float64, device=xl.device) if out is None else out
-        self._shard.apply_fused(xl, stream=stream)
-        torch.cuda.synchronize(xl.device)
-        dist.barrier(group=self.group)
-        QttShard.reduce(self._recv, y.view(nrhs, self.n), stream=stream, parts=self.world)
-        torch.cuda.synchronize(xl.device)
-        dist.barrier(group=self.group)
+        dist.barrier(group=self._hgroup)
+        for ev in self._peer_red:
+            st.wait_event(ev)
+        self._shard.apply_fused(xl, stream=st)
+        self._ev_proj.record(st)
+        dist.barrier(group=self._hgroup)
+        for ev in self._peer_proj:
+            st.wait_event(ev)
+        QttShard.reduce(self._recv, y.view(nrhs, self.n), stream=st, parts=self.world)
+        self._ev_red.record(st)
         return y if x_local.dim() == 2 else y.view(-1)
 
     def close(self):
+        if self._ev_red is not None:
+            # peers may still be storing into our buffer or reading theirs: drain
+            import torch
+            import torch.distributed as dist
+            torch.cuda.synchronize()
+            dist.barrier(group=self._hgroup)
+            self._ev_proj = self._ev_red = None
+            self._peer_proj, self._peer_red = [], []
         for o in (self._op, self._shard):
             if o is not None:
                 o.close()

@@ -104,13 +104,19 @@ def _fused_worker(rank, world, port, q):
     try:
         from paper_1511_06029_b200 import parallel as par
         _, cores, x = random_case(1700, 12, 20, 2)
+        x2 = np.ascontiguousarray(x[:, ::-1])
         op = par.ShardedQttOperator(cores, fused=True, max_nrhs=2)
-        xb = par.block_of(torch.from_numpy(np.ascontiguousarray(x)).cuda(), rank, world).contiguous()
+        refs = [par.block_of(oracle.apply_alg2(cores, v), rank, world) for v in (x, x2)]
+        xbs = [par.block_of(torch.from_numpy(np.ascontiguousarray(v)).cuda(), rank, world).contiguous()
+               for v in (x, x2)]
         errs = []
-        for _ in range(2):
-            y = op.apply(xb)
-            ref = par.block_of(oracle.apply_alg2(cores, x), rank, world)
+        # stream-ordered applies back to back (no host sync between them), alternating inputs
+        ys = [op.apply(xbs[i % 2]) for i in range(6)]
+        ys.append(op.apply(xbs[0][:1].contiguous()))          # nrhs 1 < max_nrhs
+        for i, y in enumerate(ys[:6]):
+            ref = refs[i % 2]
             errs.append(float(np.abs(y.cpu().numpy() - ref).max() / np.abs(ref).max()))
+        errs.append(float(np.abs(ys[6].cpu().numpy() - refs[0][:1]).max() / np.abs(refs[0][:1]).max()))
         op.close()
         q.put((rank, max(errs)))
     finally:
@@ -119,8 +125,9 @@ def _fused_worker(rank, world, port, q):
 
 def test_fused_exchange_two_processes_ipc(par):
     """Two processes on this one GPU: receive buffers shared through CUDA IPC,
-    host barriers (gloo) between the fused apply and the reduction -- no kernel
-    waits on another process's kernel."""
+    cross-process ordering by interprocess CUDA events (stream waits) behind
+    host-only gloo barriers -- no device synchronisation, and no kernel waits on
+    another process's kernel."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as s:
