@@ -100,7 +100,8 @@ qtt_status_t qtt_create_ex(qtt_handle_t* out, int d, const int64_t* ranks,
  *   k_first, k_last, variant : arrays of >= d ints (any may be NULL) receiving
  *                       per stage the 1-based level range and the variant
  *                       (0 generic, 1 DMMA one level, 2 DMMA merged stage,
- *                       3 merged stage with the super-core streamed from L2).
+ *                       3 merged stage with the super-core streamed from L2,
+ *                       4 small latency-bound stage, warp tiles from L2).
  */
 qtt_status_t qtt_plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
                              int* n_stages, int* k_first, int* k_last, int* variant);
@@ -307,7 +308,8 @@ qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank,
  * [*k_first, *k_last] (1-based) and runs kernel variant *variant (0 = generic,
  * 1 = fp64 tensor-core DMMA, one level; 2 = DMMA merged stage of several
  * levels with the super-core in shared memory; 3 = the same with the
- * super-core streamed from L2 in k-chunks, see qtt_plan_stages).
+ * super-core streamed from L2 in k-chunks; 4 = small latency-bound stage,
+ * one warp per 16 x 32 output block, see qtt_plan_stages).
  */
 qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int* variant);
 

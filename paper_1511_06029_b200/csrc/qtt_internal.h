@@ -22,7 +22,15 @@ namespace qtt {
 //              the level intermediates never exist.
 //   kWide    : a merged stage whose super-core is too large for shared memory:
 //              streamed from L2 in k-chunks next to the A tiles (qtt_wide_kernel.cu).
-enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2, kWide = 3 };
+//   kSmall   : latency-bound small stages: one warp per 16 x 32 output block,
+//              operands loaded straight from L2 (no smem staging, no barriers).
+enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2, kWide = 3, kSmall = 4 };
+// small variant: 16-row x 32-column warp tiles, k in steps of 8 (two k4 MMAs
+// per 16-byte A load), 4 warps per CTA
+constexpr int kSmallRows = 16;
+constexpr int kSmallCols = 32;
+constexpr int kSmallK = 8;
+constexpr int kSmallWarps = 4;
 
 // DMMA kernel instances: K = n_i * r_in <= 16*KB, n_i * roundup(r_out, 2) <= 8*NB.
 constexpr int kMaxKB = 8;
@@ -155,6 +163,9 @@ bool pdl_enabled();
 bool split_enabled();
 cudaError_t wide_prepare(int NB, size_t smem);
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st);
+// small variant (qtt_wide_kernel.cu): a.ncb = 32-column blocks, a.nchunks = k-steps of 8,
+// a.bpack = pack_small layout
+cudaError_t launch_small(const LevelArgs& a, cudaStream_t st);
 // y[s][c] = sum_g recv[g][s][c] (fixed order g = 0..parts-1), qtt_wide_kernel.cu
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,
                                 int num_sms);

@@ -48,6 +48,16 @@ constexpr double kChunkLatency = 0.4e-6;         // one more k-chunk of a wide t
 constexpr double kSmBw = 100e9;                  // bytes/s one SM's TMA pulls when few SMs are busy
 constexpr double kSms = 148;
 constexpr double kSplitLatency = 2.5e-6;        // split-K: partial store, arrival atomics, S-way sum
+constexpr double kSmallLatencyDefault = 2.0e-6; // small variant: operand round trips + epilogue of one warp tile
+// calibration knob (diagnostic): QTT_PLAN_SMALL_LAT=<seconds>
+double small_latency() {
+  static const double v = [] {
+    const char* e = std::getenv("QTT_PLAN_SMALL_LAT");
+    return e ? std::atof(e) : kSmallLatencyDefault;
+  }();
+  return v;
+}
+constexpr double kSmallStep = 0.05e-6;          // small variant: one k-step of 8 (16 dependent MMAs + loads)
 constexpr size_t kTwoCtaSmem = 113 * 1024;      // two resident-kernel CTAs per SM
 
 uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
@@ -197,6 +207,38 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
         sp->rep = 1;
         sp->stages = kWideStages;
         sp->smem = smem;
+        sp->est_seconds = t;
+        ok = true;
+      }
+    }
+  }
+  // Small variant: one warp per 16 x 32 output block straight from L2, for
+  // stages too small to fill the GPU with 64-row TMA tiles (latency-bound).
+  static const bool no_small = std::getenv("QTT_PLAN_NO_SMALL") != nullptr;   // diagnostic
+  if (!no_small && wbytes <= double(kWideMaxCoreBytes) && sp->K % 2 == 0) {
+    const int ncb = (nout + kSmallCols - 1) / kSmallCols;
+    const double wt = std::ceil(M / kSmallRows) * ncb;        // warp tiles
+    if (wt <= kSms * 64) {
+      const double nq = std::ceil(sp->K / double(kSmallK));
+      const double flops = 2.0 * wt * kSmallRows * kSmallCols * nq * kSmallK;
+      const double blocks = std::ceil(wt / kSmallWarps);
+      const double sm_used = std::min(1.0, blocks / kSms);
+      const double warps_per_sm = wt / std::min(blocks, kSms);
+      const double rate = kFp64 * sm_used * std::min(1.0, warps_per_sm / 12.0) * 0.8;
+      const double lat = small_latency() + nq * kSmallStep * std::max(1.0, warps_per_sm / 12.0);
+      static const bool force = std::getenv("QTT_PLAN_FORCE_SMALL") != nullptr;   // diagnostic
+      const double t = std::max({flops / rate, (bytes + wbytes) / kHbm, lat}) + kLaunch;
+      if (!ok || t < sp->est_seconds || force) {
+        sp->variant = kSmall;
+        sp->NB = 4;
+        sp->KB = 0;
+        sp->RP = r_out;
+        sp->ncb = ncb;
+        sp->nchunks = int(nq);
+        sp->ksplit = 1;
+        sp->rep = 1;
+        sp->stages = 0;
+        sp->smem = 0;
         sp->est_seconds = t;
         ok = true;
       }

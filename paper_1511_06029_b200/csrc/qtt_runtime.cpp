@@ -126,6 +126,17 @@ std::vector<double> pack_wide(const double* W, const qtt::StagePlan& sp) {
   });
 }
 
+// Small stage: the same Bmat as the wide stage, in pack_small order.
+std::vector<double> pack_small(const double* W, const qtt::StagePlan& sp) {
+  const int r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i, K = sp.K, nout = sp.n_i * sp.r_out;
+  return pack_small_fn(sp, [=](int kk, int n) {
+    if (kk >= K || n >= nout) return 0.0;
+    const int jj = kk / r_in, a = kk % r_in;
+    const int ii = n / r_out, b = n % r_out;
+    return W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b];
+  });
+}
+
 // Top-bit sharding: projection vectors of part g onto every
 // output block h, c_{h,g}[alpha] = [G_{d-s+1}(alpha, h_1, g_1, :) ... G_d(:, h_s, g_s, 0)],
 // written as Wp[h * r + alpha], r = ranks[d-s].
@@ -270,6 +281,16 @@ qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
     if (e != cudaSuccess) return from_cuda(e);
     return from_cuda(cudaMemcpy(S.d_core, cores[sp.k0 - 1], core_elems * sizeof(double), cudaMemcpyHostToDevice));
   }
+  if (sp.variant == qtt::kSmall) {
+    S.ctas_per_sm = 1;
+    const std::vector<double> W = sp.k0 == sp.k1
+                                      ? std::vector<double>(cores[sp.k0 - 1], cores[sp.k0 - 1] + size_t(sp.r_in) * 4 * sp.r_out)
+                                      : super_core(cores, h->ranks.data(), sp.k0, sp.k1);
+    const std::vector<double> pk = pack_small(W.data(), sp);
+    cudaError_t e = cudaMalloc(&S.d_bpack, pk.size() * sizeof(double));
+    if (e != cudaSuccess) return from_cuda(e);
+    return from_cuda(cudaMemcpy(S.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   if (sp.variant == qtt::kWide) {
     cudaError_t e = qtt::wide_prepare(sp.NB, h->smem_optin);
     if (e != cudaSuccess) return from_cuda(e);
@@ -355,6 +376,8 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
     }
     a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms)));
     e = qtt::launch_wide(a, st);
+  } else if (sp.variant == qtt::kSmall) {
+    e = qtt::launch_small(a, st);
   } else if (sp.variant != qtt::kGeneric) {
     const int64_t rows_per_stage = int64_t(qtt::kDmmaRowsPerSubtile) * sp.rep;
     const int64_t tiles = (a.M + rows_per_stage - 1) / rows_per_stage;

@@ -355,6 +355,56 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   }
 }
 
+// Small stages (latency-bound, L2-resident): one warp per 16 x 32 output block
+// (rows m0.., columns cb*32..), no smem, no barriers, no TMA.  Per k-step of 8
+// a lane loads one 16-byte A granule per row half (k = 8p + 2 t0 + {0, 1}: the
+// same k permutation as the resident kernel, so two k4 MMAs per load) and its
+// 4 n-blocks x 2 B values as two contiguous 32-byte pieces of the packed
+// operand (pack_small: [cb][p][lane][s][nb], s = the k4 step within the 8).
+__global__ void __launch_bounds__(kSmallWarps * 32) small_dmma_kernel(const LevelArgs p) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t wt = int64_t(blockIdx.x) * kSmallWarps + (threadIdx.x >> 5);
+  const int64_t mt = wt / p.ncb;
+  const int cb = int(wt - mt * p.ncb);
+  const int64_t m0 = mt * kSmallRows;
+  if (m0 >= p.M) return;
+  const int g = lane >> 2, t0 = lane & 3;
+  const int K = p.K;
+  const bool ok0 = m0 + g < p.M, ok1 = m0 + g + 8 < p.M;
+  const double* a0 = p.in + (m0 + g) * K + 2 * t0;
+  const double* a1 = a0 + int64_t(8) * K;
+  const double4* bp = reinterpret_cast<const double4*>(p.bpack) + (int64_t(cb) * p.nchunks * 32 + lane) * 2;
+  double c[4][4];
+#pragma unroll
+  for (int nb = 0; nb < 4; ++nb) c[nb][0] = c[nb][1] = c[nb][2] = c[nb][3] = 0.0;
+#pragma unroll 4
+  for (int q = 0; q < p.nchunks; ++q) {
+    const int k = q * kSmallK + 2 * t0;
+    double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+    if (k + 1 < K) {
+      if (ok0) x = __ldg(reinterpret_cast<const double2*>(a0 + q * kSmallK));
+      if (ok1) y = __ldg(reinterpret_cast<const double2*>(a1 + q * kSmallK));
+    } else if (k < K) {
+      if (ok0) x.x = __ldg(a0 + q * kSmallK);
+      if (ok1) y.x = __ldg(a1 + q * kSmallK);
+    }
+    const double4 b0 = bp[int64_t(q) * 64], b1 = bp[int64_t(q) * 64 + 1];
+    const double bs0[4] = {b0.x, b0.y, b0.z, b0.w}, bs1[4] = {b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      dmma_884(c[nb][0], c[nb][1], x.x, bs0[nb]);
+      dmma_884(c[nb][2], c[nb][3], y.x, bs0[nb]);
+    }
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      dmma_884(c[nb][0], c[nb][1], x.y, bs1[nb]);
+      dmma_884(c[nb][2], c[nb][3], y.y, bs1[nb]);
+    }
+  }
+  tile_store<4>(c, p, m0, cb * kSmallCols, lane);
+}
+
 using KernelFn = void (*)(const LevelArgs, const CUtensorMap);
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -450,6 +500,23 @@ cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, f, a, map);
+}
+
+cudaError_t launch_small(const LevelArgs& a, cudaStream_t st) {
+  const int64_t wtiles = (a.M + kSmallRows - 1) / kSmallRows * a.ncb;
+  const int64_t blocks = (wtiles + kSmallWarps - 1) / kSmallWarps;
+  if (blocks > 0x7fffffff || (a.K % 2)) return cudaErrorInvalidValue;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(blocks));
+  cfg.blockDim = dim3(kSmallWarps * 32);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, wide::small_dmma_kernel, a);
 }
 
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,

@@ -231,8 +231,41 @@ def test_wide_stages(qtt, ranks, nrhs):
     d = len(ranks) - 1
     _, cores, x = random_case(300 + d + nrhs, d, max(ranks), nrhs, ranks=ranks)
     y, st = gpu_apply(qtt, cores, x)
-    assert any(s["variant"] == "wide" for s in st), st
+    assert any(s["variant"] in ("wide", "small") for s in st), st
     oracle.assert_close(y, oracle.apply_alg2(cores, x))
+
+
+_NO_SMALL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1511_06029_b200 as q
+import oracle
+from qtt_workload import random_case
+sys.path.insert(0, sys.argv[1] + "/tests")
+from test_gpu_parity import WIDE_CASES
+for ranks, nrhs in WIDE_CASES:
+    d = len(ranks) - 1
+    _, cores, x = random_case(300 + d + nrhs, d, max(ranks), nrhs, ranks=ranks)
+    with q.QttOperator(cores) as op:
+        st = op.stages()
+        assert any(s["variant"] == "wide" for s in st) and not any(s["variant"] == "small" for s in st), st
+        y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
+print("ok")
+"""
+
+
+def test_wide_stages_without_small_variant():
+    """The same shapes with QTT_PLAN_NO_SMALL=1, so their boundary stages run on
+    the wide (TMA, streamed super-core) kernel.  Subprocess: read once."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QTT_PLAN_NO_SMALL="1")
+    r = subprocess.run([sys.executable, "-c", _NO_SMALL_SCRIPT, root], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_merged_closed_forms(qtt):
@@ -241,7 +274,7 @@ def test_merged_closed_forms(qtt):
     x = np.random.default_rng(4).standard_normal((3, 1 << d))
     for maxL in (2, 5, 6, 10):
         y, st = gpu_apply(qtt, CF.identity_cores(d), x, max_stage_levels=maxL)
-        assert any(s["variant"] in ("merged", "wide") for s in st)
+        assert any(s["k_last"] > s["k_first"] for s in st)       # multi-level stages
         np.testing.assert_array_equal(y, x)
         y, _ = gpu_apply(qtt, CF.shift_cores(d, 777), x, max_stage_levels=maxL)
         np.testing.assert_array_equal(y, np.roll(x, 777, axis=1))
@@ -461,6 +494,40 @@ def test_apply_host_chunked_launches_bitwise():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, QTT_NO_COPY_FLAGS="1")
     r = subprocess.run([sys.executable, "-c", _CHUNKED_HOST_SCRIPT, root], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+_FORCE_SMALL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1511_06029_b200 as q
+import oracle
+from qtt_workload import random_case
+cases = [(1, 1, 1, 1), (2, 2, 2, 5), (3, 3, 3, 7), (4, 6, 7, 3), (5, 9, 13, 2), (6, 10, 24, 1),
+         (7, 12, 33, 1), (8, 13, 48, 2), (9, 14, 5, 4), (13, 11, 64, 1), (14, 9, 100, 1)]
+n_small = 0
+for seed, d, r, nrhs in cases:
+    _, cores, x = random_case(seed + 900, d, r, nrhs)
+    with q.QttOperator(cores) as op:
+        n_small += sum(s["variant"] == "small" for s in op.stages())
+        y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
+assert n_small > 20, n_small
+print("ok", n_small)
+"""
+
+
+def test_small_variant_forced_everywhere():
+    """QTT_PLAN_FORCE_SMALL=1 plans the warp-tile small kernel for every stage
+    it can run (odd K, ragged rows and columns, multi-RHS); parity with the
+    oracle.  Subprocess: the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QTT_PLAN_FORCE_SMALL="1")
+    r = subprocess.run([sys.executable, "-c", _FORCE_SMALL_SCRIPT, root], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 

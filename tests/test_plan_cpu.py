@@ -25,7 +25,7 @@ def check_cover(plan, d, max_levels):
         assert a1 == b0 + 1
     for a, b, v in plan:
         assert 1 <= b - a + 1 <= max_levels
-        assert v in (0, 1, 2, 3)
+        assert v in (0, 1, 2, 3, 4)
         if v == 2:
             assert b > a                    # merged: a super-core of several levels
         if v in (0, 1):
@@ -39,7 +39,7 @@ def test_plan_covers_levels(q, name, maxL):
     plan = q.qtt_plan_stages(cfg.ranks, 0, maxL)
     check_cover(plan, cfg.d, maxL)
     if maxL == 1:
-        assert len(plan) == cfg.d and all(v in (1, 3) for _, _, v in plan)
+        assert len(plan) == cfg.d and all(v in (1, 3, 4) for _, _, v in plan)
         if cfg.N >= 1 << 21:
             assert all(v == 1 for _, _, v in plan)      # large N: smem-resident cores at r <= 48
 
@@ -64,18 +64,22 @@ def test_small_problem_few_launches(q):
 
 
 def test_large_rank_levels_use_wide_kernel(q):
-    # r = 70: 2 r = 140 > the smem-resident instances -> streamed super-core ("wide"), never generic
+    # r = 70: 2 r = 140 > the smem-resident instances -> streamed super-core
+    # ("wide"), or at tiny N the warp-tile "small" kernel; never generic
     ranks = [1, 2, 4] + [70] * 6 + [4, 2, 1]
     plan = q.qtt_plan_stages(ranks, 0, 1)
-    assert [v for _, _, v in plan][2:9] == [3] * 7
-    assert all(v in (1, 3) for _, _, v in plan)
+    assert all(v in (3, 4) for _, _, v in plan[2:9])
+    assert all(v in (1, 3, 4) for _, _, v in plan)
     check_cover(q.qtt_plan_stages(ranks), len(ranks) - 1, 10)
+    ranks = [1, 2, 4] + [70] * 11 + [4, 2, 1]                # N = 2^16: wide
+    plan = q.qtt_plan_stages(ranks, 0, 1)
+    assert [v for _, _, v in plan][2:13] == [3] * 11              # the r = 70 -> 70 levels
 
 
 def test_huge_rank_falls_back_to_generic(q):
     # r_in = r_out = 1501: the level's super-core (3002 x 3002 doubles) exceeds 64 MiB
     plan = q.qtt_plan_stages([1, 2, 1501, 1501, 2, 1], 0, 1)
-    assert [v for _, _, v in plan] == [1, 3, 0, 3, 1]
+    assert [v for _, _, v in plan][2] == 0 and [v for _, _, v in plan][1] in (3, 4)
 
 
 def test_split_k_only_for_few_tiles_and_long_k(q):
@@ -99,6 +103,14 @@ def test_split_k_only_for_few_tiles_and_long_k(q):
     # the split never changes which levels a stage covers
     check_cover([(s["k_first"], s["k_last"], 3 if s["variant"] == "wide" else 1 if s["variant"] == "dmma"
                   else 2 if s["variant"] == "merged" else 0) for s in plan], d, 10)
+
+
+def test_small_variant_only_for_small_stages(q):
+    """The warp-tile 'small' variant (no smem staging) is planned only where
+    64-row TMA tiles cannot fill the GPU: never at N >= 2^21 (c3-c5)."""
+    for name in ("c3", "c4", "c5"):
+        assert all(s["variant"] != "small" for s in q.plan_stages(configs.make_config(name).ranks)), name
+    assert q.plan_stages(configs.make_config("c1").ranks)[0]["variant"] == "small"
 
 
 def test_rank_one_and_d1(q):
