@@ -273,11 +273,14 @@ qtt_status_t qtt_shard_projection(int d, const int64_t* ranks, const double* con
  * holds peer mappings (cudaIpcOpenMemHandle) of the other GPUs' buffers.
  *   qtt_shard_set_peers  : recv[h] = part h's receive buffer as seen from this
  *                          device ([P][nrhs][n] doubles, 16-byte aligned), h = 0..P-1
- *                          (recv[part] is this part's own buffer).
+ *                          (recv[part] is this part's own buffer).  Synchronous; must
+ *                          not be called while a fused apply of this handle is in flight.
  *   qtt_shard_apply_fused: local stages + scatter projection; writes slot `part`
- *                          of every part's buffer.  The caller then makes sure all
- *                          P parts have finished (e.g. stream sync + a process barrier)
- *                          before reducing.
+ *                          of every part's buffer.  The caller orders the P parts:
+ *                          every part's fused apply complete before any part reduces,
+ *                          and every reduction of the previous apply complete before
+ *                          the next fused apply (parallel.py: interprocess CUDA events
+ *                          behind host barriers; or stream sync + a process barrier).
  *   qtt_shard_reduce     : y_local[i] = sum_{g=0..P-1} recv[g * count + i] in that fixed
  *                          order (count = nrhs * n, even; deterministic).
  */

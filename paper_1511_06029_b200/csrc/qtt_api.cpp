@@ -243,7 +243,11 @@ qtt_status_t qtt_shard_set_peers(qtt_handle_t h, double* const* recv, int parts)
       if (e == cudaSuccess) e = cudaMalloc(&h->proj_fused.d_bpack, pk.size() * sizeof(double));
       if (e == cudaSuccess)
         e = cudaMemcpy(h->proj_fused.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice);
-      if (e != cudaSuccess) return from_cuda(e);
+      if (e != cudaSuccess) {   // leave no half-built projection behind
+        if (h->proj_fused.d_bpack) cudaFree(h->proj_fused.d_bpack);
+        h->proj_fused.d_bpack = nullptr;
+        return from_cuda(e);
+      }
       h->proj_fused.ctas_per_sm = 1;
     }
     if (!h->d_peers) {
