@@ -498,6 +498,28 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
         gm, _ = time_applies(lambda: M.apply_grid(x, 3, out=y, stream=stream), 5, 2, stream)
         out["grid_apply_c4"] = {"ms_per_apply": gm, "gflops_alg2": M.flops_per_rhs / (gm * 1e-3) / 1e9}
         del x, y, ws
+    # boundary-integral preconditioner shape (Table 3's largest case, qtt_workload.bie_case):
+    # X = M Y, N = 2^21 = 4096 surfaces x 512 points, Y ranks <= 95, block-diagonal M ranks <= 50
+    from qtt_workload import bie_case
+    rmb, cMb, ryb, cYb, xb = bie_case(0, 21, 9, 95, 50, 1)
+    with q.QttOperator(cMb) as M, q.QttOperator(cYb) as Y, q.QttProduct([M, Y]) as PR:
+        x = torch.from_numpy(xb).to(dev)
+        y = torch.empty_like(x)
+        ws = torch.empty(PR.workspace_size(1) // 8 + 64, dtype=torch.float64, device=dev)
+        pm, _ = time_applies(lambda: PR.apply(x, out=y, workspace=ws, stream=stream), 10, 3, stream)
+        ym, _ = time_applies(lambda: Y.apply(x, out=y, stream=stream), 10, 3, stream)
+        F = M.flops_per_rhs + Y.flops_per_rhs
+        Fx = 0.0
+        for op_, rr_ in ((M, rmb), (Y, ryb)):
+            rows_, _, _ = stage_table(op_.stages(), rr_, 1 << 21, 1, [1.0] * op_.launches_per_apply, 1, P, BW)
+            Fx += sum(r_["flops_executed"] for r_ in rows_)
+        out["bie_product_2M"] = {
+            "ms_per_apply": pm, "ms_Y_alone": ym, "gflops_alg2": F / (pm * 1e-3) / 1e9,
+            "tflops_executed": Fx / (pm * 1e-3) / 1e12, "frac_executed_fp64": Fx / (pm * 1e-3) / P,
+            "stages_M": [[a["k_first"], a["k_last"], a["variant"], a["ksplit"]] for a in M.stages()],
+            "stages_Y": [[a["k_first"], a["k_last"], a["variant"], a["ksplit"]] for a in Y.stages()],
+            "note": "synthetic stand-in for Table 3 (N=1,966,080 padded to 2^21; paper's M/Y ranks 50/95)"}
+        del x, y, ws
     torch.cuda.empty_cache()
     return out
 

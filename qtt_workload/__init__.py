@@ -21,11 +21,11 @@ Conventions (SURVEY.md §8 readings R1, R2, R5-R8):
   memory image is exactly the column-major matrix.
 """
 from .configs import CONFIGS, Config, make_config, config_ranks, flops_per_apply
-from .gen import generate, random_cores, random_case, rank_profile_random, random_tt_vector
+from .gen import generate, random_cores, random_case, rank_profile_random, random_tt_vector, bie_case
 from . import closed_forms
 
 __all__ = [
     "CONFIGS", "Config", "make_config", "config_ranks", "flops_per_apply",
-    "generate", "random_cores", "random_case", "rank_profile_random", "random_tt_vector",
+    "generate", "random_cores", "random_case", "rank_profile_random", "random_tt_vector", "bie_case",
     "closed_forms",
 ]

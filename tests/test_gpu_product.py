@@ -71,3 +71,18 @@ def test_product_errors(qtt):
             qtt.QttProduct([a, b])          # different d
     with pytest.raises(ValueError):
         qtt.QttProduct([])
+
+
+@pytest.mark.parametrize("d,point_bits,nrhs", [(14, 9, 1), (16, 9, 2)])
+def test_bie_shaped_product(qtt, d, point_bits, nrhs):
+    """The boundary-integral preconditioner shape (qtt_workload.bie_case: Y with
+    ranks up to 95, block-diagonal M with ranks up to 50, Table 3): the product
+    against the oracle applying the factors in turn (the composed rank 4750
+    would be too large for the oracle's dense algebra)."""
+    from qtt_workload import bie_case
+    _, M, _, Y, x = bie_case(7, d, point_bits, 95, 50, nrhs)
+    ref = oracle.apply_alg2(M, oracle.apply_alg2(Y, x))
+    with qtt.QttOperator(M) as opM, qtt.QttOperator(Y) as opY, qtt.QttProduct([opM, opY]) as P:
+        y = P.apply(torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+    oracle.assert_close(y.cpu().numpy(), ref)
