@@ -272,6 +272,8 @@ def stage_table(stages, r, N, nrhs, stage_ms, n_timed, P, BW):
         # flops the kernel actually executes (unpadded): a merged stage of L levels
         # applies the 2^L r_in x 2^L r_out super-core, 2^(L+1) r_in r_out per element
         F_exec = (2 ** (k1 - k0 + 2)) * r[k0 - 1] * r[k1] * N * nrhs if k1 > k0 else F
+        if st["variant"] == "diag":        # block-diagonal digits: one batched GEMV, 2 r_in r_out per element
+            F_exec = 2 * r[k0 - 1] * r[k1] * N * nrhs
         t = stage_ms[s] / max(n_timed, 1) * 1e-3
         T = max(F / P, B / BW)
         sum_T += T

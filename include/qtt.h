@@ -312,7 +312,11 @@ qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank,
  * 1 = fp64 tensor-core DMMA, one level; 2 = DMMA merged stage of several
  * levels with the super-core in shared memory; 3 = the same with the
  * super-core streamed from L2 in k-chunks; 4 = small latency-bound stage,
- * one warp per 16 x 32 output block, see qtt_plan_stages).
+ * one warp per 16 x 32 output block; 5 = levels whose cores are all diagonal
+ * in (i_k, j_k), i.e. A block-diagonal in those digits, applied as one
+ * streaming batched GEMV whatever their number, see qtt_plan_stages).  The
+ * diagonal levels are detected at qtt_create from exact zeros; the host-only
+ * qtt_plan_stages knows ranks only and never plans variant 5.
  */
 qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int* variant);
 

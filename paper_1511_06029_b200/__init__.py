@@ -28,7 +28,7 @@ __all__ = [
     "morton_pack", "morton_unpack", "QttProduct",
 ]
 
-VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "merged", 3: "wide", 4: "small"}
+VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "merged", 3: "wide", 4: "small", 5: "diag"}
 MAX_STAGE_LEVELS = 10
 
 

@@ -95,7 +95,19 @@ static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, 
   ranks = h->ranks.data();
   qtt_status_t st = QTT_SUCCESS;
   try {
-    const std::vector<qtt::StagePlan> plan = qtt::plan_stages(dl, ranks, h->smem_optin, max_stage_levels);
+    // levels whose cores are diagonal in (i_k, j_k) (exact zeros off the diagonal):
+    // block-diagonal digits, planned as streaming diagonal stages
+    std::vector<unsigned char> diag(dl, 0);
+    for (int k = 0; k < dl; ++k) {
+      const double* G = cores[k];
+      bool dg = true;
+      for (size_t a = 0; a < size_t(ranks[k]) && dg; ++a)
+        for (int b = 0; b < ranks[k + 1] && dg; ++b)
+          dg = G[(a * 4 + 1) * ranks[k + 1] + b] == 0.0 && G[(a * 4 + 2) * ranks[k + 1] + b] == 0.0;
+      diag[k] = dg ? 1 : 0;
+    }
+    const std::vector<qtt::StagePlan> plan =
+        qtt::plan_stages(dl, ranks, h->smem_optin, max_stage_levels, diag.data());
     h->stages.resize(plan.size());
     for (size_t s = 0; s < plan.size(); ++s) {
       h->stages[s].plan = plan[s];

@@ -24,7 +24,15 @@ namespace qtt {
 //              streamed from L2 in k-chunks next to the A tiles (qtt_wide_kernel.cu).
 //   kSmall   : latency-bound small stages: one warp per 16 x 32 output block,
 //              operands loaded straight from L2 (no smem staging, no barriers).
-enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2, kWide = 3, kSmall = 4 };
+//   kDiag    : L consecutive levels whose cores are all diagonal in (i_k, j_k)
+//              (block-diagonal in those digits, e.g. the paper's surface-wise
+//              block-diagonal BIE factor M): the stage is a batched GEMV,
+//              out[(m, ii)][b] = sum_a in[(m, ii)][a] D[ii][a][b], 2 r_in r_out
+//              flops per element whatever L (qtt_level_dmma.cu diag_kernel).
+enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2, kWide = 3, kSmall = 4, kDiag = 5 };
+constexpr int kDiagMaxROut = 8;                       // r_out of a diagonal stage
+constexpr int kDiagMaxLevels = 24;
+constexpr size_t kDiagMaxCoreDoubles = size_t(1) << 23;   // D = r_in x 2^L x r_out
 // small variant: 16-row x 32-column warp tiles, k in steps of 8 (two k4 MMAs
 // per 16-byte A load), 4 warps per CTA
 constexpr int kSmallRows = 16;
@@ -129,7 +137,9 @@ struct StagePlan {
 size_t dmma_smem_bytes(int KB, int NB, int K, int rep, int stages);
 // Tiling of a DMMA stage; false if it does not fit smem_optin.
 bool dmma_tiling(int K, int KB, int NB, size_t smem_optin, int* rep, int* stages, size_t* smem);
-std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels);
+// diag[k-1] != 0: core k is diagonal in (i_k, j_k) (nullptr: none known)
+std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
+                                   const unsigned char* diag = nullptr);
 bool projection_plan(int r, int s, size_t smem_optin, StagePlan* sp);
 bool projection_plan_wide(int r, int s, size_t smem_optin, StagePlan* sp);   // fused exchange
 
@@ -137,6 +147,8 @@ cudaError_t dmma_prepare(int KB, int NB, size_t smem);   // sets the max dynamic
 cudaError_t dmma_occupancy(int KB, int NB, size_t smem, int* ctas_per_sm);
 cudaError_t launch_level_dmma(const LevelArgs& a, cudaStream_t st);
 cudaError_t launch_level_generic(const LevelArgs& a, cudaStream_t st, int num_sms);
+// diagonal stage: a.core = D [n_i][r_in][r_out], a.M = GEMM rows (nrhs N / n_i)
+cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms);
 size_t wide_smem_bytes(int NB);
 #ifndef QTT_WIDE_CG4_MIN_NB
 #define QTT_WIDE_CG4_MIN_NB 16

@@ -66,7 +66,63 @@ __global__ void level_generic_kernel(const LevelArgs p) {
   }
 }
 
+// Diagonal stage (kDiag): one warp per input row R = m n_i + ii of the [N][r_in]
+// buffer, lanes over the rank index a (coalesced row reads), the r_out <= 8
+// dot products with D[ii] reduced across the warp by a fixed xor butterfly
+// (lane b keeps output b: deterministic).  Output row m + Q (s (n_i - 1) + ii).
+__global__ void __launch_bounds__(256) diag_kernel(const LevelArgs p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int64_t nrows = p.M * p.n_i;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int r_in = p.r_in, r_out = p.r_out, n_i = p.n_i;
+  for (int64_t R = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; R < nrows; R += nw) {
+    const int64_t m = R / n_i;
+    const int ii = int(R - m * n_i);
+    const double* x = p.in + R * r_in;
+    const double* D = p.core + size_t(ii) * r_in * r_out;
+    double acc[kDiagMaxROut];
+#pragma unroll
+    for (int b = 0; b < kDiagMaxROut; ++b) acc[b] = 0.0;
+    for (int a = lane; a < r_in; a += 32) {
+      const double xa = __ldcs(x + a);
+#pragma unroll
+      for (int b = 0; b < kDiagMaxROut; ++b)
+        if (b < r_out) acc[b] = fma(xa, __ldg(D + size_t(a) * r_out + b), acc[b]);
+    }
+    double v = 0.0;
+#pragma unroll
+    for (int b = 0; b < kDiagMaxROut; ++b) {
+      if (b >= r_out) break;
+      double t = acc[b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == b) v = t;
+    }
+    const int64_t row = m + (((m >> p.log2_q) * (n_i - 1)) << p.log2_q) + (int64_t(ii) << p.log2_q);
+    if (lane < r_out) p.out[row * r_out + lane] = v;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms) {
+  const int64_t warps = a.M * a.n_i;
+  int64_t blocks = (warps + 7) / 8;
+  const int64_t cap = int64_t(num_sms) * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(blocks));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, diag_kernel, a);
+}
 
 cudaError_t dmma_prepare(int KB, int NB, size_t smem) {
   KernelFn f = lookup(KB, NB);

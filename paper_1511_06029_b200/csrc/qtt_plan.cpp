@@ -263,9 +263,34 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
 // the plan only the relative cost of flops, bytes and launches matters, and
 // the launch term is what keeps small-N problems (c1, c2) from being cut
 // into many launches, so N is the real N.
-std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels) {
+// A stage of diagonal levels k0..k1: out[(m, ii)][b] = sum_a in[(m, ii)][a] D[ii][a][b]
+// streams the input once (HBM-bound batched GEMV on CUDA cores).
+static bool diag_shape(const int64_t* ranks, int k0, int k1, int64_t n, StagePlan* sp) {
+  const int L = k1 - k0 + 1;
+  const int64_t r_in = ranks[k0 - 1], r_out = ranks[k1];
+  if (r_out > kDiagMaxROut || double(r_in) * std::ldexp(1.0, L) * double(r_out) > double(kDiagMaxCoreDoubles))
+    return false;
+  *sp = StagePlan{};
+  sp->k0 = k0;
+  sp->k1 = k1;
+  sp->variant = kDiag;
+  sp->r_in = int(r_in);
+  sp->r_out = int(r_out);
+  sp->n_i = 1 << L;
+  sp->K = sp->n_i * sp->r_in;
+  sp->RP = sp->r_out;
+  const double bytes = 8.0 * double(n) * double(r_in + r_out) + 8.0 * r_in * std::ldexp(1.0, L) * r_out;
+  const double flops = 2.0 * double(n) * double(r_in) * double(r_out);
+  sp->est_seconds = std::max(bytes / (kHbm * 0.7), flops / (kFp64 * 0.25)) + kLaunch;
+  return true;
+}
+
+std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
+                                   const unsigned char* diag) {
   const int64_t n = int64_t(1) << d;
   const int maxL = std::max(1, std::min(max_stage_levels, kMaxStageLevels));
+  // diagonal stages cost the same whatever L: allow long ones unless the caller capped L
+  const int maxLd = max_stage_levels >= kMaxStageLevels ? kDiagMaxLevels : maxL;
   std::vector<double> best(d + 1, std::numeric_limits<double>::infinity());
   std::vector<StagePlan> choice(d + 1);
   best[0] = 0;
@@ -273,6 +298,16 @@ std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_opti
     for (int L = 1; L <= std::min(maxL, k); ++L) {
       StagePlan sp;
       if (!stage_shape(ranks, k - L + 1, k, n, smem_optin, &sp)) continue;
+      const double c = best[k - L] + sp.est_seconds;
+      if (c < best[k]) {
+        best[k] = c;
+        choice[k] = sp;
+      }
+    }
+    if (!diag) continue;
+    for (int L = 1; L <= std::min(maxLd, k) && diag[k - L]; ++L) {
+      StagePlan sp;
+      if (!diag_shape(ranks, k - L + 1, k, n, &sp)) continue;
       const double c = best[k - L] + sp.est_seconds;
       if (c < best[k]) {
         best[k] = c;

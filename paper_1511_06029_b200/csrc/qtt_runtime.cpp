@@ -281,6 +281,42 @@ qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
     if (e != cudaSuccess) return from_cuda(e);
     return from_cuda(cudaMemcpy(S.d_core, cores[sp.k0 - 1], core_elems * sizeof(double), cudaMemcpyHostToDevice));
   }
+  if (sp.variant == qtt::kDiag) {
+    // D[ii][a][b] = (G_k0(:, i_1, i_1, :) ... G_k1(:, i_L, i_L, :))[a][b], ii = sum_l i_l 2^(l-1)
+    const int r_in = sp.r_in;
+    int rc = int(h->ranks[sp.k0]);
+    int n = 2;
+    std::vector<double> D(size_t(2) * r_in * rc);     // [ii][a][c]
+    {
+      const double* G = cores[sp.k0 - 1];
+      for (int i = 0; i < 2; ++i)
+        for (int a = 0; a < r_in; ++a)
+          for (int c = 0; c < rc; ++c) D[(size_t(i) * r_in + a) * rc + c] = G[((size_t(a) * 2 + i) * 2 + i) * rc + c];
+    }
+    for (int k = sp.k0 + 1; k <= sp.k1; ++k) {
+      const double* G = cores[k - 1];
+      const int rb = int(h->ranks[k]);
+      std::vector<double> V(size_t(2 * n) * r_in * rb, 0.0);
+      for (int i = 0; i < 2; ++i)
+        for (int ii = 0; ii < n; ++ii)
+          for (int a = 0; a < r_in; ++a) {
+            double* v = &V[(size_t(ii + n * i) * r_in + a) * rb];
+            const double* u = &D[(size_t(ii) * r_in + a) * rc];
+            for (int c = 0; c < rc; ++c) {
+              const double uc = u[c];
+              if (uc == 0.0) continue;
+              const double* g = G + ((size_t(c) * 2 + i) * 2 + i) * rb;
+              for (int b = 0; b < rb; ++b) v[b] += uc * g[b];
+            }
+          }
+      D.swap(V);
+      n *= 2;
+      rc = rb;
+    }
+    cudaError_t e = cudaMalloc(&S.d_core, D.size() * sizeof(double));
+    if (e != cudaSuccess) return from_cuda(e);
+    return from_cuda(cudaMemcpy(S.d_core, D.data(), D.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   if (sp.variant == qtt::kSmall) {
     S.ctas_per_sm = 1;
     const std::vector<double> W = sp.k0 == sp.k1
@@ -378,6 +414,8 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
     e = qtt::launch_wide(a, st);
   } else if (sp.variant == qtt::kSmall) {
     e = qtt::launch_small(a, st);
+  } else if (sp.variant == qtt::kDiag) {
+    e = qtt::launch_diag(a, st, h->num_sms);
   } else if (sp.variant != qtt::kGeneric) {
     const int64_t rows_per_stage = int64_t(qtt::kDmmaRowsPerSubtile) * sp.rep;
     const int64_t tiles = (a.M + rows_per_stage - 1) / rows_per_stage;

@@ -188,6 +188,41 @@ def test_split_k_matches_unsplit_host_path(qtt):
     oracle.assert_close(yd, yh)
 
 
+# ------------------------------------------------------------------ diagonal (block-diagonal) levels
+DIAG_CASES = [
+    # d, max rank, nrhs, 0-based cores made diagonal in (i, j)
+    (12, 6, 1, list(range(5, 12))),          # block-diagonal in the top 7 digits, r_d = 1
+    (13, 8, 2, [4, 5, 6, 7]),                # a diagonal run in the middle (r_out <= 8 there)
+    (11, 5, 3, [0, 1, 2]),                   # the bottom digits
+    (10, 4, 1, list(range(10))),             # every level: one diagonal stage
+]
+
+
+@pytest.mark.parametrize("d,r,nrhs,dlevels", DIAG_CASES)
+def test_diagonal_levels(qtt, d, r, nrhs, dlevels):
+    """Cores with exact zeros off the (i, j) diagonal are applied as one
+    streaming stage (variant 'diag'); parity with the oracle, which knows
+    nothing of the structure."""
+    ranks, cores, x = random_case(3100 + d, d, r, nrhs)
+    eye = np.eye(2).reshape(1, 2, 2, 1)
+    for k in dlevels:
+        cores[k] = np.ascontiguousarray(cores[k] * eye)
+    y, st = gpu_apply(qtt, cores, x)
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
+    if len(dlevels) >= 4:
+        assert any(s["variant"] == "diag" for s in st), st
+
+
+def test_diagonal_levels_planned(qtt):
+    """The block-diagonal top digits become one diag stage (BIE factor M's shape)."""
+    from qtt_workload import bie_case
+    _, M, _, _, x = bie_case(2, 15, 6, 12, 8, 1)
+    y, st = gpu_apply(qtt, M, x)
+    diag = [s for s in st if s["variant"] == "diag"]
+    assert diag and diag[-1]["k_last"] == 15 and diag[-1]["k_first"] <= 8, st
+    oracle.assert_close(y, oracle.apply_alg2(M, x))
+
+
 # ------------------------------------------------------------------ merged stages (super-cores)
 @pytest.mark.parametrize("maxL", [1, 2, 3, 4, 6, 10])
 @pytest.mark.parametrize("seed,d,maxr,nrhs", [(21, 10, 6, 3), (22, 13, 12, 2), (23, 15, 24, 1), (24, 9, 3, 7),
