@@ -79,19 +79,30 @@ __global__ void level_generic_kernel(const LevelArgs p) {
 // into registers 0.51.
 constexpr int kDiagMaxRin = 64;
 
-template <bool VEC>
+// LANE_II (few GEMM rows, M < 32, e.g. a diagonal matrix: one stage of all d
+// levels, M = nrhs): lanes take 32 consecutive ii of one m instead.
+template <bool VEC, bool LANE_II>
 __global__ void __launch_bounds__(256) diag_kernel(const LevelArgs p) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int r_in = p.r_in, r_out = p.r_out, n_i = p.n_i;
-  const int64_t mblocks = (p.M + 31) / 32;
-  const int64_t items = mblocks * n_i;
+  const int64_t mblocks = LANE_II ? p.M : (p.M + 31) / 32;
+  const int64_t items = LANE_II ? mblocks * ((n_i + 31) / 32) : mblocks * n_i;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < items; w += nw) {
-    const int64_t mb = w / n_i;
-    const int ii = int(w - mb * n_i);
-    const int64_t m = mb * 32 + lane;
-    if (m >= p.M) continue;
+    int64_t m;
+    int ii;
+    if (LANE_II) {
+      const int iblocks = (n_i + 31) / 32;
+      m = w / iblocks;
+      ii = int(w - m * iblocks) * 32 + lane;
+      if (ii >= n_i) continue;
+    } else {
+      const int64_t mb = w / n_i;
+      ii = int(w - mb * n_i);
+      m = mb * 32 + lane;
+      if (m >= p.M) continue;
+    }
     const double* x = p.in + (m * n_i + ii) * r_in;
     const double* D = p.core + size_t(ii) * r_in * r_out;
     double acc[kDiagMaxROut];
@@ -128,7 +139,8 @@ __global__ void __launch_bounds__(256) diag_kernel(const LevelArgs p) {
 
 cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms) {
   if (a.r_in > kDiagMaxRin || a.r_out > kDiagMaxROut) return cudaErrorInvalidValue;
-  const int64_t warps = (a.M + 31) / 32 * a.n_i;
+  const bool lane_ii = a.M < 32;
+  const int64_t warps = lane_ii ? a.M * ((a.n_i + 31) / 32) : (a.M + 31) / 32 * a.n_i;
   int64_t blocks = (warps + 7) / 8;
   const int64_t cap = int64_t(num_sms) * 16;
   if (blocks > cap) blocks = cap;
@@ -143,8 +155,12 @@ cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   // 16-byte row loads need even r_in (every row then starts 16-byte aligned)
-  if (a.r_in % 2 == 0) return cudaLaunchKernelEx(&cfg, diag_kernel<true>, a);
-  return cudaLaunchKernelEx(&cfg, diag_kernel<false>, a);
+  if (lane_ii) {
+    if (a.r_in % 2 == 0) return cudaLaunchKernelEx(&cfg, diag_kernel<true, true>, a);
+    return cudaLaunchKernelEx(&cfg, diag_kernel<false, true>, a);
+  }
+  if (a.r_in % 2 == 0) return cudaLaunchKernelEx(&cfg, diag_kernel<true, false>, a);
+  return cudaLaunchKernelEx(&cfg, diag_kernel<false, false>, a);
 }
 
 cudaError_t dmma_prepare(int KB, int NB, size_t smem) {

@@ -195,6 +195,8 @@ DIAG_CASES = [
     (13, 8, 2, [4, 5, 6, 7]),                # a diagonal run in the middle (r_out <= 8 there)
     (11, 5, 3, [0, 1, 2]),                   # the bottom digits
     (10, 4, 1, list(range(10))),             # every level: one diagonal stage
+    (16, 3, 2, list(range(16))),             # a diagonal matrix: M = nrhs GEMM rows (lanes over ii)
+    (15, 8, 1, list(range(3, 15))),          # 12 diagonal levels: M = 8 rows
 ]
 
 
