@@ -4,6 +4,8 @@
 // runs entirely in the kernels; nothing here touches vector data.
 #include "qtt_runtime.h"
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX: host ranges per stage for nsys / ncu --nvtx
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -463,8 +465,13 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
       fh.peers = h->d_peers;
       fh.peer_offset = int64_t(h->shard_part) * M;
     }
+    char name[64];
+    std::snprintf(name, sizeof(name), "qtt stage %d-%d v%d", proj ? h->d + 1 : S.plan.k0,
+                  proj ? h->d + h->shard_bits : S.plan.k1, S.plan.variant);
+    nvtxRangePushA(name);
     const cudaError_t e = launch_stage(h, S, proj, in, out, M, 0, counters + si, st, (proj && fused) ? &fh : nullptr,
                                        scb ? &split : nullptr);
+    nvtxRangePop();
     if (e != cudaSuccess) return from_cuda(e);
     if (h->timing && !proj) {
       cudaEventRecord(ev.stop, st);
@@ -490,7 +497,9 @@ qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nr
   }
   for (auto& g : h->graphs)
     if (g.x == x && g.y == y && g.ws == ws && g.nrhs == nrhs) {
+      nvtxRangePushA("qtt apply (graph replay)");
       cudaError_t e = cudaGraphLaunch(g.exec, st);
+      nvtxRangePop();
       if (e == cudaSuccess) e = cudaEventRecord(h->last, st);
       return from_cuda(e);
     }

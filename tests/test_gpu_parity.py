@@ -438,6 +438,43 @@ def test_abi_errors(qtt):
     assert lib.qtt_destroy(None) == E.QTT_SUCCESS
 
 
+def test_apply_does_not_block_the_host(qtt):
+    """qtt_apply only enqueues.  c4 takes ~55 ms on the device; the
+    host call (graph replay after the first apply) returns in a small fraction."""
+    import time
+    cfg, cores, x = generate("c4")
+    with qtt.QttOperator(cores) as op:
+        xt = torch.from_numpy(x).cuda()
+        y = torch.empty_like(xt)
+        op.apply(xt, out=y)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        t0 = time.perf_counter()
+        op.apply(xt, out=y)
+        host_ms = (time.perf_counter() - t0) * 1e3
+        b.record()
+        b.synchronize()
+        dev_ms = a.elapsed_time(b)
+    assert dev_ms > 20.0 and host_ms < 0.1 * dev_ms, (host_ms, dev_ms)
+
+
+def test_core_arrays_may_be_freed_after_create(qtt):
+    """SURVEY T3 / qtt.h: qtt_create copies the cores; overwriting the caller's
+    arrays afterwards does not change the operator."""
+    _, cores, x = random_case(4321, 12, 9, 2)
+    keep = [c.copy() for c in cores]
+    op = qtt.QttOperator(cores)
+    try:
+        for c in cores:
+            c.fill(np.nan)
+        del cores
+        y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    finally:
+        op.close()
+    oracle.assert_close(y, oracle.apply_alg2(keep, x))
+
+
 def test_nan_inf_propagate(qtt):
     d = 8
     _, cores, x = random_case(9, d, 6)
