@@ -243,6 +243,13 @@ class QttOperator:
         self.launches_per_apply = info["launches_per_apply"]
         self.ranks = [int(np.shape(cores[0])[0])] + [int(np.shape(G)[3]) for G in cores]
 
+    @classmethod
+    def from_ttb1(cls, path, max_stage_levels: int | None = None) -> "QttOperator":
+        """Operator from a TTB1 core file (``ttb1.load_operator``)."""
+        from . import ttb1
+        ranks, cores = ttb1.load_operator(path)
+        return cls(cores, ranks, max_stage_levels)
+
     @property
     def handle(self) -> int:
         if self._h is None:

@@ -475,6 +475,17 @@ def test_core_arrays_may_be_freed_after_create(qtt):
     oracle.assert_close(y, oracle.apply_alg2(keep, x))
 
 
+def test_operator_from_ttb1_file(qtt, tmp_path):
+    """An operator loaded from a TTB1 core file applies bitwise like the same
+    cores passed directly."""
+    from paper_1511_06029_b200 import ttb1
+    _, cores, x = generate("c2")
+    ttb1.save(tmp_path / "c2.ttb1", cores)
+    xt = torch.from_numpy(x).cuda()
+    with qtt.QttOperator.from_ttb1(tmp_path / "c2.ttb1") as a, qtt.QttOperator(cores) as b:
+        assert torch.equal(a.apply(xt), b.apply(xt))
+
+
 def test_nan_inf_propagate(qtt):
     d = 8
     _, cores, x = random_case(9, d, 6)
