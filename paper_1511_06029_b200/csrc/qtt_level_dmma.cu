@@ -78,6 +78,10 @@ __global__ void level_generic_kernel(const LevelArgs p) {
 // staged in smem (lanes then over different ii) 0.77, all row loads hoisted
 // into registers 0.51.
 constexpr int kDiagMaxRin = 64;
+#ifndef QTT_DIAG_UNROLL
+#define QTT_DIAG_UNROLL 4
+#endif
+constexpr int kDiagUnroll = QTT_DIAG_UNROLL;   // 16-byte row loads in flight per lane
 
 // LANE_II (few GEMM rows, M < 32, e.g. a diagonal matrix: one stage of all d
 // levels, M = nrhs): lanes take 32 consecutive ii of one m instead.
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(256) diag_kernel(const LevelArgs p) {
 #pragma unroll
     for (int b = 0; b < kDiagMaxROut; ++b) acc[b] = 0.0;
     if (VEC) {
-#pragma unroll 4
+#pragma unroll (kDiagUnroll)
       for (int a = 0; a < r_in; a += 2) {
         const double2 xa = __ldcs(reinterpret_cast<const double2*>(x + a));
 #pragma unroll
