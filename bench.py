@@ -611,7 +611,7 @@ def run_sharded(args, world, rank, local, dev, cfg, cores, x_np):
                           + ("fused peer-store exchange" if args.exchange == "fused" else "NCCL reduce-scatter")),
            "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                    "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8)},
-           "gpu_launches": (len(op._shard.stages())) * args.steps,
+           "gpu_launches": sum(1 + (st_.get("ksplit", 1) > 1) for st_ in op._shard.stages()) * args.steps,
            "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(out))
@@ -793,7 +793,8 @@ def main(argv=None):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(x_np.nbytes), "d2h_bytes_per_step": int(x_np.nbytes)},
-        "gpu_launches": op.launches_per_apply * args.steps,
+        # one kernel per stage, plus the reduce launch of every split-K stage
+        "gpu_launches": sum(1 + (st_["ksplit"] > 1) for st_ in op.stages()) * args.steps,
         "clocks": clocks,
         "other_configs_and_next_rows": extra,
     }

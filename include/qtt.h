@@ -326,7 +326,7 @@ qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int
  * tiles alone would leave SMs idle (few GEMM rows, long K: the last stage of
  * a constant-rank profile, whose super-core has K = 2^L r) computes each
  * output tile as S partial sums over disjoint k-ranges, added in fixed order
- * k-range 0..S-1 by the last CTA to finish (bitwise reproducible).  The split
+ * k-range 0..S-1 by a second launch (bitwise reproducible).  The split
  * scratch is part of qtt_workspace_size.  Host-only query; no GPU work.
  */
 qtt_status_t qtt_get_stage_split(qtt_handle_t h, int s, int64_t nrhs, int* ksplit);

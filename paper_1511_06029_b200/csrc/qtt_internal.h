@@ -113,12 +113,10 @@ struct LevelArgs {
   double* const* peers = nullptr;
   int64_t peer_offset = 0;         // added to every peers[ii] (this part's slot: part * M)
   // wide variant, split-K (ksplit > 1): tile t = output tile t / ksplit, k-chunks
-  // [(t % ksplit) * kcps, ...); partial sums in `partial`, arrival counters in
-  // split_cnt (zero before the launch, left zero after it)
+  // [(t % ksplit) * kcps, ...); partial sums in `partial`, reduced by the next launch
   int ksplit = 1;
   int kcps = 0;                    // k-chunks per split
   double* partial = nullptr;       // [output tiles][ksplit][consumer warps][split_slot_doubles(NB)]
-  int* split_cnt = nullptr;        // [output tiles][consumer warps]
 };
 
 // Host-side stage plan (qtt_plan.cpp): pure function of the rank profile and

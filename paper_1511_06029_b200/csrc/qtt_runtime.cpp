@@ -198,48 +198,29 @@ int stage_ksplit(const qtt_plan*, const Stage& S, int64_t) {
   return sp.variant == qtt::kWide && sp.ksplit > 1 ? sp.ksplit : 1;
 }
 
-// split-K scratch of one stage: [arrival counters][partials], both 256-aligned
-static void split_bytes(const qtt_plan* h, const Stage& S, int64_t M, size_t* cnt, size_t* part) {
-  *cnt = *part = 0;
+// split-K scratch of one stage: the partial sums, [tiles][S][consumer warps][slot]
+static size_t split_bytes(const qtt_plan* h, const Stage& S, int64_t M) {
   const int ks = stage_ksplit(h, S, M);
-  if (ks <= 1) return;
+  if (ks <= 1) return 0;
   const int64_t tiles = (M + qtt::kDmmaRowsPerSubtile - 1) / qtt::kDmmaRowsPerSubtile * S.plan.ncb;
   const int cw = qtt::wide_consumer_warps(S.plan.NB);
-  *cnt = (size_t(tiles) * cw * sizeof(int) + 255) / 256 * 256;
-  *part = size_t(tiles) * ks * cw * qtt::split_slot_doubles(S.plan.NB) * sizeof(double);
-}
-
-size_t ws_split_cnt_bytes(const qtt_plan* h, int64_t nrhs) {
-  size_t m = 0;
-  for (const auto& S : h->stages) {
-    size_t c, p;
-    split_bytes(h, S, nrhs * (int64_t(1) << (h->d - (S.plan.k1 - S.plan.k0 + 1))), &c, &p);
-    m = std::max(m, c);
-  }
-  return m;
+  return size_t(tiles) * ks * cw * qtt::split_slot_doubles(S.plan.NB) * sizeof(double);
 }
 
 static size_t ws_split_bytes(const qtt_plan* h, int64_t nrhs) {
-  size_t mc = 0, mp = 0;
-  for (const auto& S : h->stages) {
-    size_t c, p;
-    split_bytes(h, S, nrhs * (int64_t(1) << (h->d - (S.plan.k1 - S.plan.k0 + 1))), &c, &p);
-    mc = std::max(mc, c);
-    mp = std::max(mp, p);
-  }
-  return mc + mp;
+  size_t m = 0;
+  for (const auto& S : h->stages)
+    m = std::max(m, split_bytes(h, S, nrhs * (int64_t(1) << (h->d - (S.plan.k1 - S.plan.k0 + 1)))));
+  return m;
 }
 
-// Split-K scratch after the two buffers; its counters are zeroed here (each
-// split launch leaves them zero for the next).
-cudaError_t setup_split(const qtt_plan* h, void* ws, int64_t nrhs, cudaStream_t st, SplitScratch* out) {
+// Split-K scratch after the two buffers (every slot is written by the split
+// launch before its reduce launch reads it: no initialisation needed).
+cudaError_t setup_split(const qtt_plan* h, void* ws, int64_t nrhs, cudaStream_t, SplitScratch* out) {
   *out = SplitScratch{};
-  const size_t scb = ws_split_cnt_bytes(h, nrhs);
-  if (!scb) return cudaSuccess;
-  unsigned char* base = static_cast<unsigned char*>(ws) + kWsHeader + 2 * ws_buf_bytes(h, nrhs);
-  out->cnt = reinterpret_cast<int*>(base);
-  out->partial = reinterpret_cast<double*>(base + scb);
-  return cudaMemsetAsync(out->cnt, 0, scb, st);
+  if (!ws_split_bytes(h, nrhs)) return cudaSuccess;
+  out->partial = reinterpret_cast<double*>(static_cast<unsigned char*>(ws) + kWsHeader + 2 * ws_buf_bytes(h, nrhs));
+  return cudaSuccess;
 }
 
 size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs) {
@@ -408,7 +389,6 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
     if (ks > 1) {
       a.ksplit = ks;
       a.kcps = (sp.nchunks + ks - 1) / ks;
-      a.split_cnt = split->cnt;
       a.partial = split->partial;
       tiles *= ks;
     }
@@ -443,7 +423,7 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
   SplitScratch split;
   me = setup_split(h, ws, nrhs, st, &split);
   if (me != cudaSuccess) return from_cuda(me);
-  const bool scb = split.cnt != nullptr;
+  const bool scb = split.partial != nullptr;
   const double* in = x;
   const int nloc = int(h->stages.size());
   const int ns = nloc + (h->shard_bits ? 1 : 0);

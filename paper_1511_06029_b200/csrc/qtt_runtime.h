@@ -196,11 +196,9 @@ void free_plan(qtt_plan* h);
 qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores);
 // split-K scratch inside the workspace (enqueue); nullptr = no split
 struct SplitScratch {
-  int* cnt = nullptr;
   double* partial = nullptr;
 };
 int stage_ksplit(const qtt_plan* h, const Stage& S, int64_t M);
-size_t ws_split_cnt_bytes(const qtt_plan* h, int64_t nrhs);
 cudaError_t setup_split(const qtt_plan* h, void* ws, int64_t nrhs, cudaStream_t st, SplitScratch* out);
 cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* in, double* out, int64_t M,
                          int64_t m_base, int* counter, cudaStream_t st, const WideHooks* hooks = nullptr,

@@ -136,12 +136,6 @@ __device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const Leve
   }
 }
 
-__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
-  double v;
-  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -166,55 +160,24 @@ __device__ __forceinline__ void scatter_store(const double (&c)[NBC][4], const L
   }
 }
 
-// Split-K epilogue (MODE & 4).  Tile t = tile_out * S + ks covers k-chunks
-// [ks * kcps, min(nchunks, (ks + 1) * kcps)).  Each consumer warp stores its
-// 16 x 8*NBC partial to slot (tile_out, ks, warp) of p.partial (lane-minor, 256
-// bytes per store instruction), fences, and counts in on
-// split_cnt[tile_out * CW + warp].  The S-th arrival sums the S partials in
-// the fixed order ks = 0..S-1 (bitwise reproducible whatever the arrival
-// order), resets the counter for the next stage and stores the tile with the
-// ordinary row-separation epilogue.
+// Split-K (MODE & 4).  Tile t = tile_out * S + ks covers k-chunks
+// [ks * kcps, min(nchunks, (ks + 1) * kcps)); each consumer warp stores its
+// 16 x 8*NBC partial to slot (tile_out, ks, warp) of p.partial (lane-minor,
+// 256 bytes per store instruction).  split_reduce_kernel, the next launch on
+// the stream, sums the S slots in the fixed order ks = 0..S-1 (bitwise
+// reproducible) and runs the ordinary row-separation epilogue.  (An in-kernel
+// "last arrival reduces" protocol with per-tile counters read stale partials
+// in ~1 of 150 applies of a K = 24320 stage even with gpu-scope fences on
+// every lane and strong loads/stores; the kernel boundary is the one
+// synchronisation that held.)
 template <int NBC>
-__device__ __forceinline__ bool split_reduce(double (&c)[NBC][4], const LevelArgs& p, int64_t tile_out, int ks,
-                                             int warp, int cw, int slot, int lane) {
-  const int S = p.ksplit;
-  double* mine = p.partial + ((tile_out * S + ks) * cw + warp) * int64_t(slot);
+__device__ __forceinline__ void split_store(const double (&c)[NBC][4], const LevelArgs& p, int64_t tile_out, int ks,
+                                            int warp, int cw, int slot, int lane) {
+  double* mine = p.partial + ((tile_out * p.ksplit + ks) * cw + warp) * int64_t(slot);
 #pragma unroll
   for (int nb = 0; nb < NBC; ++nb)
 #pragma unroll
     for (int v = 0; v < 4; ++v) __stcg(mine + (nb * 4 + v) * 32 + lane, c[nb][v]);
-  // release: every lane's partial is ordered before lane 0's arrival (warp
-  // barrier, then lane 0's gpu-scope fence, cumulative over what it observed)
-  __syncwarp();
-  int old = 0;
-  int* cnt = p.split_cnt + tile_out * cw + warp;
-  if (lane == 0) {
-    __threadfence();
-    old = atomicAdd(cnt, 1);
-  }
-  old = __shfl_sync(0xffffffffu, old, 0);
-  if (old != S - 1) return false;
-  // acquire: lane 0 observed all S arrivals; its fence and the warp barrier
-  // order every lane's loads after them.  Strong (relaxed.gpu) loads: a weak
-  // load need not see another SM's store without this chain (observed:
-  // stale partials on some lanes once kernels overlapped under PDL).
-  if (lane == 0) {
-    __threadfence();
-    *cnt = 0;   // left zero for the next split launch
-  }
-  __syncwarp();
-#pragma unroll
-  for (int nb = 0; nb < NBC; ++nb)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) c[nb][v] = 0.0;
-  for (int k = 0; k < S; ++k) {
-    const double* src = p.partial + ((tile_out * S + k) * cw + warp) * int64_t(slot);
-#pragma unroll
-    for (int nb = 0; nb < NBC; ++nb)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) c[nb][v] += ld_relaxed_f64(src + (nb * 4 + v) * 32 + lane);
-  }
-  return true;
 }
 
 template <int NB, int NBC, int MODE>
@@ -246,9 +209,10 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
     if (++chunk == tile_nch) {
       chunk = 0;
       int64_t to = t;
-      if (MODE & 4) {
+      if (MODE & 4) {   // partial only; split_reduce_kernel stores the tile
         to = t / p.ksplit;
-        if (!split_reduce<NBC>(c, p, to, int(t - to * p.ksplit), warp, cw, slot, lane)) continue;
+        split_store<NBC>(c, p, to, int(t - to * p.ksplit), warp, cw, slot, lane);
+        continue;
       }
       const int64_t rt = to / p.ncb;
       const int cb = int(to - rt * p.ncb);
@@ -352,6 +316,59 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   } else {
     if constexpr (NB_2 > 0)
       consumer<NB, NB_2, MODE>(p, full, empty, tile_id, ring, rg, NBW + NB_1, lane, warp, CW, SLOT);
+  }
+}
+
+// Split-K reduction: one warp per (output tile, consumer-warp slot) of the
+// split stage; sums the S partials in fixed order and stores like the stage's
+// own epilogue (with the host-copy "done" publication when hooks are set).
+template <int NB, int NBC>
+__device__ __forceinline__ void split_reduce_one(const LevelArgs& p, int64_t to, int w, int rg, int nb0, int lane) {
+  constexpr int CW = kDmmaRowGroups * wide_col_groups(NB);
+  constexpr int SLOT = split_slot_doubles(NB);
+  double c[NBC][4];
+#pragma unroll
+  for (int nb = 0; nb < NBC; ++nb) c[nb][0] = c[nb][1] = c[nb][2] = c[nb][3] = 0.0;
+  for (int ks = 0; ks < p.ksplit; ++ks) {
+    const double* src = p.partial + ((to * p.ksplit + ks) * CW + w) * int64_t(SLOT);
+#pragma unroll
+    for (int nb = 0; nb < NBC; ++nb)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) c[nb][v] += __ldcs(src + (nb * 4 + v) * 32 + lane);
+  }
+  const int64_t rt = to / p.ncb;
+  const int cb = int(to - rt * p.ncb);
+  tile_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
+  if (p.done) {
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(p.done + (rt * kDmmaRowsPerSubtile) / p.done_rows, 1u);
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128) split_reduce_kernel(const LevelArgs p) {
+  pdl_wait();
+  constexpr int CG = wide_col_groups(NB);
+  constexpr int CW = kDmmaRowGroups * CG;
+  constexpr int NBW = (NB + CG - 1) / CG;
+  constexpr int NB_1 = (NB - NBW) < NBW ? (NB - NBW) : NBW;
+  constexpr int NB_2 = NB - NBW - NB_1;
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  const int64_t tiles = (p.M + kDmmaRowsPerSubtile - 1) / kDmmaRowsPerSubtile * p.ncb;
+  if (wg >= tiles * CW) return;
+  const int64_t to = wg / CW;
+  const int w = int(wg - to * CW);
+  const int rg = w % kDmmaRowGroups, cg = w / kDmmaRowGroups;
+  if constexpr (CG == 4) {
+    split_reduce_one<NB, NB / 4>(p, to, w, rg, cg * (NB / 4), lane);
+  } else if (cg == 0) {
+    split_reduce_one<NB, NBW>(p, to, w, rg, 0, lane);
+  } else if (cg == 1) {
+    if constexpr (NB_1 > 0) split_reduce_one<NB, NB_1>(p, to, w, rg, NBW, lane);
+  } else {
+    if constexpr (NB_2 > 0) split_reduce_one<NB, NB_2>(p, to, w, rg, NBW + NB_1, lane);
   }
 }
 
@@ -474,8 +491,11 @@ cudaError_t wide_prepare(int NB, size_t smem) {
 
 cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
   const bool split = a.ksplit > 1;
-  const bool hooks = a.ready != nullptr || a.done != nullptr;
-  if (split && (a.peers || !a.partial || !a.split_cnt)) return cudaErrorInvalidValue;
+  if (split && (a.peers || !a.partial)) return cudaErrorInvalidValue;
+  // the split kernel's tiles store partials only; the done hook belongs to the reduce launch
+  LevelArgs am = a;
+  if (split) am.done = nullptr;
+  const bool hooks = am.ready != nullptr || am.done != nullptr;
   wide::KernelFn f = wide::lookup(a.NB, a.peers ? 2 : (split ? 4 : 0) | (hooks ? 1 : 0));
   auto encode = wide::encode_fn();
   if (!f || !encode) return cudaErrorInvalidValue;
@@ -499,7 +519,22 @@ cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st) {
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, f, a, map);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, f, am, map);
+  if (e != cudaSuccess || !split) return e;
+  // split-K: the fixed-order reduction + epilogue as the next launch
+  const int64_t tiles = (a.M + kDmmaRowsPerSubtile - 1) / kDmmaRowsPerSubtile * a.ncb;
+  const int64_t warps = tiles * wide_consumer_warps(a.NB);
+  cudaLaunchConfig_t rc = cfg;
+  rc.gridDim = dim3(unsigned((warps + 3) / 4));
+  rc.blockDim = dim3(128);
+  rc.dynamicSmemBytes = 0;
+  switch (a.NB) {
+    case 4: return cudaLaunchKernelEx(&rc, wide::split_reduce_kernel<4>, a);
+    case 8: return cudaLaunchKernelEx(&rc, wide::split_reduce_kernel<8>, a);
+    case 12: return cudaLaunchKernelEx(&rc, wide::split_reduce_kernel<12>, a);
+    case 16: return cudaLaunchKernelEx(&rc, wide::split_reduce_kernel<16>, a);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_small(const LevelArgs& a, cudaStream_t st) {
