@@ -175,6 +175,26 @@ def test_repeated_applies_alternating_inputs_bitwise(qtt):
     oracle.assert_close(refs[0].cpu().numpy(), oracle.apply_alg2(cores, x))
 
 
+def test_repeated_applies_split_stage_bie_y(qtt):
+    """Race check for split-K at scale (found the in-kernel reduction bug,
+    DESIGN.md 6.8): the BIE factor Y (last stage K = 24320, split 4), pairs of
+    applies enqueued back to back with alternating inputs, 100 times."""
+    from qtt_workload import bie_case
+    _, _, _, Y, x = bie_case(0, 21, 9, 95, 50, 1)
+    x2 = np.ascontiguousarray(x[:, ::-1])
+    with qtt.QttOperator(Y) as op:
+        assert max(op.stage_splits(1)) > 1
+        xs = [torch.from_numpy(v).cuda() for v in (x, x2)]
+        refs = [op.apply(v).clone() for v in xs]
+        torch.cuda.synchronize()
+        bad = []
+        for i in range(100):
+            ys = [op.apply(v) for v in xs]
+            torch.cuda.synchronize()
+            bad += [(i, j) for j in range(2) if not torch.equal(ys[j], refs[j])]
+    assert not bad, bad
+
+
 def test_split_k_matches_unsplit_host_path(qtt):
     """qtt_apply_host's pipelined path never splits (its hooks need whole
     tiles); its result agrees with the split device path within tolerance."""
