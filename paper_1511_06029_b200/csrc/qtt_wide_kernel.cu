@@ -287,6 +287,8 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
         if ((MODE & 1) && p.ready) {   // this tile's rows of A must have arrived from the host
           const unsigned* f = p.ready + m0 / p.ready_rows;
           while (int(ld_acquire_u32(f) - p.ready_val) < 0) __nanosleep(200);
+          // the rows are read by the TMA unit (async proxy): order it after the acquire
+          asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         for (int ch = ch0; ch < ch1; ++ch, ++it) {
           const int s = it % kWideStages;
