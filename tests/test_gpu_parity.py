@@ -235,6 +235,17 @@ def test_diagonal_levels(qtt, d, r, nrhs, dlevels):
         assert any(s["variant"] == "diag" for s in st), st
 
 
+def test_diagonal_stage_host_apply_bitwise(qtt):
+    """qtt_apply_host with a diagonal last stage (chunked launches with row
+    offsets): bitwise equal to the device apply."""
+    from qtt_workload import bie_case
+    _, M, _, _, x = bie_case(4, 16, 9, 12, 8, 1)
+    with qtt.QttOperator(M) as op:
+        assert op.stages()[-1]["variant"] == "diag", op.stages()
+        yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        np.testing.assert_array_equal(op.apply_host(x), yd)
+
+
 def test_diagonal_levels_planned(qtt):
     """The block-diagonal top digits become one diag stage (BIE factor M's shape)."""
     from qtt_workload import bie_case
