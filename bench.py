@@ -794,7 +794,7 @@ def main(argv=None):
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(x_np.nbytes), "d2h_bytes_per_step": int(x_np.nbytes)},
         # one kernel per stage, plus the reduce launch of every split-K stage
-        "gpu_launches": sum(1 + (st_["ksplit"] > 1) for st_ in op.stages()) * args.steps,
+        "gpu_launches": sum(1 + (st_["ksplit"] > 1) for st_ in stages) * args.steps,
         "clocks": clocks,
         "other_configs_and_next_rows": extra,
     }
