@@ -202,19 +202,23 @@ def blas_threads():
         return os.cpu_count() or 1, []
 
 
-def run_cpu_baseline(cfg, cores, x, budget_s=20.0):
-    """Time the oracle (as it stands) on a bounded sample; returns a dict."""
-    s_bits = 3
-    flops, dt = oracle_sample(cores, x, cfg, s_bits)
-    # grow the sample toward ~budget_s of CPU work
-    while dt * 2 < budget_s and s_bits > 1:
-        s_bits -= 1
+def run_cpu_baseline(cfg, cores, x, budget_s=20.0, s_bits=None):
+    """Time the oracle (as it stands) on a bounded sample; returns a dict.
+    With s_bits given, that sample (1 of 2^s_bits top-bit blocks) is timed once;
+    else the sample grows from 1/8 toward ~budget_s of CPU work."""
+    if s_bits is not None:
         flops, dt = oracle_sample(cores, x, cfg, s_bits)
+    else:
+        s_bits = 3
+        flops, dt = oracle_sample(cores, x, cfg, s_bits)
+        while dt * 2 < budget_s and s_bits > 1:
+            s_bits -= 1
+            flops, dt = oracle_sample(cores, x, cfg, s_bits)
     threads, apis = blas_threads()
     return {"value": flops / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"oracle.alg2_sweep (Alg. 2, numpy/BLAS) over levels 1..{cfg.d - s_bits} on 1 of "
                       f"2^{s_bits} top-bit blocks of x ({flops / 1e9:.1f} GFLOP, {dt:.1f} s)",
-            "seconds": dt, "blas": apis, "host_cpus": os.cpu_count(), "affinity_cpus": _affinity(),
+            "seconds": dt, "s_bits": s_bits, "blas": apis, "host_cpus": os.cpu_count(), "affinity_cpus": _affinity(),
             "cpu_model": _cpu_model()}
 
 
@@ -537,8 +541,14 @@ def run_reference(args):
     nrhs = cfg.nrhs
     vals = []
     cb = None
+    # size the sample once (the first warm-up), then time the same sample every
+    # step; the per-step budget shrinks with the step count so the whole run
+    # stays within ~3 minutes of CPU time
+    budget = min(args.ref_budget, 180.0 / max(1, args.warmup + args.steps))
+    s_bits = None
     for it in range(args.warmup + args.steps):
-        c = run_cpu_baseline(cfg, cores, x, budget_s=args.ref_budget)
+        c = run_cpu_baseline(cfg, cores, x, budget_s=budget, s_bits=s_bits)
+        s_bits = c["s_bits"]
         if it >= args.warmup:
             vals.append(c["value"])
             cb = c

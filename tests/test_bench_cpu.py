@@ -57,3 +57,19 @@ def test_traffic_lookup_picks_latest_c4_summary():
           if json.load(open(p)).get("config") == "c4"
           and json.load(open(p)).get("algorithmic_flops_per_launch") == level_flops]
     assert name == max(c4, key=key)                       # the latest capture by round, then suffix
+
+
+def test_reference_arm_line():
+    """bench.py --impl reference (the oracle timed on host cores) prints the
+    contract line: impl, metric/unit of our arm, cpu_baseline, e2e."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1",
+                        "--ref-budget", "1"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == bench.UNIT and d["metric"] == bench.METRIC
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
