@@ -621,7 +621,9 @@ def run_sharded(args, world, rank, local, dev, cfg, cores, x_np):
                           + ("fused peer-store exchange" if args.exchange == "fused" else "NCCL reduce-scatter")),
            "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                    "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8)},
-           "gpu_launches": sum(1 + (st_.get("ksplit", 1) > 1) for st_ in op._shard.stages()) * args.steps,
+           # stages (+ split-K reduce launches), + the slot reduction of the fused exchange
+           "gpu_launches": (sum(1 + (st_.get("ksplit", 1) > 1) for st_ in op._shard.stages())
+                            + (1 if args.exchange == "fused" else 0)) * args.steps,
            "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(out))
