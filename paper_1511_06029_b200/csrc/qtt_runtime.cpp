@@ -181,7 +181,8 @@ bool is_device_ptr(const void* p, int dev) {
 
 // Workspace layout: [256 B: per-stage tile counters of the dynamic scheduler]
 // [buffer 0][buffer 1], each buffer max stage-boundary rank * N * nrhs doubles
-// (the ping-pong intermediate y_k of Alg. 2 at the stage boundaries).
+// (the ping-pong intermediate y_k of Alg. 2 at the stage boundaries)
+// [split-K partials of the largest split stage, if any].
 
 size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs) {
   if (h->stages.size() <= 1 && h->shard_bits == 0) return 0;
