@@ -736,6 +736,30 @@ def test_random_plan_fuzz(qtt, seed):
     oracle.assert_close(y, oracle.apply_alg2(cores, x))
 
 
+def test_variant_fuzz_with_diagonal_runs(qtt):
+    """80 random cases (d 1..18, ranks up to 64, nrhs 1..3, random stage caps),
+    half with a random run of diagonal levels, against the oracle; together they
+    exercise the merged, dmma, wide, small and diag kernels."""
+    rng = np.random.default_rng(2025)
+    seen = set()
+    for c in range(80):
+        d = int(rng.integers(1, 19))
+        maxr = int(rng.choice([2, 5, 8, 16, 24, 33, 48, 64]))
+        nrhs = int(rng.choice([1, 1, 2, 3]))
+        ranks, cores, x = random_case(8000 + c, d, maxr, nrhs)
+        if rng.random() < 0.5 and d >= 2:
+            a = int(rng.integers(0, d))
+            b = int(rng.integers(a, d)) + 1
+            eye = np.eye(2).reshape(1, 2, 2, 1)
+            for k in range(a, b):
+                cores[k] = np.ascontiguousarray(cores[k] * eye)
+        maxL = None if rng.random() < 0.6 else int(rng.integers(1, 11))
+        y, st = gpu_apply(qtt, cores, x, max_stage_levels=maxL)
+        seen.update(s["variant"] for s in st)
+        oracle.assert_close(y, oracle.apply_alg2(cores, x))
+    assert {"merged", "dmma", "wide", "small", "diag"} <= seen, seen
+
+
 def test_graph_cache_eviction_and_workspace_growth(qtt):
     """More (x, y) pairs than the 8 cached graphs, and growing nrhs (the cached
     workspace is reallocated and graphs on the old one dropped): every result
