@@ -301,8 +301,9 @@ qtt_status_t qtt_ipc_open(const unsigned char* handle64, void** ptr);
 qtt_status_t qtt_ipc_close(void* ptr);
 
 /* Plan facts: d, N, max rank, algorithmic flops per right-hand side
- * (4 * sum_k r_{k-1} r_k * N) and the number of kernel
- * launches one apply enqueues.  Any output pointer may be NULL. */
+ * (4 * sum_k r_{k-1} r_k * N) and the number of stages one
+ * apply runs (one kernel launch each; a split-K stage, see
+ * qtt_get_stage_split, adds its reduce launch).  Any output pointer may be NULL. */
 qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank,
                           double* flops_per_rhs, int* launches_per_apply);
 
