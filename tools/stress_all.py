@@ -19,8 +19,10 @@ def hunt(name, op_apply, xs, iters):
     print(name, "iterations", iters, "mismatches", bad, flush=True)
     return bad
 
+scale = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
 total = 0
 for name, iters in (("c3", 150), ("c2", 400), ("c1", 400), ("c4", 20)):
+    iters = int(iters * scale)
     cfg, cores, x = generate(name)
     x2 = np.ascontiguousarray(x[:, ::-1])
     with q.QttOperator(cores) as op:
@@ -28,6 +30,6 @@ for name, iters in (("c3", 150), ("c2", 400), ("c1", 400), ("c4", 20)):
 rm, M, ry, Y, x = bie_case(0, 21, 9, 95, 50, 1)
 x2 = np.ascontiguousarray(x[:, ::-1])
 with q.QttOperator(M) as opM, q.QttOperator(Y) as opY, q.QttProduct([opM, opY]) as P:
-    total += hunt("bie", P.apply, [torch.from_numpy(v).cuda() for v in (x, x2)], 60)
+    total += hunt("bie", P.apply, [torch.from_numpy(v).cuda() for v in (x, x2)], int(60 * scale))
 print("TOTAL", total)
 sys.exit(1 if total else 0)
