@@ -452,6 +452,9 @@ def test_abi_errors(qtt):
     assert lib.qtt_apply(h, x.ctypes.data, yt.data_ptr(), 1, None) == E.QTT_ERROR_NOT_SUPPORTED
     # null
     assert lib.qtt_apply(h, None, yt.data_ptr(), 1, None) == E.QTT_ERROR_INVALID_VALUE
+    # maximum size: N * nrhs must stay <= 2^31 (32-bit TMA row coordinates)
+    too_many = (1 << 31) // N + 1
+    assert lib.qtt_apply(h, xt.data_ptr(), yt.data_ptr(), too_many, None) == E.QTT_ERROR_NOT_SUPPORTED
     # short workspace
     ws = torch.empty(16, dtype=torch.float64, device="cuda")
     assert lib.qtt_apply_ws(h, xt.data_ptr(), yt.data_ptr(), 1, ws.data_ptr(), 128, None) == E.QTT_ERROR_INVALID_VALUE
