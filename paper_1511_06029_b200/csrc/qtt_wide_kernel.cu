@@ -23,6 +23,13 @@
 //   * 4 x CG consumer warps accumulate over all k-chunks of a tile in
 //     registers (DMMA m8n8k4, as in qtt_dmma_kernel.cuh) and store with the
 //     row-separation epilogue of the stage (out row m + Q*(s*(2^L-1) + ii)).
+//
+// This unit also holds the kernels that share that epilogue (tile_store):
+//   * instances by MODE flags: 1 host-copy hooks, 2 fused shard exchange
+//     (scatter_store into peer buffers), 4 split-K partials;
+//   * split_reduce_kernel: the fixed-order sum of split-K partials;
+//   * small_dmma_kernel: warp-tile stages straight from L2;
+//   * shard_reduce_kernel: a part's fixed-order sum of its P receive slots (§9).
 #include "qtt_dmma_kernel.cuh"
 
 #include <cuda.h>
