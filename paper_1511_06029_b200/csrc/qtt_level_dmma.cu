@@ -1,5 +1,6 @@
 // QTT stage contraction on the FP64 tensor cores of sm_100a: host-side glue
-// (instance lookup, launch) and the generic fallback kernel.  The DMMA kernel
+// (instance lookup, launch), the generic fallback kernel and the diagonal-
+// stage kernel (block-diagonal digits).  The DMMA kernel
 // template is in qtt_dmma_kernel.cuh, instantiated by qtt_dmma_inst_kb*.cu.
 //
 // One launch applies one core G_k (Alg. 2 lines 5-8), or
