@@ -17,11 +17,16 @@ def main():
     ap.add_argument("--rank", type=int, default=0, help="constant interior rank (bench's large-rank rows)")
     ap.add_argument("--d", type=int, default=18)
     ap.add_argument("--stage-times", action="store_true")
+    ap.add_argument("--bie", choices=["M", "Y"], default=None, help="a factor of qtt_workload.bie_case")
     args = ap.parse_args()
     import torch
     import paper_1511_06029_b200 as q
     from qtt_workload import generate
-    if args.rank:
+    if args.bie:
+        from qtt_workload import bie_case
+        _, cM, _, cY, x = bie_case(0, 21, 9, 95, 50, 1)
+        cores = cM if args.bie == "M" else cY
+    elif args.rank:
         from qtt_workload import random_case
         ranks = [1] + [args.rank] * (args.d - 1) + [1]
         _, cores, x = random_case(4242, args.d, args.rank, 1, ranks=ranks)
