@@ -30,7 +30,8 @@ namespace qtt {
 //              out[(m, ii)][b] = sum_a in[(m, ii)][a] D[ii][a][b], 2 r_in r_out
 //              flops per element whatever L (qtt_level_dmma.cu diag_kernel).
 enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2, kWide = 3, kSmall = 4, kDiag = 5 };
-constexpr int kDiagMaxROut = 8;                       // r_out of a diagonal stage
+constexpr int kDiagMaxROut = 8;                       // r_out of the row-per-lane diagonal kernel
+constexpr int kDiagMaxRank = 64;                      // r_in, r_out of any diagonal stage
 constexpr int kDiagMaxLevels = 24;
 constexpr size_t kDiagMaxCoreDoubles = size_t(1) << 23;   // D = r_in x 2^L x r_out
 // small variant: 16-row x 32-column warp tiles, k in steps of 8 (two k4 MMAs

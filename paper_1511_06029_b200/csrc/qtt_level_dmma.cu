@@ -140,10 +140,55 @@ __global__ void __launch_bounds__(256) diag_kernel(const LevelArgs p) {
   }
 }
 
+// Diagonal stage with r_out > 8 (e.g. block-diagonal digits at the bottom of
+// a profile, r_in small): one warp per input row R, lanes over the output
+// index b (two per lane, r_out <= 64); the row's r_in values are broadcast
+// loads, D[ii][a][b] and the output row are coalesced.  Fixed order over a.
+__global__ void __launch_bounds__(256) diag_out_kernel(const LevelArgs p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int r_in = p.r_in, r_out = p.r_out, n_i = p.n_i;
+  const int64_t nrows = p.M * n_i;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t R = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; R < nrows; R += nw) {
+    const int64_t m = R / n_i;
+    const int ii = int(R - m * n_i);
+    const double* x = p.in + R * r_in;
+    const double* D = p.core + size_t(ii) * r_in * r_out;
+    double acc0 = 0.0, acc1 = 0.0;
+    const bool b0 = lane < r_out, b1 = lane + 32 < r_out;
+#pragma unroll 4
+    for (int a = 0; a < r_in; ++a) {
+      const double xa = __ldg(x + a);
+      if (b0) acc0 = fma(xa, __ldg(D + size_t(a) * r_out + lane), acc0);
+      if (b1) acc1 = fma(xa, __ldg(D + size_t(a) * r_out + lane + 32), acc1);
+    }
+    const int64_t row = m + (((m >> p.log2_q) * (n_i - 1)) << p.log2_q) + (int64_t(ii) << p.log2_q);
+    if (b0) p.out[row * r_out + lane] = acc0;
+    if (b1) p.out[row * r_out + lane + 32] = acc1;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms) {
-  if (a.r_in > kDiagMaxRin || a.r_out > kDiagMaxROut) return cudaErrorInvalidValue;
+  if (a.r_in > kDiagMaxRin || a.r_out > kDiagMaxRank) return cudaErrorInvalidValue;
+  if (a.r_out > kDiagMaxROut) {   // lanes over the outputs
+    int64_t blocks = (a.M * a.n_i + 7) / 8;
+    const int64_t capo = int64_t(num_sms) * 16;
+    if (blocks > capo) blocks = capo;
+    if (blocks < 1) blocks = 1;
+    cudaLaunchAttribute attro[1];
+    attro[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attro[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cudaLaunchConfig_t co = {};
+    co.gridDim = dim3(unsigned(blocks));
+    co.blockDim = dim3(256);
+    co.stream = st;
+    co.attrs = attro;
+    co.numAttrs = 1;
+    return cudaLaunchKernelEx(&co, diag_out_kernel, a);
+  }
   const bool lane_ii = a.M < 32;
   const int64_t warps = lane_ii ? a.M * ((a.n_i + 31) / 32) : (a.M + 31) / 32 * a.n_i;
   int64_t blocks = (warps + 7) / 8;

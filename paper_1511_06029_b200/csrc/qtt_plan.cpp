@@ -268,7 +268,8 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
 static bool diag_shape(const int64_t* ranks, int k0, int k1, int64_t n, StagePlan* sp) {
   const int L = k1 - k0 + 1;
   const int64_t r_in = ranks[k0 - 1], r_out = ranks[k1];
-  if (r_out > kDiagMaxROut || r_in > 64 || double(r_in) * std::ldexp(1.0, L) * double(r_out) > double(kDiagMaxCoreDoubles))
+  if (r_out > kDiagMaxRank || r_in > kDiagMaxRank ||
+      double(r_in) * std::ldexp(1.0, L) * double(r_out) > double(kDiagMaxCoreDoubles))
     return false;
   *sp = StagePlan{};
   sp->k0 = k0;

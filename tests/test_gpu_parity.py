@@ -210,20 +210,22 @@ def test_split_k_matches_unsplit_host_path(qtt):
 
 # ------------------------------------------------------------------ diagonal (block-diagonal) levels
 DIAG_CASES = [
-    # d, max rank, nrhs, 0-based cores made diagonal in (i, j)
-    (12, 6, 1, list(range(5, 12))),          # block-diagonal in the top 7 digits, r_d = 1
-    (13, 8, 2, [4, 5, 6, 7]),                # a diagonal run in the middle (r_out <= 8 there)
-    (11, 5, 3, [0, 1, 2]),                   # the bottom digits
-    (10, 4, 1, list(range(10))),             # every level: one diagonal stage
-    (16, 3, 2, list(range(16))),             # a diagonal matrix: M = nrhs GEMM rows (lanes over ii)
-    (15, 8, 1, list(range(3, 15))),          # 12 diagonal levels: M = 8 rows
+    # d, max rank, nrhs, 0-based cores made diagonal in (i, j), the planner must pick "diag"
+    (12, 6, 1, list(range(5, 12)), True),           # block-diagonal in the top 7 digits, r_d = 1
+    (13, 8, 2, [4, 5, 6, 7], True),                 # a diagonal run in the middle (r_out <= 8 there)
+    (11, 5, 3, [0, 1, 2], False),                   # the bottom digits
+    (10, 4, 1, list(range(10)), True),              # every level: one diagonal stage
+    (16, 3, 2, list(range(16)), True),              # a diagonal matrix: M = nrhs GEMM rows (lanes over ii)
+    (15, 8, 1, list(range(3, 15)), True),           # 12 diagonal levels: M = 8 rows
+    (14, 40, 2, [0, 1, 2, 3, 4], False),            # bottom digits at larger rank (parity only)
+    (13, 64, 1, [5, 6], False),                     # a middle run at rank up to 64 (parity only)
 ]
 
 
-@pytest.mark.parametrize("d,r,nrhs,dlevels", DIAG_CASES)
-def test_diagonal_levels(qtt, d, r, nrhs, dlevels):
-    """Cores with exact zeros off the (i, j) diagonal are applied as one
-    streaming stage (variant 'diag'); parity with the oracle, which knows
+@pytest.mark.parametrize("d,r,nrhs,dlevels,expect", DIAG_CASES)
+def test_diagonal_levels(qtt, d, r, nrhs, dlevels, expect):
+    """Cores with exact zeros off the (i, j) diagonal; where the planner picks
+    the streaming "diag" stage it must; parity with the oracle, which knows
     nothing of the structure."""
     ranks, cores, x = random_case(3100 + d, d, r, nrhs)
     eye = np.eye(2).reshape(1, 2, 2, 1)
@@ -231,8 +233,22 @@ def test_diagonal_levels(qtt, d, r, nrhs, dlevels):
         cores[k] = np.ascontiguousarray(cores[k] * eye)
     y, st = gpu_apply(qtt, cores, x)
     oracle.assert_close(y, oracle.apply_alg2(cores, x))
-    if len(dlevels) >= 4:
+    if expect:
         assert any(s["variant"] == "diag" for s in st), st
+
+
+def test_diagonal_wide_outputs_kernel(qtt):
+    """A diagonal run whose r_out exceeds 8 (lanes-over-outputs kernel): the
+    bottom digits of a constant rank-24 profile, N = 2^18."""
+    d, r = 18, 24
+    ranks = [1] + [r] * (d - 1) + [1]
+    _, cores, x = random_case(3300, d, r, 2, ranks=ranks)
+    eye = np.eye(2).reshape(1, 2, 2, 1)
+    for k in range(0, 6):
+        cores[k] = np.ascontiguousarray(cores[k] * eye)
+    y, st = gpu_apply(qtt, cores, x)
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
+    assert st[0]["variant"] == "diag" and st[0]["k_last"] == 6, st
 
 
 def test_diagonal_stage_host_apply_bitwise(qtt):
