@@ -317,7 +317,9 @@ qtt_status_t qtt_get_info(qtt_handle_t h, int* d, int64_t* N, int64_t* max_rank,
  * in (i_k, j_k), i.e. A block-diagonal in those digits, applied as one
  * streaming batched GEMV whatever their number, see qtt_plan_stages).  The
  * diagonal levels are detected at qtt_create from exact zeros; the host-only
- * qtt_plan_stages knows ranks only and never plans variant 5.
+ * qtt_plan_stages knows ranks only and never plans variant 5.  Such zeros are
+ * structural: a NaN/Inf in x then stays inside its block instead of spreading
+ * through 0 * Inf products (reading R21).
  */
 qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int* variant);
 

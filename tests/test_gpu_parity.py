@@ -570,6 +570,29 @@ def test_nan_inf_propagate(qtt):
     np.testing.assert_array_equal(np.isnan(y), np.isnan(ref))
 
 
+def test_nan_stays_in_its_block_for_diagonal_levels(qtt):
+    """DESIGN.md R21: diagonal cores are structural zeros -- a NaN in x reaches
+    exactly the outputs of its own block (top digits equal), all others stay
+    finite and match the oracle evaluated on the NaN-free blocks."""
+    d, top = 12, 7
+    ranks, cores, x = random_case(3100 + d, d, 6, 1)      # DIAG_CASES[0]: planned as a diag stage
+    eye = np.eye(2).reshape(1, 2, 2, 1)
+    for k in range(d - top, d):
+        cores[k] = np.ascontiguousarray(cores[k] * eye)
+    x = x.copy()
+    j = 37
+    x[0, j] = np.nan
+    y, st = gpu_apply(qtt, cores, x)
+    assert any(s["variant"] == "diag" for s in st), st
+    blk = np.arange(1 << d) >> (d - top)
+    inside = blk == (j >> (d - top))
+    assert np.all(np.isnan(y[0, inside])) and np.all(np.isfinite(y[0, ~inside]))
+    xz = x.copy()
+    xz[0, j] = 0.0
+    oracle.assert_close(y[:, ~inside], oracle.apply_alg2(cores, xz)[:, ~inside],
+                        rms=float(np.sqrt(np.mean(oracle.apply_alg2(cores, xz) ** 2))), check_l2=False)
+
+
 def test_graph_replay_matches_plain_enqueue(qtt):
     """Applies replay a cached CUDA graph per (x, y, workspace, nrhs); the result is
     bitwise that of the plain per-stage enqueue (stage timing on disables graphs),
