@@ -45,6 +45,17 @@ def test_sharded_equals_full(par, d, maxr, s, nrhs):
     oracle.assert_close(y, oracle.apply_alg2(cores, x))
 
 
+@pytest.mark.parametrize("s", [1, 2])
+def test_sharded_block_diagonal_operator(par, s):
+    """Shards of a BIE-shaped block-diagonal factor (qtt_workload.bie_case M):
+    the local levels end in a diagonal stage, then the projection."""
+    from qtt_workload import bie_case
+    _, M, _, _, x = bie_case(6, 15, 6, 12, 8, 2)
+    y, stages = sharded_emulation(par, M, x, s)
+    assert any(st["variant"] == "diag" for st in stages), stages
+    oracle.assert_close(y, oracle.apply_alg2(M, x))
+
+
 def test_sharded_c3_p8(par):
     cfg, cores, x = generate("c3")
     y, _ = sharded_emulation(par, cores, x, 3)
