@@ -80,3 +80,29 @@ def test_python_validation(q):
         q.qtt_create([np.zeros((1, 2, 2, 3))], ranks=[1, 1])
     with pytest.raises(ValueError):
         q.qtt_create([])
+
+
+def _build_c_example(tmp_path, q):
+    """Compile examples/qtt_c_example.c as plain C99 against include/qtt.h."""
+    import shutil
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "qtt_c_example")
+    libdir = os.path.dirname(q.library_path())
+    cmd = [gcc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-I" + os.path.join(root, "include"),
+           "-I/usr/local/cuda/include", os.path.join(root, "examples", "qtt_c_example.c"),
+           "-L" + libdir, "-lqtt_b200", "-L/usr/local/cuda/lib64", "-lcudart", "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    env = dict(os.environ, LD_LIBRARY_PATH=libdir + ":/usr/local/cuda/lib64:" + os.environ.get("LD_LIBRARY_PATH", ""))
+    return exe, env
+
+
+def test_c_example_compiles_and_plans(tmp_path, q):
+    """The header is valid C99 and the library links from plain C; the host-only
+    planner runs without a GPU."""
+    exe, env = _build_c_example(tmp_path, q)
+    r = subprocess.run([exe, "--plan"], capture_output=True, text=True, env=env)
+    assert r.returncode == 0 and "QTT_SUCCESS" in r.stdout, r.stdout + r.stderr

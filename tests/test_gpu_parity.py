@@ -825,3 +825,19 @@ def test_graph_cache_eviction_and_workspace_growth(qtt):
             assert torch.equal(y, refs[0][:n])
     finally:
         op.close()
+
+
+def test_plain_c_program_applies_the_shift(qtt, tmp_path):
+    """examples/qtt_c_example.c: create / apply / destroy through include/qtt.h
+    from plain C (no Python in the loop); the shift operator is exact, so the
+    program checks y == roll(x, 1) bitwise."""
+    import importlib.util
+    import os
+    import subprocess
+    spec = importlib.util.spec_from_file_location(
+        "abi_cpu", os.path.join(os.path.dirname(os.path.abspath(__file__)), "test_abi_cpu.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    exe, env = mod._build_c_example(tmp_path, qtt)
+    r = subprocess.run([exe], capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode == 0 and " 0 of " in r.stdout, r.stdout + r.stderr
