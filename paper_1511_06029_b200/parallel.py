@@ -296,13 +296,17 @@ class ShardedQttOperator:
         self._ev_red.record(st)
         return y if x_local.dim() == 2 else y.view(-1)
 
-    def close(self):
+    def close(self, sync: bool = True):
+        """Free the shard and the exchange buffers.  With fused exchange, every
+        part must call close() (collective: a device sync and a host barrier,
+        so no peer still stores into our buffer).  The finaliser passes
+        sync=False: it must not block on peers that may already be gone."""
         if self._ev_red is not None:
-            # peers may still be storing into our buffer or reading theirs: drain
-            import torch
-            import torch.distributed as dist
-            torch.cuda.synchronize()
-            dist.barrier(group=self._hgroup)
+            if sync:
+                import torch
+                import torch.distributed as dist
+                torch.cuda.synchronize()
+                dist.barrier(group=self._hgroup)
             self._ev_proj = self._ev_red = None
             self._peer_proj, self._peer_red = [], []
         for o in (self._op, self._shard):
@@ -319,7 +323,7 @@ class ShardedQttOperator:
 
     def __del__(self):
         try:
-            self.close()
+            self.close(sync=False)
         except Exception:
             pass
 
