@@ -122,6 +122,10 @@ qtt_status_t qtt_plan_stages_split(int d, const int64_t* ranks, size_t smem_opti
  * keeps a cached workspace of qtt_workspace_size() bytes, allocated on first
  * use with cudaMallocAsync on `stream`; concurrent applies on one handle
  * from different streams must use qtt_apply_ws instead.  No host sync.
+ * CUDA graph capture of `stream` is supported once the cached workspace
+ * exists for this nrhs (apply once outside the capture, or use qtt_apply_ws);
+ * otherwise QTT_ERROR_NOT_SUPPORTED.  Work captured into the caller's graph
+ * is not tracked for the cross-stream ordering of later applies.
  */
 qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
                        qtt_stream_t stream);

@@ -214,6 +214,9 @@ qtt_status_t qtt_shard_apply(qtt_handle_t h, const double* x_local, double* send
   try {
     DeviceGuard g(h->device);
     const size_t need = ws_bytes_for(h, nrhs);
+    const bool capturing = stream_is_capturing(st);
+    // a workspace allocated inside a graph capture would belong to that graph
+    if (capturing && need > h->ws_bytes) return QTT_ERROR_NOT_SUPPORTED;
     if (need > h->ws_bytes) {
       if (h->ws) cudaFreeAsync(h->ws, h->ws_stream);
       h->ws = nullptr;
@@ -228,7 +231,7 @@ qtt_status_t qtt_shard_apply(qtt_handle_t h, const double* x_local, double* send
     }
     qtt_status_t so = order_after_last(h, st);
     if (so == QTT_SUCCESS) so = enqueue(h, x_local, send, nrhs, h->ws, st);
-    if (so == QTT_SUCCESS) {
+    if (so == QTT_SUCCESS && !capturing) {
       h->last_stream = st;
       h->has_last = true;
     }
@@ -281,6 +284,9 @@ qtt_status_t qtt_shard_apply_fused(qtt_handle_t h, const double* x_local, int64_
   try {
     DeviceGuard g(h->device);
     const size_t need = ws_bytes_for(h, nrhs);
+    const bool capturing = stream_is_capturing(st);
+    // a workspace allocated inside a graph capture would belong to that graph
+    if (capturing && need > h->ws_bytes) return QTT_ERROR_NOT_SUPPORTED;
     if (need > h->ws_bytes) {
       if (h->ws) cudaFreeAsync(h->ws, h->ws_stream);
       h->ws = nullptr;
@@ -295,7 +301,7 @@ qtt_status_t qtt_shard_apply_fused(qtt_handle_t h, const double* x_local, int64_
     }
     qtt_status_t so = order_after_last(h, st);
     if (so == QTT_SUCCESS) so = enqueue(h, x_local, nullptr, nrhs, h->ws, st, true);
-    if (so == QTT_SUCCESS) {
+    if (so == QTT_SUCCESS && !capturing) {
       h->last_stream = st;
       h->has_last = true;
     }
@@ -409,6 +415,9 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
   try {
     DeviceGuard g(h->device);
     const size_t need = ws_bytes_for(h, nrhs);
+    const bool capturing = stream_is_capturing(st);
+    // a workspace allocated inside a graph capture would belong to that graph
+    if (capturing && need > h->ws_bytes) return QTT_ERROR_NOT_SUPPORTED;
     if (need > h->ws_bytes) {
       if (h->ws) {
         // the old buffer may still be in use by work on its stream
@@ -432,7 +441,7 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
     const qtt_status_t so = order_after_last(h, st);
     if (so != QTT_SUCCESS) return so;
     const qtt_status_t s2 = enqueue_graphed(h, x, y, nrhs, h->ws, st);
-    if (s2 == QTT_SUCCESS) {
+    if (s2 == QTT_SUCCESS && !capturing) {
       h->last_stream = st;
       h->has_last = true;
     }

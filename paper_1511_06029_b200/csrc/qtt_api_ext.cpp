@@ -243,6 +243,8 @@ qtt_status_t qtt_product_apply(qtt_product_t p, const double* x, double* y, int6
   try {
     DeviceGuard g(p->device);
     const size_t need = product_ws_bytes(p, nrhs);
+    // a workspace allocated inside a graph capture would belong to that graph
+    if (need > p->ws_bytes && stream_is_capturing(st)) return QTT_ERROR_NOT_SUPPORTED;
     if (need > p->ws_bytes) {
       if (p->ws) cudaFreeAsync(p->ws, p->ws_stream);
       p->ws = nullptr;

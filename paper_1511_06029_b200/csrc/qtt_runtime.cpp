@@ -461,7 +461,9 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
     in = out;
   }
   if (h->timing) h->timed_applies++;
-  if (st != h->capture_stream) cudaEventRecord(h->last, st);
+  // an event recorded inside a capture (ours or the caller's) cannot order
+  // later work outside it: only plain enqueues update the handle's last event
+  if (st != h->capture_stream && !stream_is_capturing(st)) cudaEventRecord(h->last, st);
   return QTT_SUCCESS;
 }
 
@@ -513,6 +515,15 @@ qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nr
 // The cached workspace is shared by every apply on the handle: order this one
 // after the previous one when that was enqueued on another stream (skipped
 // while `st` is being captured by the caller).
+bool stream_is_capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
 qtt_status_t order_after_last(qtt_plan* h, cudaStream_t st) {
   if (!h->has_last || h->last_stream == st) return QTT_SUCCESS;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;

@@ -206,6 +206,8 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
 qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
                      bool fused = false);
 qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st);
+// true while `st` is being captured into a CUDA graph (ours or the caller's)
+bool stream_is_capturing(cudaStream_t st);
 qtt_status_t order_after_last(qtt_plan* h, cudaStream_t st);
 qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs);
 // qtt_host_copy.cpp

@@ -593,6 +593,38 @@ def test_nan_stays_in_its_block_for_diagonal_levels(qtt):
                         rms=float(np.sqrt(np.mean(oracle.apply_alg2(cores, xz) ** 2))), check_l2=False)
 
 
+def test_caller_graph_capture(qtt):
+    """The caller captures qtt_apply into its own CUDA graph (torch.cuda.graph):
+    replays are bitwise equal to plain applies, plain applies on other streams
+    still work afterwards (the captured event is not used for ordering), and a
+    capture before the cached workspace exists is refused (NOT_SUPPORTED)."""
+    _, cores, x = generate("c2")
+    xt = torch.from_numpy(x).cuda()
+    s = torch.cuda.Stream()
+    with qtt.QttOperator(cores) as op:
+        ref = op.apply(xt).clone()
+        torch.cuda.synchronize()
+        y = torch.empty_like(xt)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            op.apply(xt, out=y)
+        for _ in range(3):
+            y.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(y, ref)
+        assert torch.equal(op.apply(xt), ref)
+        del g
+    with qtt.QttOperator(cores) as op:
+        g = torch.cuda.CUDAGraph()
+        y = torch.empty_like(xt)
+        with pytest.raises(qtt.QttError):
+            with torch.cuda.graph(g, stream=s):
+                op.apply(xt, out=y)
+        torch.cuda.synchronize()
+        assert torch.equal(op.apply(xt), ref)
+
+
 def test_graph_replay_matches_plain_enqueue(qtt):
     """Applies replay a cached CUDA graph per (x, y, workspace, nrhs); the result is
     bitwise that of the plain per-stage enqueue (stage timing on disables graphs),
