@@ -155,6 +155,8 @@ static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, 
     }
   } catch (const std::bad_alloc&) {
     st = QTT_ERROR_OUT_OF_MEMORY;
+  } catch (...) {   // no exception may cross the C ABI
+    st = QTT_ERROR_CUDA;
   }
   if (st == QTT_SUCCESS && cudaEventCreateWithFlags(&h->last, cudaEventDisableTiming) != cudaSuccess)
     st = QTT_ERROR_CUDA;
