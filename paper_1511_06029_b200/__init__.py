@@ -244,6 +244,16 @@ class QttOperator:
         self.ranks = [int(np.shape(cores[0])[0])] + [int(np.shape(G)[3]) for G in cores]
 
     @classmethod
+    def transpose_of(cls, cores, max_stage_levels: int | None = None) -> "QttOperator":
+        """The operator A^T for A given by `cores`: the row and column digits of
+        every core swapped, G^T_k[a][j][i][b] = G_k[a][i][j][b] (the QTT
+        definition P:953-962 read with i and j exchanged).  Host-side reshuffle
+        of the cores; the apply is the ordinary one."""
+        arrs, ranks = _marshal_cores(cores, None)
+        return cls([np.ascontiguousarray(np.transpose(G, (0, 2, 1, 3))) for G in arrs], ranks,
+                   max_stage_levels)
+
+    @classmethod
     def from_ttb1(cls, path, max_stage_levels: int | None = None) -> "QttOperator":
         """Operator from a TTB1 core file (``ttb1.load_operator``)."""
         from . import ttb1

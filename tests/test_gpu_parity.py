@@ -525,6 +525,21 @@ def test_core_arrays_may_be_freed_after_create(qtt):
     oracle.assert_close(y, oracle.apply_alg2(keep, x))
 
 
+def test_transpose_of(qtt):
+    """QttOperator.transpose_of(cores) applies A^T: against the oracle on the
+    pinned transpose (oracle.transpose), and <u, A v> = <A^T u, v>."""
+    _, cores, x = random_case(4545, 12, 9, 2)
+    with qtt.QttOperator.transpose_of(cores) as opT, qtt.QttOperator(cores) as op:
+        xt = torch.from_numpy(x).cuda()
+        yT = opT.apply(xt).cpu().numpy()
+        y = op.apply(xt).cpu().numpy()
+    oracle.assert_close(yT, oracle.apply_alg2(oracle.transpose(cores), x))
+    u, v = x[0], x[1]
+    lhs = float(u @ y[1])          # <u, A v>
+    rhs = float(yT[0] @ v)         # <A^T u, v>
+    assert abs(lhs - rhs) <= 1e-10 * max(1.0, abs(lhs)), (lhs, rhs)
+
+
 def test_operator_from_ttb1_file(qtt, tmp_path):
     """An operator loaded from a TTB1 core file applies bitwise like the same
     cores passed directly."""
