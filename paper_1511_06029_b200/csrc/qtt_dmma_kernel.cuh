@@ -139,6 +139,7 @@ __device__ __forceinline__ void subtile_store(const double (&c)[NBC > 0 ? NBC : 
       if (coff[nb] < 0) continue;
       double* dst = rowp + coff[nb];
       const double v0 = c[nb][2 * h], v1 = c[nb][2 * h + 1];
+      QTT_CHECK_OUT(p, dst, vec_out ? 2 : 1);
       if (vec_out) {
         *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
       } else {

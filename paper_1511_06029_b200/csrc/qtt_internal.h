@@ -76,6 +76,17 @@ QTT_HD constexpr bool wide_instantiated(int NB) { return NB == 4 || NB == 8 || N
 //   out[(m + Q*(s*(n_i-1) + ii)) * r_out + b] = sum_{jj,a} W[a,ii,jj,b] * A[m][jj*r_in + a]
 // with Q = N / n_i, s = m / Q (the RHS), W the stage's super-core.  L = 1 is
 // one level of Alg. 2 (W = G_k): out row m + (N/2)(s + i_k).
+#ifdef QTT_BOUNDS_CHECK
+#define QTT_CHECK_OUT(p, ptr, n)                                                                        \
+  do {                                                                                                \
+    if ((p).out_limit && ((ptr) < (p).out || (ptr) - (p).out + (n) > (p).out_limit)) __trap();       \
+  } while (0)
+#else
+#define QTT_CHECK_OUT(p, ptr, n) \
+  do {                           \
+  } while (0)
+#endif
+
 struct LevelArgs {
   const double* in = nullptr;
   double* out = nullptr;
@@ -115,6 +126,9 @@ struct LevelArgs {
   int64_t peer_offset = 0;         // added to every peers[ii] (this part's slot: part * M)
   // wide variant, split-K (ksplit > 1): tile t = output tile t / ksplit, k-chunks
   // [(t % ksplit) * kcps, ...); partial sums in `partial`, reduced by the next launch
+  // debug builds (-DQTT_BOUNDS_CHECK): doubles addressable from `out` (0 = unchecked);
+  // every epilogue store traps outside [out, out + out_limit)
+  int64_t out_limit = 0;
   int ksplit = 1;
   int kcps = 0;                    // k-chunks per split
   double* partial = nullptr;       // [output tiles][ksplit][consumer warps][split_slot_doubles(NB)]

@@ -63,7 +63,9 @@ __global__ void level_generic_kernel(const LevelArgs p) {
       for (int a = 0; a < r_in; ++a) acc = fma(g[size_t(a) * 4 * r_out], in[a], acc);
     }
     const int64_t sr = m >> p.log2_q;   // L = 1: n_i = 2, Q = N/2
-    p.out[(m + ((sr + i) << p.log2_q)) * r_out + b] = acc;
+    double* dst = p.out + (m + ((sr + i) << p.log2_q)) * r_out + b;
+    QTT_CHECK_OUT(p, dst, 1);
+    *dst = acc;
   }
 }
 
@@ -136,7 +138,10 @@ __global__ void __launch_bounds__(256) diag_kernel(const LevelArgs p) {
     const int64_t row = m + (((m >> p.log2_q) * (n_i - 1)) << p.log2_q) + (int64_t(ii) << p.log2_q);
 #pragma unroll
     for (int b = 0; b < kDiagMaxROut; ++b)
-      if (b < r_out) p.out[row * r_out + b] = acc[b];
+      if (b < r_out) {
+        QTT_CHECK_OUT(p, p.out + row * r_out + b, 1);
+        p.out[row * r_out + b] = acc[b];
+      }
   }
 }
 
@@ -164,8 +169,14 @@ __global__ void __launch_bounds__(256) diag_out_kernel(const LevelArgs p) {
       if (b1) acc1 = fma(xa, __ldg(D + size_t(a) * r_out + lane + 32), acc1);
     }
     const int64_t row = m + (((m >> p.log2_q) * (n_i - 1)) << p.log2_q) + (int64_t(ii) << p.log2_q);
-    if (b0) p.out[row * r_out + lane] = acc0;
-    if (b1) p.out[row * r_out + lane + 32] = acc1;
+    if (b0) {
+      QTT_CHECK_OUT(p, p.out + row * r_out + lane, 1);
+      p.out[row * r_out + lane] = acc0;
+    }
+    if (b1) {
+      QTT_CHECK_OUT(p, p.out + row * r_out + lane + 32, 1);
+      p.out[row * r_out + lane + 32] = acc1;
+    }
   }
 }
 

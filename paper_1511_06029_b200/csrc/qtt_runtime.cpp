@@ -373,6 +373,9 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
   a.nchunks = sp.nchunks;
   a.ncb = sp.ncb;
   a.nout = sp.n_i * sp.r_out;
+  // rows the stage's output holds from `out` on (a chunk's pointer is pre-offset
+  // by m_base rows): the whole output is max(M n_i, N) rows of r_out doubles
+  a.out_limit = (std::max<int64_t>(M * sp.n_i, h->N) - m_base) * sp.r_out;
   if (hooks) {
     a.peers = hooks->peers;
     a.peer_offset = hooks->peer_offset;

@@ -124,13 +124,16 @@ __device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const Leve
       const int n = n_lane + nb * 8;
       if (n < p.nout) {
         double* dst = p.out + (rowbase + (int64_t(ii) << p.log2_q)) * r_out + b;
+        QTT_CHECK_OUT(p, dst, vec ? 2 : 1);
         if (vec) {
           *reinterpret_cast<double2*>(dst) = make_double2(c[nb][2 * h], c[nb][2 * h + 1]);
         } else {
           dst[0] = c[nb][2 * h];
           if (n + 1 < p.nout) {
             const bool wrap = (b + 1 == r_out);
-            p.out[(rowbase + (int64_t(ii + wrap) << p.log2_q)) * r_out + (wrap ? 0 : b + 1)] = c[nb][2 * h + 1];
+            double* d1 = p.out + (rowbase + (int64_t(ii + wrap) << p.log2_q)) * r_out + (wrap ? 0 : b + 1);
+            QTT_CHECK_OUT(p, d1, 1);
+            *d1 = c[nb][2 * h + 1];
           }
         }
       }
