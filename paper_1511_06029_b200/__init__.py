@@ -236,6 +236,8 @@ class QttOperator:
         else:
             self._h = qtt_create_ex(cores, ranks, max_stage_levels)
         info = qtt_get_info(self._h)
+        import torch
+        self.device = torch.device("cuda", torch.cuda.current_device())   # where qtt_create put the cores
         self.d = info["d"]
         self.N = info["N"]
         self.max_rank = info["max_rank"]
@@ -317,7 +319,7 @@ class QttOperator:
         if cores_only:
             R = [a * b for a, b in zip(self.ranks, br)]
             sizes = [R[k] * 2 * R[k + 1] for k in range(self.d)]
-            buf = torch.empty(sum(sizes), dtype=torch.float64, device="cuda")
+            buf = torch.empty(sum(sizes), dtype=torch.float64, device=self.device)
             _lib.check("qtt_compressed_matvec_cores", lib.qtt_compressed_matvec_cores(
                 self.handle, rb, ptrs, _ptr(buf), buf.numel() * 8, cr, _stream_handle(stream)))
             out_cores, off = [], 0
@@ -325,7 +327,7 @@ class QttOperator:
                 out_cores.append(buf[off:off + sizes[k]].view(R[k], 2, R[k + 1]))
                 off += sizes[k]
             return out_cores
-        y = torch.empty(self.N, dtype=torch.float64, device="cuda") if out is None else out
+        y = torch.empty(self.N, dtype=torch.float64, device=self.device) if out is None else out
         if y.numel() != self.N or y.dtype != torch.float64 or not y.is_cuda or not y.is_contiguous():
             raise ValueError("out must be a contiguous float64 CUDA tensor of N entries")
         _lib.check("qtt_compressed_matvec", lib.qtt_compressed_matvec(
