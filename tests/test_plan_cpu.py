@@ -129,6 +129,16 @@ def test_plan_validation(q):
         q.qtt_plan_stages([1, 2, 1], 0, 0)
     with pytest.raises(QttError):
         q.qtt_plan_stages([1] * 32)
+    # the split variant validates the same way and accepts NULL outputs
+    import ctypes as C
+    lib = q._lib.load()
+    n = C.c_int()
+    r = (C.c_int64 * 3)(2, 1, 1)
+    assert lib.qtt_plan_stages_split(2, r, 0, 10, C.byref(n), None, None, None, None) == q._lib.QTT_ERROR_INVALID_VALUE
+    r = (C.c_int64 * 3)(1, 3, 1)
+    assert lib.qtt_plan_stages_split(2, r, 0, 10, C.byref(n), None, None, None, None) == q._lib.QTT_SUCCESS
+    assert n.value >= 1
+    assert lib.qtt_plan_stages_split(2, r, 0, 10, None, None, None, None, None) == q._lib.QTT_ERROR_INVALID_VALUE
 
 
 # --- super-cores (host logic of merged stages) --------------------------------
