@@ -14,6 +14,7 @@ see DESIGN.md §"Oracle and pins".  No function here is "parity unpinned".
 """
 from .qtt_oracle import (
     entry, dense_matrix, apply_dense, apply_bitwise, alg2_sweep, apply_alg2,
+    blas_sweep, apply_blas_sweep, top_projection, apply_chunked, kron_apply_modes,
     apply_rows, compose, transpose, compressed_matvec, tt_vector_dense,
     tt_vector_entries, kron_vector_cores,
 )
@@ -22,6 +23,7 @@ from . import morton
 
 __all__ = [
     "entry", "dense_matrix", "apply_dense", "apply_bitwise", "alg2_sweep",
-    "apply_alg2", "apply_rows", "compose", "transpose", "compressed_matvec",
+    "apply_alg2", "blas_sweep", "apply_blas_sweep", "top_projection", "apply_chunked",
+    "kron_apply_modes", "apply_rows", "compose", "transpose", "compressed_matvec",
     "tt_vector_dense", "tt_vector_entries", "kron_vector_cores", "compare", "assert_close", "morton",
 ]

@@ -146,6 +146,124 @@ def apply_alg2(cores, x, dtype=np.float64):
 
 
 # ---------------------------------------------------------------------------
+# Alg. 2 with BLAS calls and no copies (SURVEY §8(c) oracle 3, the timed CPU
+# baseline).  The same lines 3-10 as ``alg2_sweep``; only the storage of y_k
+# differs: Matlab keeps y_k (r_k x N) column-major, and a C-order numpy array
+# Y_k of shape [N][r_k] is exactly those bytes, Y_k[c][alpha] = y_k(alpha, c).
+#   line 6  b_k(overline{alpha_{k-1} j_k}, c') = y_{k-1}(alpha_{k-1}, overline{j_k c'})
+#           -> b_k^T = Y_{k-1} viewed as [N/2][2 r_{k-1}]  (free reshape)
+#   line 7  phi_k = M_k b_k  ->  phi_k^T = b_k^T M_k^T
+#   line 8  y_k(alpha_k, overline{c' i_k}) = phi_k(overline{alpha_k i_k}, c')
+#           -> Y_k[c' + (N/2) i_k] = (b_k^T M_k^T)[c', i_k r_k : (i_k+1) r_k]
+# so each level is two matmuls, one per i_k, each writing straight into its
+# half of Y_k (``out=``); two buffers rotate.
+# ---------------------------------------------------------------------------
+def _mt_half(G, i, dtype):
+    """Columns i r_k .. (i+1) r_k - 1 of M_k^T (Alg. 2 line 5):
+    M_k^T[alpha_{k-1} + r_{k-1} j, beta] = G_k[alpha_{k-1}, i, j, beta]."""
+    Gi = np.asarray(G[:, i, :, :], dtype=dtype)              # [alpha_{k-1}, j, beta]
+    return np.ascontiguousarray(Gi.transpose(1, 0, 2).reshape(2 * G.shape[0], G.shape[3]))
+
+
+def blas_sweep(cores, b, dtype=np.float64):
+    """Alg. 2 lines 3-9 on one vector b of length 2^len(cores); returns Y_d,
+    the C-order [N][r_d] array (= y_d column-major; an open right bond r_d > 1
+    is allowed, as ``alg2_sweep``).  With no cores, Y_0 = b as [N][1]."""
+    b = np.ascontiguousarray(np.asarray(b, dtype=dtype).reshape(-1))
+    N = b.shape[0]
+    d = len(cores)
+    assert N == 1 << d
+    ranks = [1] + [int(G.shape[3]) for G in cores]
+    if d == 0:
+        return b.reshape(N, 1)
+    rmax = max(ranks[1:])
+    bufs = [np.empty(N * rmax, dtype=dtype), np.empty(N * rmax, dtype=dtype)]
+    Y = b                                                      # line 3: y_0 = b^T (r_0 = 1)
+    for k in range(1, d + 1):
+        G = cores[k - 1]
+        r_prev, r_k = ranks[k - 1], ranks[k]
+        inp = Y.reshape(N // 2, 2 * r_prev)                    # line 6 (view)
+        out = bufs[k % 2][: N * r_k].reshape(N, r_k)
+        for i in (0, 1):                                       # lines 7-8
+            np.matmul(inp, _mt_half(G, i, dtype), out=out[i * (N // 2):(i + 1) * (N // 2)])
+        Y = out
+    return Y.reshape(N, ranks[d])
+
+
+def apply_blas_sweep(cores, x, dtype=np.float64):
+    """y = A x by ``blas_sweep`` (line 10: y = y_d^T, r_d = 1), one RHS at a time."""
+    x = np.atleast_2d(np.asarray(x, dtype=dtype))
+    out = np.empty_like(x)
+    for s in range(x.shape[0]):
+        Y = blas_sweep(cores, x[s], dtype)
+        assert Y.shape[1] == 1
+        out[s] = Y[:, 0]
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Chunked sweep (SURVEY §8(c) oracle 4; top-bit blocks, P:1487-1496).  Split
+# the index into its top s digits (g for the column, h for the row) and the
+# low d - s digits.  By the definition (Eq. TTdeccores, P:519-523),
+#   A(h n + i', g n + j') = [G_1 ... G_{d-s}](i', j') . c_{h,g},
+#   c_{h,g} = G_{d-s+1}(:, h_1 g_1, :) ... G_d(:, h_s g_s, :)     (r_{d-s} x 1)
+# so y[h-block] = sum_g T_g c_{h,g} with T_g = Alg. 2 levels 1..d-s applied
+# to the block x[g-block] alone (Y_{d-s} of that block, open right bond).
+# Peak memory is two n x r buffers (n = N / 2^s), which is what lets c5
+# (N = 2^27, r = 24: 25.8 GB per full buffer) run on a modest host.
+# ---------------------------------------------------------------------------
+def top_projection(cores, s: int, h: int, g: int, dtype=np.float64):
+    """c_{h,g} = prod_{l=1..s} G_{d-s+l}(:, h_l, g_l, :), an r_{d-s}-vector
+    (h_l, g_l = bit l-1 of h, g)."""
+    d = len(cores)
+    c = np.eye(int(cores[d - s].shape[0]) if s else 1, dtype=dtype)
+    for l in range(s):
+        G = np.asarray(cores[d - s + l], dtype=dtype)
+        c = c @ G[:, (h >> l) & 1, (g >> l) & 1, :]
+    return c[:, 0]
+
+
+def apply_chunked(cores, x, s: int, dtype=np.float64):
+    """y = A x through 2^s top-bit blocks: Alg. 2 (``blas_sweep``) on each
+    block of x for levels 1..d-s, then the projections onto every output block."""
+    x = np.atleast_2d(np.asarray(x, dtype=dtype))
+    nrhs, N = x.shape
+    d = len(cores)
+    assert N == 1 << d and 0 <= s <= d
+    P, n = 1 << s, N >> s
+    low = list(cores[: d - s])
+    out = np.zeros((nrhs, N), dtype=dtype)
+    for t in range(nrhs):
+        for g in range(P):
+            T = blas_sweep(low, x[t, g * n:(g + 1) * n], dtype)     # [n][r_{d-s}]
+            for h in range(P):
+                out[t, h * n:(h + 1) * n] += T @ top_projection(cores, s, h, g, dtype)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Rank-1 (Kronecker) operators applied mode by mode: A = F_d (x) ... (x) F_1
+# (P:1226-1231 "Kronecker product"; SURVEY §8(c) pin P3).  With x reshaped to
+# (2,)*d in C order, axis 0 is digit d (MSB) and axis d-1 is digit 1 (LSB);
+# F_k acts on axis d-k.  O(N d) work: a closed form at any d that shares
+# nothing with Alg. 2.
+# ---------------------------------------------------------------------------
+def kron_apply_modes(factors, x, dtype=np.float64):
+    x = np.atleast_2d(np.asarray(x, dtype=dtype))
+    nrhs, N = x.shape
+    d = len(factors)
+    assert N == 1 << d
+    out = np.empty_like(x)
+    for t in range(nrhs):
+        Z = x[t].reshape((2,) * d) if d else x[t].reshape(())
+        for k, F in enumerate(factors, start=1):
+            ax = d - k
+            Z = np.moveaxis(np.tensordot(np.asarray(F, dtype=dtype), Z, axes=([1], [ax])), 0, ax)
+        out[t] = np.reshape(Z, N)
+    return out
+
+
+# ---------------------------------------------------------------------------
 # Sampled outputs: y[i] = sum_j A(i, j) x[j] for a few rows i, at any N.
 # With the row digits fixed, contract the source digits j_1, j_2, ... in turn:
 #   W_0[J, .] = x[J];  W_k[J', b] = sum_{j,a} W_{k-1}[j + 2 J', a] G_k[a, i_k, j, b]

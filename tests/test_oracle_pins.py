@@ -18,6 +18,9 @@ from qtt_workload import generate, random_case, flops_per_apply
 
 APPLIES = {
     "alg2": oracle.apply_alg2,
+    "blas": oracle.apply_blas_sweep,
+    "chunked1": lambda cores, x: oracle.apply_chunked(cores, x, min(1, len(cores))),
+    "chunked3": lambda cores, x: oracle.apply_chunked(cores, x, min(3, len(cores))),
     "bitwise": oracle.apply_bitwise,
     "dense": oracle.apply_dense,
     "rows": lambda cores, x: oracle.apply_rows(cores, x, np.arange(np.atleast_2d(x).shape[1])),
@@ -337,3 +340,163 @@ def test_morton_separable_function():
         y = sum(((q >> (3 * l + 1)) & 1) << l for l in range(lv))
         z = sum(((q >> (3 * l + 2)) & 1) << l for l in range(lv))
         assert xq[q] == f[x] * g[y] * h[z]
+
+
+# --- the BLAS sweep and the chunked sweep: their own plausible mistakes are caught ----------
+def _pins_hold(apply_fn):
+    """True iff every pin below holds for ``apply_fn``: shift bitwise (np.roll),
+    Kronecker against np.kron, and a random rank profile against the dense matrix."""
+    d = 6
+    x = np.random.default_rng(3).standard_normal((1, 1 << d))
+    if not np.array_equal(apply_fn(CF.shift_cores(d, 5), x)[0], np.roll(x[0], 5)):
+        return False
+    rng = np.random.default_rng(5)
+    F = [rng.standard_normal((2, 2)) for _ in range(d)]
+    A = np.ones((1, 1))
+    for Fk in F:
+        A = np.kron(Fk, A)
+    if not np.allclose(apply_fn(CF.kron_cores(F), x), x @ A.T, rtol=1e-12, atol=1e-13):
+        return False
+    _, cores, xr = random_case(9, d, 4)
+    return bool(np.allclose(apply_fn(cores, xr), oracle.apply_dense(cores, xr), rtol=1e-12, atol=1e-13))
+
+
+_orig_mt_half = Q._mt_half
+_orig_top = Q.top_projection
+
+
+def _mut_mt_swap_ij(G, i, dtype):
+    return _orig_mt_half(np.ascontiguousarray(G.transpose(0, 2, 1, 3)), i, dtype)
+
+
+def _mut_mt_merge_order(G, i, dtype):          # column merge as j + 2 alpha instead of alpha + r j
+    return np.ascontiguousarray(np.asarray(G[:, i, :, :], dtype=dtype).reshape(2 * G.shape[0], G.shape[3]))
+
+
+def _mut_top_swap_hg(cores, s, h, g, dtype=np.float64):
+    return _orig_top(cores, s, g, h, dtype)
+
+
+def _mut_top_msb_first(cores, s, h, g, dtype=np.float64):
+    rev = lambda v: sum(((v >> l) & 1) << (s - 1 - l) for l in range(s))
+    return _orig_top(cores, s, rev(h), rev(g), dtype)
+
+
+@pytest.mark.parametrize("name,mut,fn", [
+    ("_mt_half", _mut_mt_swap_ij, "blas"),
+    ("_mt_half", _mut_mt_merge_order, "blas"),
+    ("top_projection", _mut_top_swap_hg, "chunked3"),
+    ("top_projection", _mut_top_msb_first, "chunked3"),
+])
+def test_pins_catch_sweep_mutations(monkeypatch, name, mut, fn):
+    assert _pins_hold(APPLIES[fn])
+    monkeypatch.setattr(Q, name, mut)
+    assert not _pins_hold(APPLIES[fn])
+
+
+@pytest.mark.parametrize("d,s", [(5, 0), (5, 2), (5, 5), (9, 4), (12, 3)])
+def test_chunked_equals_alg2_dense(d, s):
+    _, cores, x = random_case(60 + d + s, d, 6, nrhs=2)
+    ref = oracle.apply_dense(cores, x)
+    oracle.assert_close(oracle.apply_chunked(cores, x, s), ref, l2_tol=1e-13)
+    oracle.assert_close(oracle.apply_blas_sweep(cores, x), ref, l2_tol=1e-13)
+
+
+# --- Kronecker operators applied mode by mode (P3 at any d) --------------------------------
+@pytest.mark.parametrize("d", [0, 1, 4, 7, 10])
+def test_kron_modes_equals_np_kron(d):
+    rng = np.random.default_rng(200 + d)
+    F = [rng.standard_normal((2, 2)) for _ in range(d)]
+    A = np.ones((1, 1))
+    for Fk in F:              # F_1 innermost (fastest digit)
+        A = np.kron(Fk, A)
+    x = rng.standard_normal((2, 1 << d))
+    np.testing.assert_allclose(oracle.kron_apply_modes(F, x), x @ A.T, rtol=1e-12, atol=1e-13)
+
+
+def test_kron_modes_hadamard_and_permutation():
+    d = 11
+    H2 = np.array([[1.0, 1.0], [1.0, -1.0]])
+    x = np.random.default_rng(4).integers(-5, 6, (1, 1 << d)).astype(float)
+    # integer data: the Walsh-Hadamard transform is exact, compare bitwise
+    np.testing.assert_array_equal(oracle.kron_apply_modes([H2] * d, x),
+                                  x @ scipy.linalg.hadamard(1 << d).T.astype(float))
+    # swap matrix on digit k only: y[i] = x[i xor 2^(k-1)]
+    X2 = np.array([[0.0, 1.0], [1.0, 0.0]])
+    for k in (1, 5, d):
+        F = [np.eye(2)] * d
+        F = F[:k - 1] + [X2] + F[k:]
+        np.testing.assert_array_equal(oracle.kron_apply_modes(F, x)[0], x[0][np.arange(1 << d) ^ (1 << (k - 1))])
+
+
+def test_kron_modes_agrees_with_sweeps_large():
+    d = 16
+    rng = np.random.default_rng(17)
+    F = [rng.standard_normal((2, 2)) / 1.3 for _ in range(d)]
+    x = rng.standard_normal((1, 1 << d))
+    ref = oracle.kron_apply_modes(F, x)
+    cores = CF.kron_cores(F)
+    oracle.assert_close(oracle.apply_blas_sweep(cores, x), ref, l2_tol=1e-13)
+    oracle.assert_close(oracle.apply_chunked(cores, x, 4), ref, l2_tol=1e-13)
+
+
+# --- TT vectors of rank > 1: an exact closed form, and the compressed matvec ----------------
+def _linear_tt(d, a, b):
+    """Exact rank-2 TT vector of v[i] = a + b i (i = sum_k i_k 2^{k-1}): the bond
+    carries (running sum, 1)."""
+    cores = []
+    for k in range(d):
+        w = float(b) * (1 << k)
+        if d == 1:
+            H = np.array([[[a], [a + w]]])                       # (1, 2, 1)
+        elif k == 0:
+            H = np.zeros((1, 2, 2))
+            for i in (0, 1):
+                H[0, i] = [1.0, a + w * i]
+        elif k == d - 1:
+            H = np.zeros((2, 2, 1))
+            for i in (0, 1):
+                H[:, i, 0] = [w * i, 1.0]
+        else:
+            H = np.zeros((2, 2, 2))
+            for i in (0, 1):
+                H[:, i, :] = [[1.0, w * i], [0.0, 1.0]]
+        cores.append(H)
+    return cores
+
+
+@pytest.mark.parametrize("d", [1, 2, 9])
+def test_tt_vector_linear_closed_form(d):
+    cores = _linear_tt(d, 3.0, -2.0)
+    ref = 3.0 - 2.0 * np.arange(1 << d, dtype=float)
+    np.testing.assert_array_equal(oracle.tt_vector_dense(cores), ref)
+    idx = np.arange(1 << d)
+    np.testing.assert_array_equal(oracle.tt_vector_entries(cores, idx), ref)
+
+
+def _mut_compressed_right_bond(A_cores, b_cores):
+    out = []
+    for GA, Gb in zip(A_cores, b_cores):
+        C = np.einsum("aijc,bjd->abidc", GA, Gb)       # right bond merged as (beta', alpha')
+        out.append(C.reshape(GA.shape[0] * Gb.shape[0], 2, GA.shape[3] * Gb.shape[2]))
+    return out
+
+
+@pytest.mark.parametrize("seed,d,ra,rb", [(1, 8, 5, 2), (2, 9, 4, 4), (3, 7, 3, 6)])
+def test_compressed_matvec_rank_gt1(seed, d, ra, rb):
+    """c = A b in QTT form for a TT vector b of rank up to rb > 1:
+    its dense form equals Alg. 2 applied to the dense b; the (beta', alpha')
+    mutant of the right-bond merge fails the same check."""
+    from qtt_workload import random_tt_vector
+    _, A, _ = random_case(seed, d, ra)
+    _, bc = random_tt_vector(seed + 50, d, rb)
+    assert max(H.shape[2] for H in bc[:-1]) > 1
+    bdense = oracle.tt_vector_dense(bc)
+    ref = oracle.apply_dense(A, bdense)
+    oracle.assert_close(oracle.tt_vector_dense(oracle.compressed_matvec(A, bc))[None], ref, l2_tol=1e-13)
+    m = oracle.compare(oracle.tt_vector_dense(_mut_compressed_right_bond(A, bc))[None], ref)[0]
+    assert m["rel_l2"] > 1e-3
+    # the linear vector: A (a + b i) computed through the compressed matvec
+    lin = _linear_tt(d, 0.5, 0.25)
+    oracle.assert_close(oracle.tt_vector_dense(oracle.compressed_matvec(A, lin))[None],
+                        oracle.apply_dense(A, 0.5 + 0.25 * np.arange(1 << d)), l2_tol=1e-13)
