@@ -9,9 +9,11 @@ resident in HBM.  Every buffer exceeds L2 (x 128 MiB; intermediates up to
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
 
-Multi-GPU (--gpus N, launched by torchrun): N independent replicas (weak
-scaling, no data-path collective).  Rank 0 prints ONE
-JSON line.
+Multi-GPU (--gpus N, launched by torchrun): for a single-RHS config (c4) one
+apply is sharded over the N GPUs by the top index bits with one NCCL
+reduce-scatter (strong scaling); multi-RHS configs
+(or --mode replicas) run N independent replicas (weak scaling, no data-path
+collective).  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -168,29 +170,67 @@ def dist_barrier(world: int):
 
 
 # --------------------------------------------------------------------------- helpers
-def config_desc(cfg, nrhs):
+def resolve_mode(args, nrhs: int) -> str:
+    """Multi-GPU mode: one apply sharded by the top index bits (SURVEY 8(e),
+    strong scaling) for single-RHS configs, independent replicas otherwise;
+    --mode overrides."""
+    if args.mode is not None:
+        return args.mode
+    return "sharded" if nrhs == 1 else "replicas"
+
+
+def parallelism_desc(mode: str, world: int, exchange: str = "nccl") -> str:
+    if world <= 1:
+        return "single GPU"
+    if mode == "sharded":
+        return (f"top-bit shards x{world} + "
+                + ("fused peer-store exchange" if exchange == "fused" else "NCCL reduce-scatter"))
+    return f"replicas x{world} (independent problems, no data-path collective)"
+
+
+def config_desc(cfg, nrhs, parallelism="single GPU"):
+    """The workload description; both arms (ours and --impl reference) print
+    exactly this dict for the same arguments."""
     prof = "tapered r_k=min(2^k,2^(d-k),48)" if cfg.name == "c4" else f"r={max(cfg.ranks)}"
     return {"workload": f"{cfg.name}: QTT apply d={cfg.d} N=2^{cfg.d} {prof}, nrhs={nrhs}, seed {cfg.seed}",
             "d": cfg.d, "N": cfg.N, "nrhs": nrhs, "max_rank": max(cfg.ranks),
             "x_dist": cfg.x_dist, "stands_for": cfg.stands_for,
             "l2": "no flush: inputs larger than L2 (x %d MiB, intermediates up to %.1f GB)"
                   % (cfg.N * nrhs * 8 >> 20, max(cfg.ranks[1:-1] or [1]) * cfg.N * nrhs * 8 / 1e9),
-            "parallelism": "replicas"}
+            "parallelism": parallelism}
 
 
-def oracle_sample(cores, x, cfg, s_bits: int):
-    """Bounded CPU sample of the same workload: Alg. 2 levels 1..d-s on the first
-    of 2^s top-bit blocks of x (these levels never mix blocks)."""
+# host buffers of the oracle's sweep above this size switch it to the chunked
+# variant (top-bit blocks; same result, SURVEY 8(c) oracle 4): c5 only
+ORACLE_BUFFER_LIMIT = 8 << 30
+
+
+def oracle_whole_apply(cores, x, cfg):
+    """One whole apply by the CPU oracle, as it stands: Alg. 2 with BLAS calls
+    (oracle.apply_blas_sweep, SURVEY 8(c) oracle 3), or its chunked form when
+    one intermediate buffer would exceed ORACLE_BUFFER_LIMIT.  Returns
+    (seconds, description)."""
     import oracle
-    d = cfg.d
-    n = cfg.N >> s_bits
-    sub = cores[: d - s_bits]
-    ranks = cfg.ranks
-    flops = 4 * sum(ranks[k] * ranks[k + 1] for k in range(d - s_bits)) * n
+    rmax = max(cfg.ranks)
+    s = 0
+    while (cfg.N >> s) * rmax * 8 > ORACLE_BUFFER_LIMIT:
+        s += 1
     t0 = time.perf_counter()
-    oracle.alg2_sweep(sub, x[0, :n])
-    dt = time.perf_counter() - t0
-    return flops, dt
+    if s == 0:
+        oracle.apply_blas_sweep(cores, x)
+        what = "oracle.apply_blas_sweep (Alg. 2, two numpy matmul(out=half) per level)"
+    else:
+        oracle.apply_chunked(cores, x, s)
+        what = f"oracle.apply_chunked (Alg. 2 BLAS sweep per 2^{s} top-bit blocks + projections)"
+    return time.perf_counter() - t0, what
+
+
+def oracle_warm_sample(cores, x, cfg, s_bits=3):
+    """Untimed warm-up of the oracle: Alg. 2 levels 1..d-s on the first of 2^s
+    top-bit blocks of x (these levels never mix blocks)."""
+    import oracle
+    n = cfg.N >> s_bits
+    oracle.blas_sweep(cores[: cfg.d - s_bits], x[0, :n])
 
 
 def blas_threads():
@@ -202,30 +242,24 @@ def blas_threads():
         return os.cpu_count() or 1, []
 
 
-def run_cpu_baseline(cfg, cores, x, budget_s=20.0, s_bits=None):
-    """Time the oracle (as it stands) on a bounded sample; returns a dict.
-    With s_bits given, that sample (1 of 2^s_bits top-bit blocks) is timed once;
-    else the sample grows from 1/8 toward ~budget_s of CPU work."""
-    if s_bits is not None:
-        flops, dt = oracle_sample(cores, x, cfg, s_bits)
-    else:
-        s_bits = 3
-        flops, dt = oracle_sample(cores, x, cfg, s_bits)
-        while dt * 2 < budget_s and s_bits > 1:
-            s_bits -= 1
-            flops, dt = oracle_sample(cores, x, cfg, s_bits)
+def run_cpu_baseline(cfg, cores, x):
+    """Time the oracle (as it stands) on ONE WHOLE APPLY of the workload (all d
+    levels, every entry of x; ~10-20 s of CPU work at c4): no sampling and no
+    extrapolation."""
+    dt, what = oracle_whole_apply(cores, x, cfg)
+    F = 4 * sum(cfg.ranks[k] * cfg.ranks[k + 1] for k in range(cfg.d)) * cfg.N * cfg.nrhs
     threads, apis = blas_threads()
-    return {"value": flops / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"oracle.alg2_sweep (Alg. 2, numpy/BLAS) over levels 1..{cfg.d - s_bits} on 1 of "
-                      f"2^{s_bits} top-bit blocks of x ({flops / 1e9:.1f} GFLOP, {dt:.1f} s)",
-            "seconds": dt, "s_bits": s_bits, "blas": apis, "host_cpus": os.cpu_count(), "affinity_cpus": _affinity(),
-            "cpu_model": _cpu_model()}
+    return {"value": F / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"one whole {cfg.name} apply ({F / 1e9:.0f} GFLOP, all {cfg.d} levels, {cfg.N} x "
+                      f"{cfg.nrhs} entries): {what}, {dt:.2f} s",
+            "seconds": dt, "ms_per_apply": dt * 1e3, "blas": apis, "host_cpus": os.cpu_count(),
+            "affinity_cpus": _affinity(), "cpu_model": _cpu_model()}
 
 
 def small_config_oracle_ms(threads=None):
-    """cpu_baseline leg: the oracle's Alg. 2 sweep timed on c1, c2, c3 (whole
-    applies); threads=1 limits BLAS to one thread (comparable to
-    the paper's serial Xeon)."""
+    """cpu_baseline leg: the same oracle timed on c1, c2, c3 (whole applies);
+    threads=1 limits BLAS to one thread (comparable to the
+    paper's serial Xeon)."""
     import contextlib
     import oracle
     from qtt_workload import generate
@@ -240,9 +274,13 @@ def small_config_oracle_ms(threads=None):
     with ctx:
         for name in ("c1", "c2", "c3"):
             _, cores, x = generate(name)
-            t0 = time.perf_counter()
-            oracle.apply_alg2(cores, x)
-            out[name] = (time.perf_counter() - t0) * 1e3
+            oracle.apply_blas_sweep(cores, x)            # warm-up
+            ts = []
+            for _ in range(3 if name != "c3" else 1):
+                t0 = time.perf_counter()
+                oracle.apply_blas_sweep(cores, x)
+                ts.append((time.perf_counter() - t0) * 1e3)
+            out[name] = statistics.median(ts)
     return out
 
 
@@ -532,42 +570,64 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
 
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    """The reference arm: the CPU oracle as it stands (no reference code exists;
+    the paper ships none), on the host cores of rank 0.  Every timed step is
+    one WHOLE apply of the workload (oracle_whole_apply); warm-up steps run a
+    1/8 top-bit sample (untimed).  Under torchrun only rank 0 runs."""
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from qtt_workload import generate
     cfg, cores, x = generate(args.config)
     nrhs = cfg.nrhs
-    vals = []
-    cb = None
-    # size the sample once (the first warm-up), then time the same sample every
-    # step; the per-step budget shrinks with the step count so the whole run
-    # stays within ~3 minutes of CPU time
-    budget = min(args.ref_budget, 180.0 / max(1, args.warmup + args.steps))
-    s_bits = None
-    for it in range(args.warmup + args.steps):
-        c = run_cpu_baseline(cfg, cores, x, budget_s=budget, s_bits=s_bits)
-        s_bits = c["s_bits"]
-        if it >= args.warmup:
-            vals.append(c["value"])
-            cb = c
-    v = statistics.median(vals)
+    for _ in range(args.warmup):
+        oracle_warm_sample(cores, x, cfg)
+    secs = []
+    what = None
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        dt, what = oracle_whole_apply(cores, x, cfg)
+        secs.append(dt)
+    wall = time.perf_counter() - wall0
     total_flops = 4 * sum(cfg.ranks[k] * cfg.ranks[k + 1] for k in range(cfg.d)) * cfg.N * nrhs
+    ms_step = statistics.median(secs) * 1e3
+    v = total_flops / (ms_step * 1e-3) / 1e9
+    threads, _ = blas_threads()
+    mode = resolve_mode(args, nrhs)
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_flops / (v * 1e9) * 1e3,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded; random cores with the config's rank profile)",
-           "config": config_desc(cfg, nrhs),
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
-                            "sample": cb["sample"]},
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+           "higher_is_better": True, "scaling": "strong" if mode == "sharded" else "weak",
+           "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded; random cores with the config's rank profile stand in for the paper's inverse cores)",
+           "config": config_desc(cfg, nrhs, parallelism_desc(mode, world, args.exchange)),
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": f"every timed step is one whole {cfg.name} apply: {what}; "
+                                      f"warm-up steps: levels 1..{cfg.d - 3} on 1/8 of x (untimed)"},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "note": "ms_per_step extrapolates the sampled rate to one full apply"}
+           "timed_wall_s": wall, "step_seconds": secs,
+           "note": "the oracle runs on rank 0's host cores only; ms_per_step is the median measured whole apply"}
     print(json.dumps(out))
     return 0
 
 
 # --------------------------------------------------------------------------- our arm
+def comm_info(world: int):
+    """The communicator the data-path collective runs on (checkable: its size
+    must equal n_gpus)."""
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    info = {"backend": dist.get_backend(), "world_size": dist.get_world_size()}
+    try:
+        import torch
+        if info["backend"] == "nccl":
+            info["nccl_version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+    except Exception:
+        pass
+    return info
+
+
 def run_sharded(args, world, rank, local, dev, cfg, cores, x_np):
     """One apply of the config sharded over `world` GPUs by the top index bits:
     each rank runs its shard plan on its block, then one sum reduce-scatter
@@ -617,8 +677,8 @@ def run_sharded(args, world, rank, local, dev, cfg, cores, x_np):
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded; random cores with the config's rank profile)",
-           "config": dict(config_desc(cfg, nrhs), parallelism=f"top-bit shards x{world} + "
-                          + ("fused peer-store exchange" if args.exchange == "fused" else "NCCL reduce-scatter")),
+           "config": config_desc(cfg, nrhs, parallelism_desc("sharded", world, args.exchange)),
+           "comm": comm_info(world),
            "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                    "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8)},
            # stages (+ split-K reduce launches), + the slot reduction of the fused exchange
@@ -649,9 +709,10 @@ def main(argv=None):
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
                     help="sharded mode: NCCL reduce-scatter of a send buffer, or the fused projection "
                          "storing into the other GPUs' receive buffers (CUDA IPC over NVLink)")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
-                    help="N>1: independent replicas (weak scaling, default) or one apply sharded by the "
-                         "top index bits with one NCCL reduce-scatter (strong scaling; DESIGN.md 9)")
+    ap.add_argument("--mode", default=None, choices=["replicas", "sharded"],
+                    help="N>1: one apply sharded by the top index bits with one NCCL reduce-scatter "
+                         "(strong scaling; DESIGN.md 9; the default for single-RHS configs) or independent "
+                         "replicas (weak scaling; the default for multi-RHS configs)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
@@ -668,7 +729,8 @@ def main(argv=None):
 
     cfg, cores, x_np = generate(args.config)
     nrhs = cfg.nrhs
-    if args.mode == "sharded" and world > 1:
+    mode = resolve_mode(args, nrhs)
+    if mode == "sharded" and world > 1:
         return run_sharded(args, world, rank, local, dev, cfg, cores, x_np)
     op = q.QttOperator(cores, max_stage_levels=args.max_stage_levels)
     x = torch.from_numpy(x_np).to(dev)
@@ -745,6 +807,12 @@ def main(argv=None):
                 "peak_source": fp64_src + "; MEASURED_PEAKS.json has no FP64 figure",
                 "algorithmic_flops_per_launch": dom_flops,
                 "traffic_source": tr[1] if tr else None}
+    # the whole step on the executed-flop basis, next to the Alg. 2-basis `value`
+    # (reading R16: merged boundary stages execute fewer flops than Alg. 2)
+    exec_flops = sum(rr["flops_executed"] for rr in stage_rows)
+    roofline["step_tflops_executed"] = exec_flops / (ms_step * 1e-3) / 1e12
+    roofline["step_frac_executed"] = roofline["step_tflops_executed"] / fp64
+    roofline["step_tflops_alg2"] = flops_step / (ms_step * 1e-3) / 1e12
     per_stage = {"frac": sum_T / sum_t if sum_t else None, "sum_T_ms": sum_T * 1e3, "sum_t_ms": sum_t * 1e3,
                  "fp64_peak_tflops": fp64, "hbm_gbs": hbm, "hbm_source": hbm_src,
                  "frac_vs_nominal_fp64": None, "stages": stage_rows}
@@ -779,7 +847,7 @@ def main(argv=None):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = run_cpu_baseline(cfg, cores, x_np, budget_s=20.0)
+        cpu = run_cpu_baseline(cfg, cores, x_np)
         cpu.pop("seconds", None)
         # the same CPU baseline (the oracle, all host cores) on the small configs, whole applies
         cpu["other_configs_ms"] = small_config_oracle_ms()
@@ -788,11 +856,13 @@ def main(argv=None):
     clocks = clk.summary()
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if mode == "sharded" else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; random cores with the config's rank profile stand in for the paper's inverse cores)",
-        "config": dict(config_desc(cfg, nrhs), launches_per_apply=op.launches_per_apply,
-                       stages=[[st["k_first"], st["k_last"]] for st in stages]),
+        "config": config_desc(cfg, nrhs, parallelism_desc(mode, world, args.exchange)),
+        "plan": {"launches_per_apply": op.launches_per_apply,
+                 "stages": [[st["k_first"], st["k_last"], st["variant"]] for st in stages]},
         "gbs": (16 * N * nrhs) / (ms_step * 1e-3) / 1e9,
         "value_basis": "Alg. 2 flops (4*sum_k r_{k-1} r_k * N * nrhs, reading R4) per second; the boundary "
                        "stages apply exact super-cores with fewer flops (DESIGN.md 6.4), so value may exceed "

@@ -91,10 +91,12 @@ class QttShard:
         _lib.check("qtt_workspace_size", _lib.load().qtt_workspace_size(self._h, int(nrhs), C.byref(b)))
         return int(b.value)
 
-    def stages(self):
-        from . import qtt_get_info, qtt_get_stage
+    def stages(self, nrhs: int = 1):
+        """Per launch: {'k_first', 'k_last', 'variant', 'ksplit'} (the last stage
+        is the projection)."""
+        from . import qtt_get_info, qtt_get_stage, qtt_get_stage_split
         n = qtt_get_info(self._h)["launches_per_apply"]
-        return [qtt_get_stage(self._h, i) for i in range(n)]
+        return [dict(qtt_get_stage(self._h, i), ksplit=qtt_get_stage_split(self._h, i, nrhs)) for i in range(n)]
 
     def apply(self, x_local, send=None, stream=None, workspace=None):
         import torch
@@ -258,7 +260,11 @@ class ShardedQttOperator:
             return self._apply_fused(x_local, out, stream)
         send = self.local_apply(x_local, send=send, stream=stream, workspace=workspace)
         y = torch.empty((send.shape[0], self.n), dtype=torch.float64, device=send.device) if out is None else out
-        exchange(send, y.view(send.shape[0], self.n), self.group)
+        # the collective runs on the stream the shard kernels were enqueued on
+        # (torch.distributed issues NCCL work on the current stream)
+        st = torch.cuda.current_stream(send.device) if stream is None else stream
+        with torch.cuda.stream(st):
+            exchange(send, y.view(send.shape[0], self.n), self.group)
         return y if x_local.dim() == 2 else y.view(-1)
 
     def _apply_fused(self, x_local, out, stream):

@@ -64,8 +64,8 @@ def test_reference_arm_line():
     contract line: impl, metric/unit of our arm, cpu_baseline, e2e."""
     import subprocess
     import sys
-    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1",
-                        "--ref-budget", "1"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1",
+                        "--config", "c3"], cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
@@ -73,3 +73,24 @@ def test_reference_arm_line():
     assert d["impl"] == "reference" and d["unit"] == bench.UNIT and d["metric"] == bench.METRIC
     assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    # every timed step is one whole apply (no extrapolation): ms_per_step is the
+    # median measured step, and the timed steps fit in the measured wall time
+    assert len(d["step_seconds"]) == 2
+    assert d["ms_per_step"] * 1e-3 <= d["timed_wall_s"]
+    assert "whole c3 apply" in d["cpu_baseline"]["sample"]
+    # the same config dict our arm prints for the same arguments
+    from qtt_workload.configs import make_config
+    assert d["config"] == bench.config_desc(make_config("c3"), 1, "single GPU")
+    assert d["scaling"] == "strong"      # single-RHS config: the multi-GPU mode is top-bit sharding
+
+
+def test_multi_gpu_mode_defaults():
+    import argparse
+    a = argparse.Namespace(mode=None, exchange="nccl")
+    assert bench.resolve_mode(a, 1) == "sharded"
+    assert bench.resolve_mode(a, 16) == "replicas"
+    a.mode = "replicas"
+    assert bench.resolve_mode(a, 1) == "replicas"
+    assert bench.parallelism_desc("sharded", 2) == "top-bit shards x2 + NCCL reduce-scatter"
+    assert bench.parallelism_desc("sharded", 1) == "single GPU"
+    assert bench.parallelism_desc("replicas", 4).startswith("replicas x4")

@@ -1,0 +1,115 @@
+"""Full-vector GPU parity at BASELINE.json's full sizes (north_star: "GPU
+results must match the oracle ... on all five configs").
+
+Every entry of y is compared, per RHS column, with the CPU oracle through
+``oracle.compare`` (rel. l2 <= 1e-12, RMS-floored elementwise <= 1e-10,
+reading R11).  The oracle variants used here are pinned in
+``tests/test_oracle_pins.py``:
+  * ``apply_blas_sweep``: Alg. 2 with BLAS calls (c3, c3x16, c4);
+  * ``apply_chunked``: Alg. 2 per top-bit block + the top-digit projections
+    (SURVEY §8(c) oracle 4) for c5, whose full intermediate
+    (25.8 GB per buffer) would not fit a modest host;
+  * ``kron_apply_modes``: the closed form of a Kronecker operator, applied
+    mode by mode in O(N d) (SURVEY §8(c) pin P3), at d = 24, 27.
+The GPU side runs the same launch configuration ``bench.py`` times (the
+default stage plan through ``QttOperator.apply``).  Metrics are printed and,
+when ``QTT_PARITY_LOG`` names a file, appended to it as JSON lines.
+"""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import oracle
+from qtt_workload import closed_forms as CF
+from qtt_workload import generate
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def qtt():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    import paper_1511_06029_b200 as q
+    q._lib.load()
+    return q
+
+
+def _gpu_apply(q, cores, x):
+    op = q.QttOperator(cores)
+    try:
+        xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        y = op.apply(xt)
+        torch.cuda.synchronize()
+        stages = op.stages()
+        out = y.cpu().numpy()
+        del xt, y
+    finally:
+        op.close()
+        torch.cuda.empty_cache()
+    return out, stages
+
+
+def _log(name, metrics, oracle_s, stages):
+    rec = {"case": name, "oracle_s": round(oracle_s, 2),
+           "stages": [[s["k_first"], s["k_last"], s["variant"]] for s in stages],
+           "columns": [{k: v for k, v in m.items()} for m in metrics]}
+    worst = {"rel_l2": max(m["rel_l2"] for m in metrics),
+             "elem_floor": max(m["elem_floor"] for m in metrics),
+             "raw_elem_max": max(m["raw_elem_max"] for m in metrics),
+             "raw_offenders": sum(m["raw_offenders"] for m in metrics)}
+    rec["worst"] = worst
+    print(f"\n[full parity] {name}: {json.dumps(worst)} (oracle {oracle_s:.1f} s)")
+    path = os.environ.get("QTT_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
+def _check(name, y, ref, oracle_s, stages):
+    assert y.shape == ref.shape
+    metrics = oracle.compare(y, ref)
+    _log(name, metrics, oracle_s, stages)
+    oracle.assert_close(y, ref)
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_full_vector_blas_oracle(qtt, name):
+    cfg, cores, x = generate(name)
+    y, stages = _gpu_apply(qtt, cores, x)
+    t = time.perf_counter()
+    ref = oracle.apply_blas_sweep(cores, x)
+    _check(name, y, ref, time.perf_counter() - t, stages)
+
+
+def test_full_vector_c3x16_all_columns(qtt):
+    cfg, cores, x = generate("c3x16")
+    y, stages = _gpu_apply(qtt, cores, x)
+    t = time.perf_counter()
+    ref = oracle.apply_blas_sweep(cores, x)
+    _check("c3x16", y, ref, time.perf_counter() - t, stages)
+
+
+def test_full_vector_c5_chunked_oracle(qtt):
+    cfg, cores, x = generate("c5")
+    y, stages = _gpu_apply(qtt, cores, x)
+    t = time.perf_counter()
+    ref = oracle.apply_chunked(cores, x, 2)      # 4 top-bit blocks: two 6.4 GB host buffers
+    _check("c5", y, ref, time.perf_counter() - t, stages)
+
+
+@pytest.mark.parametrize("d", [24, 27])
+def test_full_vector_kronecker_modes(qtt, d):
+    """A = F_d (x) ... (x) F_1 with random 2x2 factors, applied by the library
+    (rank-1 QTT) and mode by mode on the host (closed form), full vector."""
+    rng = np.random.default_rng(900 + d)
+    F = [rng.standard_normal((2, 2)) / 1.2 for _ in range(d)]
+    x = rng.standard_normal((1, 1 << d))
+    y, stages = _gpu_apply(qtt, CF.kron_cores(F), x)
+    t = time.perf_counter()
+    ref = oracle.kron_apply_modes(F, x)
+    _check(f"kron_d{d}", y, ref, time.perf_counter() - t, stages)
