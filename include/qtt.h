@@ -23,9 +23,12 @@
  *
  * Semantics: y = A x up to fp64 rounding (IEEE binary64, FMA contraction,
  * no reduced precision).  NaN/Inf propagate per IEEE; nothing is checked.
- * Results are bitwise deterministic for a fixed (handle, nrhs): no split-K
- * and no atomic accumulation (the one atomic, the dynamic tile scheduler,
- * decides only which SM computes a tile, never the order of its arithmetic).
+ * Results are bitwise deterministic run to run, and each RHS column is
+ * bitwise the same whatever nrhs it is applied with: there is no atomic
+ * accumulation (the one atomic, the dynamic tile scheduler, decides only which
+ * SM computes a tile, never the order of its arithmetic), and a split-K stage
+ * (qtt_get_stage_split) sums its partial products in a fixed k-range order in
+ * a separate launch, with the split fixed per plan.
  * No exceptions cross this boundary; every entry point returns a qtt_status_t.
  * Threading: a handle (its cached workspace, graphs and staging buffers) must
  * not be used by several host threads at once; separate handles are independent.
@@ -116,12 +119,19 @@ qtt_status_t qtt_plan_stages_split(int d, const int64_t* ranks, size_t smem_opti
  *   x, y  : DEVICE pointers (on the handle's device) owned by the caller, column-major N x nrhs,
  *           16-byte aligned; the ranges [x, x+N*nrhs) and [y, y+N*nrhs)
  *           must not overlap (in-place is impossible, reading R13).
- *   nrhs  : number of right-hand sides, >= 1, with N * nrhs <= 2^31
- *           (QTT_ERROR_NOT_SUPPORTED beyond: 32-bit TMA row coordinates).
+ *   nrhs  : number of right-hand sides, >= 1 (N * nrhs <= 2^60).  Every launch
+ *           covers at most 2^31 GEMM rows (32-bit TMA row coordinates), so
+ *           an apply with N * nrhs > 2^31 runs as consecutive groups of
+ *           2^31 / N right-hand sides; qtt_apply also lowers the group while
+ *           the group's workspace would not fit in the free device memory.
+ *           Columns are independent, so results do not depend on the grouping.
  * Argument errors return synchronously and enqueue nothing.  The handle
- * keeps a cached workspace of qtt_workspace_size() bytes, allocated on first
- * use with cudaMallocAsync on `stream`; concurrent applies on one handle
- * from different streams must use qtt_apply_ws instead.  No host sync.
+ * keeps a cached workspace (at most qtt_workspace_size(h, nrhs) bytes),
+ * allocated on first use with cudaMallocAsync on `stream`; it grows when a
+ * later apply needs more, the old block being released stream-ordered after
+ * its last user.  Applies on one handle from different streams are ordered one
+ * after another through the workspace's event (no host sync); for
+ * concurrent applies use qtt_apply_ws with one workspace per stream.
  * CUDA graph capture of `stream` is supported once the cached workspace
  * exists for this nrhs (apply once outside the capture, or use qtt_apply_ws);
  * otherwise QTT_ERROR_NOT_SUPPORTED.  Work captured into the caller's graph
@@ -143,8 +153,10 @@ qtt_status_t qtt_stage_super_core(int d, const int64_t* ranks, const double* con
                                   int k_last, double* W);
 
 /* Bytes of device workspace one apply with `nrhs` right-hand sides needs
- * (256 bytes of scheduler counters plus two ping-pong buffers of max
- * stage-boundary rank * N * nrhs doubles; absent for a one-stage plan). */
+ * (256 bytes of scheduler counters, two ping-pong buffers of max
+ * stage-boundary rank * N * g doubles -- absent for a one-stage plan -- and
+ * the split-K partials, where g = min(nrhs, 2^31 / N) is the launch group
+ * of qtt_apply_ws, see qtt_apply).  Shard handles: g = nrhs. */
 qtt_status_t qtt_workspace_size(qtt_handle_t h, int64_t nrhs, size_t* bytes);
 
 /* qtt_apply with caller-owned DEVICE workspace `ws` of `ws_bytes` >= the

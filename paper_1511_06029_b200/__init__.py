@@ -353,7 +353,14 @@ class QttOperator:
         if x.ndim not in (1, 2) or x.shape[-1] != self.N:
             raise ValueError(f"x must have shape (N,) or (nrhs, N) with N={self.N}")
         nrhs = 1 if x.ndim == 1 else x.shape[0]
-        y = np.empty_like(x) if out is None else out
+        if out is None:
+            y = np.empty_like(x)
+        else:
+            # the C side writes N * nrhs doubles at out's data pointer
+            if (not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.shape != x.shape
+                    or not out.flags.c_contiguous or not out.flags.writeable):
+                raise ValueError(f"out must be a writeable C-contiguous float64 array of shape {x.shape}")
+            y = out
         qtt_apply_host(self.handle, x, y, nrhs, stream)
         return y
 

@@ -215,28 +215,11 @@ qtt_status_t qtt_shard_apply(qtt_handle_t h, const double* x_local, double* send
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   try {
     DeviceGuard g(h->device);
-    const size_t need = ws_bytes_for(h, nrhs);
     const bool capturing = stream_is_capturing(st);
-    // a workspace allocated inside a graph capture would belong to that graph
-    if (capturing && need > h->ws_bytes) return QTT_ERROR_NOT_SUPPORTED;
-    if (need > h->ws_bytes) {
-      if (h->ws) cudaFreeAsync(h->ws, h->ws_stream);
-      h->ws = nullptr;
-      h->ws_bytes = 0;
-      cudaError_t e = cudaMallocAsync(&h->ws, need, st);
-      if (e != cudaSuccess) {
-        h->ws = nullptr;
-        return from_cuda(e);
-      }
-      h->ws_bytes = need;
-      h->ws_stream = st;
-    }
-    qtt_status_t so = order_after_last(h, st);
+    qtt_status_t so = cached_acquire(&h->ws, &h->ws_bytes, &h->ws_used, h->ws_pending, ws_bytes_for(h, nrhs), st,
+                                     capturing, nullptr);
     if (so == QTT_SUCCESS) so = enqueue(h, x_local, send, nrhs, h->ws, st);
-    if (so == QTT_SUCCESS && !capturing) {
-      h->last_stream = st;
-      h->has_last = true;
-    }
+    if (so == QTT_SUCCESS) so = cached_release(h->ws_used, &h->ws_pending, st, capturing);
     return so;
   } catch (...) {
     return QTT_ERROR_CUDA;
@@ -285,28 +268,11 @@ qtt_status_t qtt_shard_apply_fused(qtt_handle_t h, const double* x_local, int64_
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   try {
     DeviceGuard g(h->device);
-    const size_t need = ws_bytes_for(h, nrhs);
     const bool capturing = stream_is_capturing(st);
-    // a workspace allocated inside a graph capture would belong to that graph
-    if (capturing && need > h->ws_bytes) return QTT_ERROR_NOT_SUPPORTED;
-    if (need > h->ws_bytes) {
-      if (h->ws) cudaFreeAsync(h->ws, h->ws_stream);
-      h->ws = nullptr;
-      h->ws_bytes = 0;
-      cudaError_t e = cudaMallocAsync(&h->ws, need, st);
-      if (e != cudaSuccess) {
-        h->ws = nullptr;
-        return from_cuda(e);
-      }
-      h->ws_bytes = need;
-      h->ws_stream = st;
-    }
-    qtt_status_t so = order_after_last(h, st);
+    qtt_status_t so = cached_acquire(&h->ws, &h->ws_bytes, &h->ws_used, h->ws_pending, ws_bytes_for(h, nrhs), st,
+                                     capturing, nullptr);
     if (so == QTT_SUCCESS) so = enqueue(h, x_local, nullptr, nrhs, h->ws, st, true);
-    if (so == QTT_SUCCESS && !capturing) {
-      h->last_stream = st;
-      h->has_last = true;
-    }
+    if (so == QTT_SUCCESS) so = cached_release(h->ws_used, &h->ws_pending, st, capturing);
     return so;
   } catch (...) {
     return QTT_ERROR_CUDA;
@@ -388,23 +354,64 @@ qtt_status_t qtt_stage_super_core(int d, const int64_t* ranks, const double* con
   return QTT_SUCCESS;
 }
 
+// graphs captured on a released cached workspace are stale
+static void drop_graphs_on(qtt_plan* h, const void* old_ws) {
+  for (size_t i = h->graphs.size(); i-- > 0;)
+    if (h->graphs[i].ws == old_ws) {
+      cudaGraphExecDestroy(h->graphs[i].exec);
+      h->graphs.erase(h->graphs.begin() + i);
+    }
+}
+
 qtt_status_t qtt_workspace_size(qtt_handle_t h, int64_t nrhs, size_t* bytes) {
   if (!h || !bytes || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
-  *bytes = ws_bytes_for(h, nrhs);
+  *bytes = ws_bytes_for(h, h->shard_bits ? nrhs : rhs_group(h, nrhs));
   return QTT_SUCCESS;
+}
+
+// Enqueue y = A x for nrhs RHS as consecutive groups of `group` RHS sharing
+// one workspace (stream order serialises the groups).  One group replays the
+// cached CUDA graph; several use plain launches (a graph per group pointer
+// pair would only churn the cache at these sizes).
+static qtt_status_t enqueue_groups(qtt_plan* h, const double* x, double* y, int64_t nrhs, int64_t group, void* ws,
+                                   cudaStream_t st) {
+  if (group >= nrhs) return enqueue_graphed(h, x, y, nrhs, ws, st);
+  for (int64_t r0 = 0; r0 < nrhs; r0 += group) {
+    const int64_t g = std::min(group, nrhs - r0);
+    const size_t off = size_t(r0) * size_t(h->N);
+    const qtt_status_t s = enqueue(h, x + off, y + off, g, ws, st);
+    if (s != QTT_SUCCESS) return s;
+  }
+  return QTT_SUCCESS;
+}
+
+// RHS per group for an apply on the cached workspace: rhs_group, lowered
+// further while the workspace for the group would not fit in the device
+// memory free now (plus the cached block it replaces).
+static int64_t cached_group(qtt_plan* h, int64_t nrhs) {
+  int64_t g = rhs_group(h, nrhs);
+  if (ws_bytes_for(h, g) <= h->ws_bytes) return g;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    return g;
+  }
+  const double avail = 0.92 * double(free_b + h->ws_bytes);
+  while (g > 1 && double(ws_bytes_for(h, g)) > avail) g = (g + 1) / 2;
+  return g;
 }
 
 qtt_status_t qtt_apply_ws(qtt_handle_t h, const double* x, double* y, int64_t nrhs, void* ws,
                           size_t ws_bytes, qtt_stream_t stream) {
   qtt_status_t s = check_apply_args(h, x, y, nrhs);
   if (s != QTT_SUCCESS) return s;
-  const size_t need = ws_bytes_for(h, nrhs);
+  const size_t need = ws_bytes_for(h, rhs_group(h, nrhs));
   if (!ws || ws_bytes < need) return QTT_ERROR_INVALID_VALUE;
   if (reinterpret_cast<uintptr_t>(ws) % 256) return QTT_ERROR_NOT_SUPPORTED;
   if (!is_device_ptr(ws)) return QTT_ERROR_NOT_SUPPORTED;
   try {
     DeviceGuard g(h->device);
-    return enqueue_graphed(h, x, y, nrhs, ws, reinterpret_cast<cudaStream_t>(stream));
+    return enqueue_groups(h, x, y, nrhs, rhs_group(h, nrhs), ws, reinterpret_cast<cudaStream_t>(stream));
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
@@ -416,38 +423,16 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   try {
     DeviceGuard g(h->device);
-    const size_t need = ws_bytes_for(h, nrhs);
     const bool capturing = stream_is_capturing(st);
-    // a workspace allocated inside a graph capture would belong to that graph
-    if (capturing && need > h->ws_bytes) return QTT_ERROR_NOT_SUPPORTED;
-    if (need > h->ws_bytes) {
-      if (h->ws) {
-        // the old buffer may still be in use by work on its stream
-        cudaFreeAsync(h->ws, h->ws_stream);
-        for (size_t i = h->graphs.size(); i-- > 0;)
-          if (h->graphs[i].ws == h->ws) {
-            cudaGraphExecDestroy(h->graphs[i].exec);
-            h->graphs.erase(h->graphs.begin() + i);
-          }
-        h->ws = nullptr;
-        h->ws_bytes = 0;
-      }
-      cudaError_t e = cudaMallocAsync(&h->ws, need, st);
-      if (e != cudaSuccess) {
-        h->ws = nullptr;
-        return from_cuda(e);
-      }
-      h->ws_bytes = need;
-      h->ws_stream = st;
-    }
-    const qtt_status_t so = order_after_last(h, st);
-    if (so != QTT_SUCCESS) return so;
-    const qtt_status_t s2 = enqueue_graphed(h, x, y, nrhs, h->ws, st);
-    if (s2 == QTT_SUCCESS && !capturing) {
-      h->last_stream = st;
-      h->has_last = true;
-    }
-    return s2;
+    void* old_ws = h->ws;
+    bool grew = false;
+    const int64_t group = cached_group(h, nrhs);
+    qtt_status_t so = cached_acquire(&h->ws, &h->ws_bytes, &h->ws_used, h->ws_pending, ws_bytes_for(h, group), st,
+                                     capturing, &grew);
+    if (grew) drop_graphs_on(h, old_ws);
+    if (so == QTT_SUCCESS) so = enqueue_groups(h, x, y, nrhs, group, h->ws, st);
+    if (so == QTT_SUCCESS) so = cached_release(h->ws_used, &h->ws_pending, st, capturing);
+    return so;
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
@@ -459,7 +444,10 @@ qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   try {
     DeviceGuard g(h->device);
-    const size_t elems = size_t(h->N) * size_t(nrhs);
+    // staging for one group of RHS at a time (bounded by rhs_group and by
+    // the device memory the group's workspace needs)
+    const int64_t group = std::min(cached_group(h, nrhs), rhs_group(h, nrhs));
+    const size_t elems = size_t(h->N) * size_t(group);
     if (elems > h->h_elems) {
       if (h->hx) cudaFree(h->hx);
       if (h->hy) cudaFree(h->hy);
@@ -474,34 +462,26 @@ qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host
     if (nrhs == 1 && h->stages.size() >= 2 && h->shard_bits == 0 && !h->timing &&
         (h->N >> (h->stages.front().plan.k1 - h->stages.front().plan.k0 + 1)) >= 8 * 64 &&
         (h->N >> (h->stages.back().plan.k1 - h->stages.back().plan.k0 + 1)) >= 8 * 64) {
-      const size_t need = ws_bytes_for(h, 1);
-      if (need > h->ws_bytes) {
-        if (h->ws) cudaFreeAsync(h->ws, h->ws_stream);
-        h->ws = nullptr;
-        h->ws_bytes = 0;
-        for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
-        h->graphs.clear();
-        cudaError_t e = cudaMallocAsync(&h->ws, need, st);
-        if (e != cudaSuccess) {
-          h->ws = nullptr;
-          return from_cuda(e);
-        }
-        h->ws_bytes = need;
-        h->ws_stream = st;
-      }
-      qtt_status_t s = order_after_last(h, st);
+      void* old_ws = h->ws;
+      bool grew = false;
+      qtt_status_t s = cached_acquire(&h->ws, &h->ws_bytes, &h->ws_used, h->ws_pending, ws_bytes_for(h, 1), st,
+                                      false, &grew);
+      if (grew) drop_graphs_on(h, old_ws);
       if (s == QTT_SUCCESS) s = apply_host_pipelined(h, x_host, y_host, st);
+      if (s == QTT_SUCCESS) s = cached_release(h->ws_used, &h->ws_pending, st, false);
       if (s != QTT_SUCCESS) return s;
-      h->last_stream = st;
-      h->has_last = true;
       return from_cuda(cudaStreamSynchronize(st));
     }
-    cudaError_t e = cudaMemcpyAsync(h->hx, x_host, elems * sizeof(double), cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return from_cuda(e);
-    qtt_status_t s = qtt_apply(h, h->hx, h->hy, nrhs, stream);
-    if (s != QTT_SUCCESS) return s;
-    e = cudaMemcpyAsync(y_host, h->hy, elems * sizeof(double), cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return from_cuda(e);
+    for (int64_t r0 = 0; r0 < nrhs; r0 += group) {
+      const int64_t gr = std::min(group, nrhs - r0);
+      const size_t off = size_t(r0) * size_t(h->N), n = size_t(gr) * size_t(h->N);
+      cudaError_t e = cudaMemcpyAsync(h->hx, x_host + off, n * sizeof(double), cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return from_cuda(e);
+      qtt_status_t s = qtt_apply(h, h->hx, h->hy, gr, stream);
+      if (s != QTT_SUCCESS) return s;
+      e = cudaMemcpyAsync(y_host + off, h->hy, n * sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return from_cuda(e);
+    }
     return from_cuda(cudaStreamSynchronize(st));
   } catch (...) {
     return QTT_ERROR_CUDA;
@@ -579,9 +559,11 @@ qtt_status_t qtt_stage_times(qtt_handle_t h, float* ms, int n_stages, int* n_app
 qtt_status_t qtt_destroy(qtt_handle_t h) {
   if (!h) return QTT_SUCCESS;
   DeviceGuard g(h->device);
+  // every plain enqueue records `last`; the cached buffers' events cover the
+  // work around an apply that uses them (grid pack/unpack, host copies)
   if (h->last) cudaEventSynchronize(h->last);
-  if (h->ws && h->ws_stream) cudaStreamSynchronize(h->ws_stream);
-  if (h->gx && h->g_stream) cudaStreamSynchronize(h->g_stream);
+  if (h->ws_pending) cudaEventSynchronize(h->ws_used);
+  if (h->g_pending) cudaEventSynchronize(h->g_used);
   free_plan(h);
   return QTT_SUCCESS;
 }

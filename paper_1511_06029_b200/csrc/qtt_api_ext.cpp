@@ -53,22 +53,22 @@ qtt_status_t qtt_apply_grid(qtt_handle_t h, const double* grid_in, double* grid_
   try {
     DeviceGuard g(h->device);
     const size_t elems = size_t(h->N) * size_t(nrhs);
-    if (elems > h->g_elems) {
-      if (h->gx) cudaFreeAsync(h->gx, h->g_stream);
-      if (h->gy) cudaFreeAsync(h->gy, h->g_stream);
-      h->gx = h->gy = nullptr;
-      h->g_elems = 0;
-      cudaError_t e = cudaMallocAsync(&h->gx, elems * sizeof(double), st);
-      if (e == cudaSuccess) e = cudaMallocAsync(&h->gy, elems * sizeof(double), st);
-      if (e != cudaSuccess) return from_cuda(e);
-      h->g_elems = elems;
-      h->g_stream = st;
-    }
-    qtt_status_t s = qtt_morton_pack(grid_in, h->gx, dim, levels, nrhs, stream);
+    const bool capturing = stream_is_capturing(st);
+    // the staging vectors are shared by the handle's grid applies: order this
+    // one after the previous (on any stream) before the pack overwrites gx
+    void* gbuf = h->gx;
+    size_t gbytes = h->g_elems * 2 * sizeof(double);
+    qtt_status_t s = cached_acquire(&gbuf, &gbytes, &h->g_used, h->g_pending, elems * 2 * sizeof(double), st,
+                                    capturing, nullptr);
     if (s != QTT_SUCCESS) return s;
-    s = qtt_apply(h, h->gx, h->gy, nrhs, stream);
-    if (s != QTT_SUCCESS) return s;
-    return qtt_morton_unpack(h->gy, grid_out, dim, levels, nrhs, stream);
+    h->g_elems = gbytes / (2 * sizeof(double));
+    h->gx = static_cast<double*>(gbuf);
+    h->gy = h->gx + h->g_elems;
+    s = qtt_morton_pack(grid_in, h->gx, dim, levels, nrhs, stream);
+    if (s == QTT_SUCCESS) s = qtt_apply(h, h->gx, h->gy, nrhs, stream);
+    if (s == QTT_SUCCESS) s = qtt_morton_unpack(h->gy, grid_out, dim, levels, nrhs, stream);
+    if (s == QTT_SUCCESS) s = cached_release(h->g_used, &h->g_pending, st, capturing);
+    return s;
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
@@ -200,7 +200,7 @@ qtt_status_t qtt_product_create(qtt_product_t* out, int n_factors, const qtt_han
 
 qtt_status_t qtt_product_workspace_size(qtt_product_t p, int64_t nrhs, size_t* bytes) {
   if (!p || !bytes || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
-  *bytes = product_ws_bytes(p, nrhs);
+  *bytes = product_ws_bytes(p, rhs_group(p->factors[0], nrhs));
   return QTT_SUCCESS;
 }
 
@@ -209,7 +209,9 @@ qtt_status_t qtt_product_apply_ws(qtt_product_t p, const double* x, double* y, i
   if (!p) return QTT_ERROR_INVALID_VALUE;
   qtt_status_t s = check_apply_args(p->factors[0], x, y, nrhs);
   if (s != QTT_SUCCESS) return s;
-  const size_t need = product_ws_bytes(p, nrhs);
+  // RHS in groups of rhs_group (N * group <= 2^31 rows per launch)
+  const int64_t group = rhs_group(p->factors[0], nrhs);
+  const size_t need = product_ws_bytes(p, group);
   if (!ws || ws_bytes < need) return QTT_ERROR_INVALID_VALUE;
   if (reinterpret_cast<uintptr_t>(ws) % 256) return QTT_ERROR_NOT_SUPPORTED;
   if (!is_device_ptr(ws)) return QTT_ERROR_NOT_SUPPORTED;
@@ -217,17 +219,21 @@ qtt_status_t qtt_product_apply_ws(qtt_product_t p, const double* x, double* y, i
     DeviceGuard g(p->device);
     const int n = int(p->factors.size());
     unsigned char* base = static_cast<unsigned char*>(ws);
-    const size_t vb = product_vec_bytes(p, nrhs);
+    const size_t vb = product_vec_bytes(p, group);
     double* tmp[2] = {reinterpret_cast<double*>(base), reinterpret_cast<double*>(base + vb)};
     const size_t nvec = n >= 3 ? 2 : (n == 2 ? 1 : 0);
     void* fws = base + nvec * vb;
-    const double* in = x;
-    // F_{n-1} first; each factor's stages read the previous factor's output
-    for (int i = n - 1, step = 0; i >= 0; --i, ++step) {
-      double* out = (i == 0) ? y : tmp[step & 1];
-      s = enqueue(p->factors[i], in, out, nrhs, fws, reinterpret_cast<cudaStream_t>(stream));
-      if (s != QTT_SUCCESS) return s;
-      in = out;
+    for (int64_t r0 = 0; r0 < nrhs; r0 += group) {
+      const int64_t gr = std::min(group, nrhs - r0);
+      const size_t off = size_t(r0) * size_t(p->N);
+      const double* in = x + off;
+      // F_{n-1} first; each factor's stages read the previous factor's output
+      for (int i = n - 1, step = 0; i >= 0; --i, ++step) {
+        double* out = (i == 0) ? y + off : tmp[step & 1];
+        s = enqueue(p->factors[i], in, out, gr, fws, reinterpret_cast<cudaStream_t>(stream));
+        if (s != QTT_SUCCESS) return s;
+        in = out;
+      }
     }
     return QTT_SUCCESS;
   } catch (...) {
@@ -242,22 +248,13 @@ qtt_status_t qtt_product_apply(qtt_product_t p, const double* x, double* y, int6
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   try {
     DeviceGuard g(p->device);
-    const size_t need = product_ws_bytes(p, nrhs);
-    // a workspace allocated inside a graph capture would belong to that graph
-    if (need > p->ws_bytes && stream_is_capturing(st)) return QTT_ERROR_NOT_SUPPORTED;
-    if (need > p->ws_bytes) {
-      if (p->ws) cudaFreeAsync(p->ws, p->ws_stream);
-      p->ws = nullptr;
-      p->ws_bytes = 0;
-      cudaError_t e = cudaMallocAsync(&p->ws, need, st);
-      if (e != cudaSuccess) {
-        p->ws = nullptr;
-        return from_cuda(e);
-      }
-      p->ws_bytes = need;
-      p->ws_stream = st;
-    }
-    return qtt_product_apply_ws(p, x, y, nrhs, p->ws, p->ws_bytes, stream);
+    const bool capturing = stream_is_capturing(st);
+    qtt_status_t s2 = cached_acquire(&p->ws, &p->ws_bytes, &p->ws_used, p->ws_pending,
+                                     product_ws_bytes(p, rhs_group(p->factors[0], nrhs)),
+                                     st, capturing, nullptr);
+    if (s2 == QTT_SUCCESS) s2 = qtt_product_apply_ws(p, x, y, nrhs, p->ws, p->ws_bytes, stream);
+    if (s2 == QTT_SUCCESS) s2 = cached_release(p->ws_used, &p->ws_pending, st, capturing);
+    return s2;
   } catch (...) {
     return QTT_ERROR_CUDA;
   }
@@ -266,10 +263,9 @@ qtt_status_t qtt_product_apply(qtt_product_t p, const double* x, double* y, int6
 qtt_status_t qtt_product_destroy(qtt_product_t p) {
   if (!p) return QTT_SUCCESS;
   DeviceGuard g(p->device);
-  if (p->ws) {
-    if (p->ws_stream) cudaStreamSynchronize(p->ws_stream);
-    cudaFree(p->ws);
-  }
+  if (p->ws_pending) cudaEventSynchronize(p->ws_used);
+  if (p->ws) cudaFree(p->ws);
+  if (p->ws_used) cudaEventDestroy(p->ws_used);
   delete p;
   return QTT_SUCCESS;
 }

@@ -239,9 +239,10 @@ void free_plan(qtt_plan* h) {
   if (h->proj_fused.d_bpack) cudaFree(h->proj_fused.d_bpack);
   if (h->d_peers) cudaFree(h->d_peers);
   if (h->ws) cudaFree(h->ws);
-  if (h->gx) cudaFree(h->gx);
+  if (h->gx) cudaFree(h->gx);        // gy lives in the same allocation
   if (h->cmv) cudaFree(h->cmv);
-  if (h->gy) cudaFree(h->gy);
+  if (h->ws_used) cudaEventDestroy(h->ws_used);
+  if (h->g_used) cudaEventDestroy(h->g_used);
   if (h->hx) cudaFree(h->hx);
   if (h->hy) cudaFree(h->hy);
   for (auto& e : h->pending) {
@@ -527,21 +528,48 @@ bool stream_is_capturing(cudaStream_t st) {
   return cs != cudaStreamCaptureStatusNone;
 }
 
-qtt_status_t order_after_last(qtt_plan* h, cudaStream_t st) {
-  if (!h->has_last || h->last_stream == st) return QTT_SUCCESS;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
-    cudaGetLastError();
-    return QTT_SUCCESS;
+qtt_status_t cached_acquire(void** ptr, size_t* bytes, cudaEvent_t* used, bool pending, size_t need,
+                            cudaStream_t st, bool capturing, bool* grew) {
+  if (grew) *grew = false;
+  if (capturing && need > *bytes) return QTT_ERROR_NOT_SUPPORTED;
+  if (!*used && cudaEventCreateWithFlags(used, cudaEventDisableTiming) != cudaSuccess) {
+    *used = nullptr;
+    return QTT_ERROR_CUDA;
   }
-  return from_cuda(cudaStreamWaitEvent(st, h->last, 0));
+  if (pending && !capturing) {
+    const cudaError_t e = cudaStreamWaitEvent(st, *used, 0);
+    if (e != cudaSuccess) return from_cuda(e);
+  }
+  if (need <= *bytes) return QTT_SUCCESS;
+  if (*ptr) {
+    const cudaError_t e = cudaFreeAsync(*ptr, st);
+    if (e != cudaSuccess) return from_cuda(e);
+    *ptr = nullptr;
+    *bytes = 0;
+  }
+  if (grew) *grew = true;
+  const cudaError_t e = cudaMallocAsync(ptr, need, st);
+  if (e != cudaSuccess) {
+    *ptr = nullptr;
+    return from_cuda(e);
+  }
+  *bytes = need;
+  return QTT_SUCCESS;
+}
+
+qtt_status_t cached_release(cudaEvent_t used, bool* pending, cudaStream_t st, bool capturing) {
+  if (capturing || !used) return QTT_SUCCESS;
+  const cudaError_t e = cudaEventRecord(used, st);
+  if (e != cudaSuccess) return from_cuda(e);
+  *pending = true;
+  return QTT_SUCCESS;
 }
 
 qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs) {
   if (!h || !x || !y || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
   if (h->shard_bits) return QTT_ERROR_INVALID_VALUE;   // shard handles use qtt_shard_apply
-  // N * nrhs <= 2^31 keeps every GEMM row index a valid 32-bit TMA coordinate
-  if (nrhs > (int64_t(1) << 31) / h->N) return QTT_ERROR_NOT_SUPPORTED;
+  // an apply's byte range must be addressable (launches are grouped by rhs_group)
+  if (nrhs > (int64_t(1) << 60) / h->N) return QTT_ERROR_INVALID_VALUE;
   const uintptr_t xs = reinterpret_cast<uintptr_t>(x), ys = reinterpret_cast<uintptr_t>(y);
   const uintptr_t bytes = uintptr_t(h->N) * uintptr_t(nrhs) * sizeof(double);
   if (xs < ys + bytes && ys < xs + bytes) return QTT_ERROR_INVALID_VALUE;

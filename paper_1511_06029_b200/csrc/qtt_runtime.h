@@ -53,18 +53,19 @@ struct qtt_plan {
   Stage proj_fused;                // the projection as a wide stage writing into peers
   double** d_peers = nullptr;      // device table of the P receive buffers (qtt_shard_set_peers)
   int64_t max_interior_rank = 0;
-  // cached workspace (qtt_apply)
+  // cached workspace (qtt_apply, qtt_apply_host, shard applies) and the event
+  // recorded after the last apply that used it (cross-stream ordering; no
+  // caller stream is kept beyond a call)
   void* ws = nullptr;
   size_t ws_bytes = 0;
-  cudaStream_t ws_stream = nullptr;
-  // stream of the last apply that used the cached workspace (cross-stream ordering)
-  cudaStream_t last_stream = nullptr;
-  bool has_last = false;
-  // cached QTT-order staging vectors (qtt_apply_grid)
+  cudaEvent_t ws_used = nullptr;
+  bool ws_pending = false;
+  // cached QTT-order staging vectors (qtt_apply_grid): one allocation, gy = gx + g_elems
   double* gx = nullptr;
   double* gy = nullptr;
   size_t g_elems = 0;
-  cudaStream_t g_stream = nullptr;
+  cudaEvent_t g_used = nullptr;
+  bool g_pending = false;
   // cached scratch of the compressed matvec (b's cores, product cores, densify workspace)
   void* cmv = nullptr;
   size_t cmv_bytes = 0;
@@ -102,7 +103,8 @@ struct qtt_product {
   int64_t N = 0;
   void* ws = nullptr;
   size_t ws_bytes = 0;
-  cudaStream_t ws_stream = nullptr;
+  cudaEvent_t ws_used = nullptr;
+  bool ws_pending = false;
 };
 
 namespace qtt {
@@ -192,6 +194,16 @@ std::vector<double> pack_small(const double* W, const qtt::StagePlan& sp);
 std::vector<double> shard_projection(int d, const int64_t* ranks, const double* const* cores, int s, int g);
 size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs);
 size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs);
+// Right-hand sides per launch group: every launch keeps N * group <= 2^31 so
+// each GEMM row index is a valid 32-bit TMA coordinate; an apply with more
+// RHS runs as consecutive groups (the RHS are independent problems, and the
+// plan -- split-K included -- does not depend on the group size, so results
+// are bitwise those of one launch per RHS).
+constexpr int64_t kMaxRowsPerLaunch = int64_t(1) << 31;
+inline int64_t rhs_group(const qtt_plan* h, int64_t nrhs) {
+  const int64_t g = kMaxRowsPerLaunch / h->N;
+  return nrhs < g ? nrhs : (g < 1 ? 1 : g);
+}
 void free_plan(qtt_plan* h);
 qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores);
 // split-K scratch inside the workspace (enqueue); nullptr = no split
@@ -208,7 +220,17 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
 qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st);
 // true while `st` is being captured into a CUDA graph (ours or the caller's)
 bool stream_is_capturing(cudaStream_t st);
-qtt_status_t order_after_last(qtt_plan* h, cudaStream_t st);
+// Grow-only device buffers cached per handle (workspace, grid staging,
+// product workspace).  cached_acquire orders `st` after the previous apply
+// that used the buffer (its `used` event; skipped while `st` is being
+// captured), then -- if `need` exceeds the buffer -- releases the old block on
+// `st` itself (so the free follows every earlier user) and allocates the new
+// one there; *grew reports that.  A buffer cannot grow during a capture (it
+// would belong to the caller's graph): NOT_SUPPORTED.  cached_release records
+// `used` on `st` after the apply's last use (skipped while capturing).
+qtt_status_t cached_acquire(void** ptr, size_t* bytes, cudaEvent_t* used, bool pending, size_t need,
+                            cudaStream_t st, bool capturing, bool* grew);
+qtt_status_t cached_release(cudaEvent_t used, bool* pending, cudaStream_t st, bool capturing);
 qtt_status_t check_apply_args(qtt_plan* h, const double* x, const double* y, int64_t nrhs);
 // qtt_host_copy.cpp
 qtt_status_t apply_host_pipelined(qtt_plan* h, const double* x_host, double* y_host, cudaStream_t st);

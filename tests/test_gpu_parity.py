@@ -468,9 +468,9 @@ def test_abi_errors(qtt):
     assert lib.qtt_apply(h, x.ctypes.data, yt.data_ptr(), 1, None) == E.QTT_ERROR_NOT_SUPPORTED
     # null
     assert lib.qtt_apply(h, None, yt.data_ptr(), 1, None) == E.QTT_ERROR_INVALID_VALUE
-    # maximum size: N * nrhs must stay <= 2^31 (32-bit TMA row coordinates)
-    too_many = (1 << 31) // N + 1
-    assert lib.qtt_apply(h, xt.data_ptr(), yt.data_ptr(), too_many, None) == E.QTT_ERROR_NOT_SUPPORTED
+    # a byte range beyond 2^63 (N * nrhs > 2^60) cannot be addressed
+    too_many = (1 << 60) // N + 1
+    assert lib.qtt_apply(h, xt.data_ptr(), yt.data_ptr(), too_many, None) == E.QTT_ERROR_INVALID_VALUE
     # short workspace
     ws = torch.empty(16, dtype=torch.float64, device="cuda")
     assert lib.qtt_apply_ws(h, xt.data_ptr(), yt.data_ptr(), 1, ws.data_ptr(), 128, None) == E.QTT_ERROR_INVALID_VALUE
@@ -797,6 +797,105 @@ def test_back_to_back_applies_on_two_streams(qtt):
             a.synchronize()
             b.synchronize()
             assert torch.equal(ya, ref1) and torch.equal(yb, ref2)
+    finally:
+        op.close()
+
+
+def test_cached_ws_ordered_across_caller_ws_apply(qtt):
+    """apply(A) on the cached workspace (stream a), apply_ws(B) with the
+    caller's workspace (stream b), apply(C) on the cached workspace (stream c):
+    C is ordered after A (the cached workspace's own event), not after B."""
+    cfg, cores, x = generate("c3")
+    xs = [x, np.ascontiguousarray(x[:, ::-1]), np.ascontiguousarray(-x)]
+    op = qtt.QttOperator(cores)
+    try:
+        refs = [op.apply(torch.from_numpy(v).cuda()) for v in xs]
+        torch.cuda.synchronize()
+        ws = torch.empty(op.workspace_size(1) // 8 + 64, dtype=torch.float64, device="cuda")
+        st = [torch.cuda.Stream() for _ in range(3)]
+        xd = [torch.from_numpy(v).cuda() for v in xs]
+        torch.cuda.synchronize()
+        for _ in range(4):
+            ya = op.apply(xd[0], stream=st[0])
+            yb = torch.empty_like(xd[1])
+            with torch.cuda.stream(st[1]):
+                op.apply(xd[1], out=yb, workspace=ws, stream=st[1])
+            yc = op.apply(xd[2], stream=st[2])
+            for s_ in st:
+                s_.synchronize()
+            assert torch.equal(ya, refs[0]) and torch.equal(yb, refs[1]) and torch.equal(yc, refs[2])
+    finally:
+        op.close()
+
+
+def test_cached_ws_grows_on_another_stream(qtt):
+    """The cached workspace grows (nrhs 1 -> 4) on stream b while an apply that
+    used the old block is still queued on stream a: the old block is released
+    on b after a's apply (stream-ordered), and both results are right."""
+    cfg, cores, x = generate("c3")
+    x4 = np.ascontiguousarray(np.concatenate([x, -x, 2 * x, x[:, ::-1]]))
+    op = qtt.QttOperator(cores)
+    try:
+        ref1 = op.apply(torch.from_numpy(x).cuda())
+        ref4 = op.apply(torch.from_numpy(x4).cuda())
+        torch.cuda.synchronize()
+        for _ in range(2):
+            op2 = qtt.QttOperator(cores)            # a fresh handle: workspace sized for nrhs = 1
+            a, b = torch.cuda.Stream(), torch.cuda.Stream()
+            xa, xb = torch.from_numpy(x).cuda(), torch.from_numpy(x4).cuda()
+            torch.cuda.synchronize()
+            ya = op2.apply(xa, stream=a)
+            yb = op2.apply(xb, stream=b)
+            a.synchronize()
+            b.synchronize()
+            assert torch.equal(ya, ref1) and torch.equal(yb, ref4)
+            op2.close()
+    finally:
+        op.close()
+
+
+def test_grid_apply_two_streams(qtt):
+    """Grid applies on one handle from two streams share the staging vectors:
+    the second is ordered after the first."""
+    d = 15
+    _, cores, _ = random_case(4242, d, 12)
+    rng = np.random.default_rng(1)
+    g1 = rng.standard_normal((1, 1 << d))
+    g2 = rng.standard_normal((1, 1 << d))
+    op = qtt.QttOperator(cores)
+    try:
+        r1 = op.apply_grid(torch.from_numpy(g1).cuda(), dim=3)
+        r2 = op.apply_grid(torch.from_numpy(g2).cuda(), dim=3)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Stream(), torch.cuda.Stream()
+        x1, x2 = torch.from_numpy(g1).cuda(), torch.from_numpy(g2).cuda()
+        torch.cuda.synchronize()
+        for _ in range(3):
+            y1 = op.apply_grid(x1, dim=3, stream=a)
+            y2 = op.apply_grid(x2, dim=3, stream=b)
+            a.synchronize()
+            b.synchronize()
+            assert torch.equal(y1, r1) and torch.equal(y2, r2)
+    finally:
+        op.close()
+
+
+def test_apply_host_out_validation(qtt):
+    _, cores, x = random_case(5, 8, 4, nrhs=2)
+    op = qtt.QttOperator(cores)
+    try:
+        ref = op.apply_host(x)
+        for bad in (np.empty(x.shape, dtype=np.float32), np.empty((x.shape[1],)),
+                    np.empty((2, 2 * x.shape[1]))[:, ::2], np.empty((3, x.shape[1]))):
+            with pytest.raises(ValueError):
+                op.apply_host(x, out=bad)
+        ro = np.empty_like(x)
+        ro.flags.writeable = False
+        with pytest.raises(ValueError):
+            op.apply_host(x, out=ro)
+        out = np.empty_like(x)
+        assert op.apply_host(x, out=out) is out
+        np.testing.assert_array_equal(out, ref)
     finally:
         op.close()
 
