@@ -373,23 +373,34 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
         with q.QttOperator(cores, max_stage_levels=max_stage_levels) as op:
             x = torch.from_numpy(x_np).to(dev)
             y = torch.empty_like(x)
-            ws = torch.empty(max(op.workspace_size(cfg.nrhs), 8) // 8 + 64, dtype=torch.float64, device=dev)
+            ws = None
             reps = 5 if name == "c5" else 20
-            fn = lambda: op.apply(x, out=y, workspace=ws, stream=stream)
+            # the default user path: qtt_apply on the handle's cached workspace
+            fn = lambda: op.apply(x, out=y, stream=stream)
             med, mn = time_applies(fn, reps, 3, stream)
+            apply_plan = op.stages(cfg.nrhs)
+            launches = op.launches(cfg.nrhs)
+            # per-stage times: stage timing runs (and reports) the per-stage launches
             op.set_stage_timing(True)
             op.stage_times()
+            timed_stages = op.stages(cfg.nrhs)
             for _ in range(3):
                 fn()
             torch.cuda.synchronize()
             op.set_stage_timing(False)
             sms, nt = op.stage_times()
-            rows, sT, st_ = stage_table(op.stages(), cfg.ranks, cfg.N, cfg.nrhs, sms, nt, P, BW)
+            rows, sT, st_ = stage_table(timed_stages, cfg.ranks, cfg.N, cfg.nrhs, sms, nt, P, BW)
             F = op.flops_per_rhs * cfg.nrhs
             Fx = sum(rr["flops_executed"] for rr in rows)
+            if apply_plan and apply_plan[0]["variant"] == "fused":
+                Lf = [a_["k_last"] - a_["k_first"] + 1 for a_ in apply_plan]
+                Fx = sum(2 ** (L_ + 1) * cfg.ranks[a_["k_first"] - 1] * cfg.ranks[a_["k_last"]] * cfg.N * cfg.nrhs
+                         for L_, a_ in zip(Lf, apply_plan))
             out[name] = {"ms_per_apply": med, "ms_single_call_min": mn,
                          "gflops_alg2": F / (med * 1e-3) / 1e9,
-                         "tflops_executed": Fx / (med * 1e-3) / 1e12, "launches": op.launches_per_apply,
+                         "tflops_executed": Fx / (med * 1e-3) / 1e12, "launches": launches,
+                         "apply_plan": [[a_["k_first"], a_["k_last"], a_["variant"]] for a_ in apply_plan],
+                         "per_stage_note": "per-stage rows below: the per-stage launches stage timing runs",
                          "per_stage_frac": sT / st_ if st_ else None,
                          "per_stage_frac_executed": sum(
                              max(rr["flops_executed"] / P, (8 * cfg.N * cfg.nrhs * (rr["ranks"][0] + rr["ranks"][1])) / BW)

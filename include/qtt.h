@@ -351,6 +351,22 @@ qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int
 qtt_status_t qtt_get_stage_split(qtt_handle_t h, int s, int64_t nrhs, int* ksplit);
 
 /*
+ * qtt_get_apply_plan -- what an apply with `nrhs` right-hand sides on this
+ * handle launches (host-only query; no GPU work).
+ *   launches : receives the number of kernel launches of the whole apply
+ *              (stages, split-K reduce launches, RHS groups; 1 for a fused apply).
+ *   n_stages, k_first, k_last, variant : the stages it runs (arrays of >= d
+ *              ints, any may be NULL), as qtt_plan_stages; variant 6 = FUSED:
+ *              every stage of the apply in ONE persistent launch (grid
+ *              barriers between stages, intermediates in L2),
+ *              chosen at create time for latency-bound sizes (small N * nrhs)
+ *              when the cost model prefers it.  A handle with stage timing on
+ *              (qtt_set_stage_timing) runs and reports the per-stage plan.
+ */
+qtt_status_t qtt_get_apply_plan(qtt_handle_t h, int64_t nrhs, int* launches, int* n_stages, int* k_first,
+                                int* k_last, int* variant);
+
+/*
  * Stage timing (for the bench's roofline): when enabled, each apply records
  * a CUDA event pair around every stage launch on the apply stream.
  * qtt_stage_times synchronizes those events, writes the summed milliseconds

@@ -23,12 +23,12 @@ from ._lib import QttError, SYMBOLS
 
 __all__ = [
     "QttOperator", "QttError", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "plan_stages", "qtt_apply", "qtt_apply_ws", "qtt_apply_host",
-    "qtt_workspace_size", "qtt_get_info", "qtt_get_stage", "qtt_get_stage_split", "qtt_set_stage_timing",
+    "qtt_workspace_size", "qtt_get_info", "qtt_get_stage", "qtt_get_stage_split", "qtt_get_apply_plan", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy", "qtt_status_string", "library_path", "SYMBOLS",
     "morton_pack", "morton_unpack", "QttProduct",
 ]
 
-VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "merged", 3: "wide", 4: "small", 5: "diag"}
+VARIANT_NAMES = {0: "generic", 1: "dmma", 2: "merged", 3: "wide", 4: "small", 5: "diag", 6: "fused"}
 MAX_STAGE_LEVELS = 10
 
 
@@ -169,6 +169,19 @@ def qtt_get_stage(h: int, s: int) -> dict:
     a, b, v = C.c_int(), C.c_int(), C.c_int()
     _lib.check("qtt_get_stage", _lib.load().qtt_get_stage(h, int(s), C.byref(a), C.byref(b), C.byref(v)))
     return dict(k_first=a.value, k_last=b.value, variant=VARIANT_NAMES.get(v.value, str(v.value)))
+
+
+def qtt_get_apply_plan(h: int, nrhs: int = 1):
+    """(launches, [{'k_first', 'k_last', 'variant'}]) of an apply with nrhs RHS (host only)."""
+    info = qtt_get_info(h)
+    n = max(info["d"], 1)
+    launches, ns = C.c_int(), C.c_int()
+    a, b, v = (C.c_int * n)(), (C.c_int * n)(), (C.c_int * n)()
+    _lib.check("qtt_get_apply_plan", _lib.load().qtt_get_apply_plan(
+        h, int(nrhs), C.byref(launches), C.byref(ns), C.cast(a, C.c_void_p), C.cast(b, C.c_void_p),
+        C.cast(v, C.c_void_p)))
+    return launches.value, [dict(k_first=a[i], k_last=b[i], variant=VARIANT_NAMES.get(v[i], str(v[i])))
+                            for i in range(ns.value)]
 
 
 def qtt_get_stage_split(h: int, s: int, nrhs: int = 1) -> int:
@@ -367,10 +380,18 @@ class QttOperator:
     def workspace_size(self, nrhs: int = 1) -> int:
         return qtt_workspace_size(self.handle, nrhs)
 
-    def stages(self):
-        """Per launch: {'k_first', 'k_last', 'variant', 'ksplit'} (as plan_stages)."""
-        return [dict(qtt_get_stage(self.handle, s), ksplit=qtt_get_stage_split(self.handle, s, 1))
+    def stages(self, nrhs: int = 1):
+        """The stages an apply with `nrhs` RHS runs: {'k_first', 'k_last', 'variant',
+        'ksplit'} each (variant 'fused': all of them in one persistent launch)."""
+        _, st = qtt_get_apply_plan(self.handle, nrhs)
+        if st and st[0]["variant"] == "fused":
+            return [dict(s_, ksplit=1) for s_ in st]
+        return [dict(qtt_get_stage(self.handle, s), ksplit=qtt_get_stage_split(self.handle, s, nrhs))
                 for s in range(self.launches_per_apply)]
+
+    def launches(self, nrhs: int = 1) -> int:
+        """Kernel launches of one apply with `nrhs` RHS (1 for a fused apply)."""
+        return qtt_get_apply_plan(self.handle, nrhs)[0]
 
     def stage_splits(self, nrhs: int = 1):
         """Split-K factor of every stage at `nrhs` (1 = unsplit)."""

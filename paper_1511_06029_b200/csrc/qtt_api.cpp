@@ -116,6 +116,40 @@ static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, 
         h->max_interior_rank = std::max<int64_t>(h->max_interior_rank, plan[s].r_out);
     }
     for (size_t s = 0; s < plan.size() && st == QTT_SUCCESS; ++s) st = upload_stage(h, h->stages[s], cores);
+    // the fused apply: ONE persistent launch for latency-bound sizes, when the
+    // cost model prefers it to the per-stage launches.  Only
+    // with the default stage cap (a cap asks for that launch structure).
+    static const bool no_fused = std::getenv("QTT_NO_FUSED") != nullptr;
+    static const bool force_fused = std::getenv("QTT_FORCE_FUSED") != nullptr;
+    if (st == QTT_SUCCESS && !shard_bits && !no_fused && max_stage_levels >= qtt::kMaxStageLevels) {
+      double est1 = 0;
+      std::vector<qtt::StagePlan> fp = qtt::plan_stages_fused(dl, ranks, max_stage_levels, h->N, &est1);
+      int64_t fr = 1;
+      for (size_t s = 0; s + 1 < fp.size(); ++s) fr = std::max<int64_t>(fr, fp[s].r_out);
+      int64_t pmax = 0;
+      for (int64_t p = 1; !fp.empty() && p <= 64; p *= 2) {
+        if (2.0 * double(fr) * double(h->N) * double(p) * 8.0 > double(qtt::kFusedMaxL2Bytes)) break;
+        // this fused plan at p RHS against the best per-stage plan at p RHS
+        double ef = qtt::fused_launch_seconds();
+        for (const auto& sp : fp) {
+          qtt::StagePlan tmp;
+          ef += qtt::fused_stage_seconds(ranks, sp.k0, sp.k1, double(h->N) * double(p), &tmp);
+        }
+        const double er = qtt::plan_seconds(
+            qtt::plan_stages(dl, ranks, h->smem_optin, max_stage_levels, diag.data(), h->N * p));
+        if (!(ef < er) && !force_fused) break;
+        pmax = p;
+      }
+      if (pmax > 0) {
+        h->fstages.resize(fp.size());
+        for (size_t s = 0; s < fp.size() && st == QTT_SUCCESS; ++s) {
+          h->fstages[s].plan = fp[s];
+          st = upload_stage(h, h->fstages[s], cores);
+        }
+        h->fused_max_nrhs = pmax;
+        if (fp.size() > 1) h->max_interior_rank = std::max(h->max_interior_rank, fr);
+      }
+    }
     if (st == QTT_SUCCESS && shard_bits) {
       qtt::StagePlan& pp = h->proj.plan;
       const int rp = int(h->ranks[dl]), P = 1 << shard_bits;   // padded local top rank
@@ -374,7 +408,8 @@ qtt_status_t qtt_workspace_size(qtt_handle_t h, int64_t nrhs, size_t* bytes) {
 // cached CUDA graph; several use plain launches (a graph per group pointer
 // pair would only churn the cache at these sizes).
 static qtt_status_t enqueue_groups(qtt_plan* h, const double* x, double* y, int64_t nrhs, int64_t group, void* ws,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, bool bar_zero = false) {
+  if (group >= nrhs && use_fused(h, nrhs)) return enqueue_fused(h, x, y, nrhs, ws, st, !bar_zero);
   if (group >= nrhs) return enqueue_graphed(h, x, y, nrhs, ws, st);
   for (int64_t r0 = 0; r0 < nrhs; r0 += group) {
     const int64_t g = std::min(group, nrhs - r0);
@@ -426,11 +461,23 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
     const bool capturing = stream_is_capturing(st);
     void* old_ws = h->ws;
     bool grew = false;
-    const int64_t group = cached_group(h, nrhs);
+    int64_t group = cached_group(h, nrhs);
     qtt_status_t so = cached_acquire(&h->ws, &h->ws_bytes, &h->ws_used, h->ws_pending, ws_bytes_for(h, group), st,
                                      capturing, &grew);
-    if (grew) drop_graphs_on(h, old_ws);
-    if (so == QTT_SUCCESS) so = enqueue_groups(h, x, y, nrhs, group, h->ws, st);
+    while (so == QTT_ERROR_OUT_OF_MEMORY && group > 1 && !capturing) {   // smaller RHS groups
+      group = (group + 1) / 2;
+      bool g2 = false;
+      so = cached_acquire(&h->ws, &h->ws_bytes, &h->ws_used, h->ws_pending, ws_bytes_for(h, group), st, false, &g2);
+      grew = grew || g2;
+    }
+    if (grew) {
+      drop_graphs_on(h, old_ws);
+      h->ws_header_zero = false;
+    }
+    // the cached workspace's grid-barrier words stay 0 once cleared (every
+    // fused launch leaves them so; per-stage applies clear the whole header)
+    if (so == QTT_SUCCESS) so = enqueue_groups(h, x, y, nrhs, group, h->ws, st, h->ws_header_zero);
+    if (so == QTT_SUCCESS) h->ws_header_zero = true;
     if (so == QTT_SUCCESS) so = cached_release(h->ws_used, &h->ws_pending, st, capturing);
     return so;
   } catch (...) {
@@ -468,6 +515,7 @@ qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host
                                       false, &grew);
       if (grew) drop_graphs_on(h, old_ws);
       if (s == QTT_SUCCESS) s = apply_host_pipelined(h, x_host, y_host, st);
+      if (s == QTT_SUCCESS) h->ws_header_zero = true;      // the pipelined apply cleared the header
       if (s == QTT_SUCCESS) s = cached_release(h->ws_used, &h->ws_pending, st, false);
       if (s != QTT_SUCCESS) return s;
       return from_cuda(cudaStreamSynchronize(st));
@@ -514,6 +562,27 @@ qtt_status_t qtt_get_stage(qtt_handle_t h, int s, int* k_first, int* k_last, int
   if (k_first) *k_first = h->stages[s].plan.k0;
   if (k_last) *k_last = h->stages[s].plan.k1;
   if (variant) *variant = h->stages[s].plan.variant;
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_get_apply_plan(qtt_handle_t h, int64_t nrhs, int* launches, int* n_stages, int* k_first,
+                                int* k_last, int* variant) {
+  if (!h || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
+  const int64_t group = h->shard_bits ? nrhs : rhs_group(h, nrhs);
+  const int64_t groups = (nrhs + group - 1) / group;
+  const bool fused = group >= nrhs && use_fused(h, nrhs);
+  const std::vector<Stage>& S = fused ? h->fstages : h->stages;
+  int per = fused ? 1 : 0;
+  if (!fused)
+    for (const Stage& st : S) per += 1 + (stage_ksplit(h, st, 0) > 1 ? 1 : 0);
+  if (h->shard_bits) per += 1;
+  if (launches) *launches = int(std::min<int64_t>(int64_t(per) * groups, 0x7fffffff));
+  if (n_stages) *n_stages = int(S.size());
+  for (size_t i = 0; i < S.size(); ++i) {
+    if (k_first) k_first[i] = S[i].plan.k0;
+    if (k_last) k_last[i] = S[i].plan.k1;
+    if (variant) variant[i] = fused ? int(qtt::kFused) : S[i].plan.variant;
+  }
   return QTT_SUCCESS;
 }
 

@@ -29,7 +29,10 @@ namespace qtt {
 //              block-diagonal BIE factor M): the stage is a batched GEMV,
 //              out[(m, ii)][b] = sum_a in[(m, ii)][a] D[ii][a][b], 2 r_in r_out
 //              flops per element whatever L (qtt_level_dmma.cu diag_kernel).
-enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2, kWide = 3, kSmall = 4, kDiag = 5 };
+//   kFused   : every stage of a latency-bound apply in ONE persistent launch
+//              (small-variant warp tiles, grid barriers between stages,
+//              intermediates in L2; qtt_wide_kernel.cu fused_small_kernel).
+enum Variant : int { kGeneric = 0, kDmma = 1, kMerged = 2, kWide = 3, kSmall = 4, kDiag = 5, kFused = 6 };
 constexpr int kDiagMaxROut = 8;                       // r_out of the row-per-lane diagonal kernel
 constexpr int kDiagMaxRank = 64;                      // r_in, r_out of any diagonal stage
 constexpr int kDiagMaxLevels = 24;
@@ -151,8 +154,18 @@ size_t dmma_smem_bytes(int KB, int NB, int K, int rep, int stages);
 // Tiling of a DMMA stage; false if it does not fit smem_optin.
 bool dmma_tiling(int K, int KB, int NB, size_t smem_optin, int* rep, int* stages, size_t* smem);
 // diag[k-1] != 0: core k is diagonal in (i_k, j_k) (nullptr: none known)
+// rows = nrhs * N the estimates are made at (0: N, one RHS)
 std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
-                                   const unsigned char* diag = nullptr);
+                                   const unsigned char* diag = nullptr, int64_t rows = 0);
+double plan_seconds(const std::vector<StagePlan>& p);   // sum of the stage estimates
+// one fused stage's shape and estimate at `rows` input rows (-1: too large)
+double fused_stage_seconds(const int64_t* ranks, int k0, int k1, double rows, StagePlan* sp);
+double fused_launch_seconds();
+// fused apply (variant kFused): the stage split of one persistent launch at
+// `rows` = nrhs * N GEMM input rows, and its estimated time (*est; +inf and an
+// empty plan when none fits)
+std::vector<StagePlan> plan_stages_fused(int d, const int64_t* ranks, int max_stage_levels, int64_t rows,
+                                         double* est);
 bool projection_plan(int r, int s, size_t smem_optin, StagePlan* sp);
 bool projection_plan_wide(int r, int s, size_t smem_optin, StagePlan* sp);   // fused exchange
 
@@ -191,6 +204,26 @@ cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st);
 // small variant (qtt_wide_kernel.cu): a.ncb = 32-column blocks, a.nchunks = k-steps of 8,
 // a.bpack = pack_small layout
 cudaError_t launch_small(const LevelArgs& a, cudaStream_t st);
+// fused apply (variant kFused): the stages of one apply in one cooperative launch
+constexpr int kFusedWarps = 8;        // warps per CTA (two per SM sub-partition)
+constexpr int kFusedMaxStages = 16;
+constexpr size_t kFusedMaxCoreBytes = size_t(4) << 20;   // a fused stage's packed super-core, read from L2
+constexpr size_t kFusedMaxL2Bytes = size_t(40) << 20;    // both intermediate buffers of a fused apply
+constexpr size_t kFusedBarOffset = 192;                  // grid-barrier words in the workspace header
+struct FusedStage {
+  const double* in = nullptr;
+  double* out = nullptr;
+  const double* bpack = nullptr;   // pack_small layout
+  int64_t M = 0;                   // GEMM rows: nrhs * N / n_i
+  int64_t out_limit = 0;           // QTT_BOUNDS_CHECK builds
+  int log2_q = 0, n_i = 2, r_out = 0, nout = 0, K = 0, nchunks = 0, ncb = 0;
+};
+struct FusedArgs {
+  FusedStage st[kFusedMaxStages];
+  int nstages = 0;
+  unsigned* bar = nullptr;         // [count, generation]; count 0 at launch
+};
+cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st);
 // y[s][c] = sum_g recv[g][s][c] (fixed order g = 0..parts-1), qtt_wide_kernel.cu
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,
                                 int num_sms);

@@ -286,9 +286,41 @@ static bool diag_shape(const int64_t* ranks, int k0, int k1, int64_t n, StagePla
   return true;
 }
 
+// Diagnostic (A/B of stage splits): QTT_PLAN_FORCE_STAGES="1-7,8-9,...,18-24"
+// forces the partition of levels 1..d into stages (each gets its cheapest
+// kernel instance); ignored unless it covers exactly 1..d with coverable stages.
+static bool forced_stages(int d, const int64_t* ranks, size_t smem_optin, int64_t n, std::vector<StagePlan>* out) {
+  static const char* spec = std::getenv("QTT_PLAN_FORCE_STAGES");
+  if (!spec) return false;
+  std::vector<StagePlan> p;
+  int next = 1;
+  const char* c = spec;
+  while (*c) {
+    char* e = nullptr;
+    const long a = std::strtol(c, &e, 10);
+    if (e == c || *e != '-') return false;
+    c = e + 1;
+    const long b = std::strtol(c, &e, 10);
+    if (e == c || a != next || b < a || b > d || b - a + 1 > kMaxStageLevels) return false;
+    StagePlan sp;
+    if (!stage_shape(ranks, int(a), int(b), n, smem_optin, &sp)) return false;
+    p.push_back(sp);
+    next = int(b) + 1;
+    c = e;
+    if (*c == ',') ++c;
+  }
+  if (next != d + 1) return false;
+  *out = p;
+  return true;
+}
+
 std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_optin, int max_stage_levels,
-                                   const unsigned char* diag) {
-  const int64_t n = int64_t(1) << d;
+                                   const unsigned char* diag, int64_t rows) {
+  const int64_t n = rows > 0 ? rows : int64_t(1) << d;
+  {
+    std::vector<StagePlan> forced;
+    if (forced_stages(d, ranks, smem_optin, n, &forced)) return forced;
+  }
   const int maxL = std::max(1, std::min(max_stage_levels, kMaxStageLevels));
   // diagonal stages cost the same whatever L: allow long ones unless the caller capped L
   const int maxLd = max_stage_levels >= kMaxStageLevels ? kDiagMaxLevels : maxL;
@@ -320,6 +352,89 @@ std::vector<StagePlan> plan_stages(int d, const int64_t* ranks, size_t smem_opti
   for (int k = d; k > 0; k = choice[k].k0 - 1) out.push_back(choice[k]);
   std::reverse(out.begin(), out.end());
   return out;
+}
+
+// ---- fused apply (variant kFused): the whole apply as ONE persistent launch.
+// Every stage is a small-variant stage (16 x 32 warp tiles from L2) run by all
+// warps of the grid, stages separated by grid barriers (fused_small_kernel).
+// Cost of a stage: its warp tiles spread over the SM sub-partitions, each tile
+// a chain of nq k-steps of 16 DMMA.8x8x4 (16 clk each on one sub-partition's
+// FP64 tensor pipe: 0.13 us per step at 1.965 GHz), plus one L2 round trip
+// and the barrier.  Calibrated on the box; QTT_FUSED_STEP /
+// _LAT / _BAR / _LAUNCH override the constants (diagnostics).
+namespace {
+double env_or(const char* name, double v) {
+  const char* e = std::getenv(name);
+  return e ? std::atof(e) : v;
+}
+}  // namespace
+
+double fused_stage_seconds(const int64_t* ranks, int k0, int k1, double rows, StagePlan* sp) {
+  static const double kStep = env_or("QTT_FUSED_STEP", 0.13e-6);
+  static const double kLat = env_or("QTT_FUSED_LAT", 0.6e-6);
+  static const double kBar = env_or("QTT_FUSED_BAR", 0.7e-6);
+  const int L = k1 - k0 + 1;
+  const int n_i = 1 << L;
+  const int r_in = int(ranks[k0 - 1]), r_out = int(ranks[k1]);
+  const int K = n_i * r_in, nout = n_i * r_out;
+  if (double(K) * nout * 8.0 > double(kFusedMaxCoreBytes)) return -1.0;
+  *sp = StagePlan{};
+  sp->k0 = k0;
+  sp->k1 = k1;
+  sp->variant = kFused;
+  sp->r_in = r_in;
+  sp->r_out = r_out;
+  sp->n_i = n_i;
+  sp->K = K;
+  sp->RP = r_out;
+  sp->NB = 4;
+  sp->ncb = (nout + kSmallCols - 1) / kSmallCols;
+  sp->nchunks = (K + kSmallK - 1) / kSmallK;
+  const double wt = std::ceil(rows / n_i / kSmallRows) * sp->ncb;
+  const double slots = kSms * 4;
+  sp->est_seconds = std::ceil(wt / slots) * sp->nchunks * kStep + kLat + kBar;
+  return sp->est_seconds;
+}
+
+double fused_launch_seconds() {
+  static const double v = env_or("QTT_FUSED_LAUNCH", 2.0e-6);
+  return v;
+}
+
+std::vector<StagePlan> plan_stages_fused(int d, const int64_t* ranks, int max_stage_levels, int64_t rows,
+                                         double* est) {
+  const double kLaunchF = fused_launch_seconds();
+  const int maxL = std::max(1, std::min(max_stage_levels, kMaxStageLevels));
+  std::vector<double> best(d + 1, std::numeric_limits<double>::infinity());
+  std::vector<int> cnt(d + 1, 0);
+  std::vector<StagePlan> choice(d + 1);
+  best[0] = 0;
+  for (int k = 1; k <= d; ++k)
+    for (int L = 1; L <= std::min(maxL, k); ++L) {
+      StagePlan sp;
+      const double t = fused_stage_seconds(ranks, k - L + 1, k, double(rows), &sp);
+      if (t < 0 || cnt[k - L] + 1 > kFusedMaxStages) continue;
+      if (best[k - L] + t < best[k]) {
+        best[k] = best[k - L] + t;
+        cnt[k] = cnt[k - L] + 1;
+        choice[k] = sp;
+      }
+    }
+  std::vector<StagePlan> out;
+  if (!std::isfinite(best[d])) {
+    if (est) *est = std::numeric_limits<double>::infinity();
+    return out;
+  }
+  for (int k = d; k > 0; k = choice[k].k0 - 1) out.push_back(choice[k]);
+  std::reverse(out.begin(), out.end());
+  if (est) *est = best[d] + kLaunchF;
+  return out;
+}
+
+double plan_seconds(const std::vector<StagePlan>& p) {
+  double t = 0;
+  for (const auto& sp : p) t += sp.est_seconds;
+  return t;
 }
 
 // Projection stage of a shard (top-bit sharding): T[m][alpha]

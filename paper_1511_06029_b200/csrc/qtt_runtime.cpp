@@ -185,7 +185,7 @@ bool is_device_ptr(const void* p, int dev) {
 // [split-K partials of the largest split stage, if any].
 
 size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs) {
-  if (h->stages.size() <= 1 && h->shard_bits == 0) return 0;
+  if (h->stages.size() <= 1 && h->fstages.size() <= 1 && h->shard_bits == 0) return 0;
   const size_t one = size_t(h->max_interior_rank) * size_t(h->N) * size_t(nrhs) * sizeof(double);
   return (one + 255) / 256 * 256;
 }
@@ -302,7 +302,7 @@ qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
     if (e != cudaSuccess) return from_cuda(e);
     return from_cuda(cudaMemcpy(S.d_core, D.data(), D.size() * sizeof(double), cudaMemcpyHostToDevice));
   }
-  if (sp.variant == qtt::kSmall) {
+  if (sp.variant == qtt::kSmall || sp.variant == qtt::kFused) {
     S.ctas_per_sm = 1;
     const std::vector<double> W = sp.k0 == sp.k1
                                       ? std::vector<double>(cores[sp.k0 - 1], cores[sp.k0 - 1] + size_t(sp.r_in) * 4 * sp.r_out)
@@ -471,6 +471,58 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
   return QTT_SUCCESS;
 }
 
+bool use_fused(const qtt_plan* h, int64_t nrhs) {
+  return !h->fstages.empty() && nrhs <= h->fused_max_nrhs && !h->timing && h->shard_bits == 0;
+}
+
+qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
+                           bool zero_bar) {
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  const size_t bb = ws_buf_bytes(h, nrhs);
+  double* buf[2] = {reinterpret_cast<double*>(base + kWsHeader), reinterpret_cast<double*>(base + kWsHeader + bb)};
+  qtt::FusedArgs a;
+  a.nstages = int(h->fstages.size());
+  a.bar = reinterpret_cast<unsigned*>(base + qtt::kFusedBarOffset);
+  int64_t max_wt = 1;
+  const double* in = x;
+  for (int s = 0; s < a.nstages; ++s) {
+    const qtt::StagePlan& sp = h->fstages[s].plan;
+    qtt::FusedStage& f = a.st[s];
+    const int L = sp.k1 - sp.k0 + 1;
+    const bool last = s + 1 == a.nstages;
+    f.in = in;
+    f.out = last ? y : buf[s & 1];
+    f.bpack = h->fstages[s].d_bpack;
+    f.M = nrhs * (h->N >> L);
+    f.out_limit = int64_t(h->N) * nrhs * sp.r_out;
+    f.log2_q = h->d - L;
+    f.n_i = sp.n_i;
+    f.r_out = sp.r_out;
+    f.nout = sp.n_i * sp.r_out;
+    f.K = sp.K;
+    f.nchunks = sp.nchunks;
+    f.ncb = sp.ncb;
+    max_wt = std::max<int64_t>(max_wt, (f.M + qtt::kSmallRows - 1) / qtt::kSmallRows * f.ncb);
+    in = f.out;
+  }
+  const int grid = int(std::min<int64_t>(h->num_sms, (max_wt + qtt::kFusedWarps - 1) / qtt::kFusedWarps));
+  if (zero_bar) {
+    const cudaError_t e = cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return from_cuda(e);
+  }
+  nvtxRangePushA("qtt fused apply");
+  const cudaError_t e = qtt::launch_fused(a, grid, st);
+  nvtxRangePop();
+  if (e != cudaSuccess) {
+    if (std::getenv("QTT_DEBUG"))
+      std::fprintf(stderr, "qtt: fused apply (%d stages, grid %d) launch failed: %s\n", a.nstages, grid,
+                   cudaGetErrorString(e));
+    return from_cuda(e);
+  }
+  if (!stream_is_capturing(st)) cudaEventRecord(h->last, st);
+  return QTT_SUCCESS;
+}
+
 // enqueue() through a cached CUDA graph: captured once per (x, y, ws, nrhs) on
 // an internal stream, then replayed on `st` with one launch.  Falls back to a
 // plain enqueue while stage timing is on, when `st` is itself being captured,
@@ -548,8 +600,21 @@ qtt_status_t cached_acquire(void** ptr, size_t* bytes, cudaEvent_t* used, bool p
     *bytes = 0;
   }
   if (grew) *grew = true;
-  const cudaError_t e = cudaMallocAsync(ptr, need, st);
+  cudaError_t e = cudaMallocAsync(ptr, need, st);
+  if (e == cudaErrorMemoryAllocation) {
+    // the released block (and other freed blocks) may still sit in the
+    // stream-ordered pool, unusable for a larger allocation: wait for the
+    // stream, return the pool's free memory to the device and retry once
+    cudaGetLastError();
+    cudaMemPool_t pool = nullptr;
+    int dev = 0;
+    if (cudaStreamSynchronize(st) == cudaSuccess && cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(ptr, need, st);
+  }
   if (e != cudaSuccess) {
+    cudaGetLastError();
     *ptr = nullptr;
     return from_cuda(e);
   }

@@ -53,6 +53,12 @@ struct qtt_plan {
   Stage proj_fused;                // the projection as a wide stage writing into peers
   double** d_peers = nullptr;      // device table of the P receive buffers (qtt_shard_set_peers)
   int64_t max_interior_rank = 0;
+  // fused apply (variant kFused, ONE launch per apply): the
+  // stage split of the persistent kernel, packed as small stages; used for
+  // applies with nrhs <= fused_max_nrhs (0 = never) unless stage timing is on
+  std::vector<Stage> fstages;
+  int64_t fused_max_nrhs = 0;
+  bool ws_header_zero = false;     // the cached workspace's grid-barrier words are 0
   // cached workspace (qtt_apply, qtt_apply_host, shard applies) and the event
   // recorded after the last apply that used it (cross-stream ordering; no
   // caller stream is kept beyond a call)
@@ -218,6 +224,11 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
 qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
                      bool fused = false);
 qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st);
+// the fused apply (one persistent launch); zero_bar: clear the workspace's
+// grid-barrier words first (a workspace not known to hold them at 0)
+bool use_fused(const qtt_plan* h, int64_t nrhs);
+qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
+                           bool zero_bar);
 // true while `st` is being captured into a CUDA graph (ours or the caller's)
 bool stream_is_capturing(cudaStream_t st);
 // Grow-only device buffers cached per handle (workspace, grid staging,

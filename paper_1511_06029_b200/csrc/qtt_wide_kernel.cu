@@ -103,8 +103,8 @@ __device__ __forceinline__ void chunk_mma(double (&c)[NBC][4], const unsigned ch
 
 // Row-separation epilogue (Alg. 2 line 8 for all L levels): column n = ii*r_out + b
 // of GEMM row m goes to out[(m + Q*(s*(n_i-1) + ii)) * r_out + b], s = m / Q.
-template <int NBC>
-__device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const LevelArgs& p, int64_t m_first,
+template <int NBC, class P>
+__device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const P& p, int64_t m_first,
                                            int n_first, int lane) {
   const int g = lane >> 2, t0 = lane & 3;
   const int r_out = p.r_out;
@@ -153,19 +153,28 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 }
 
 // Fused shard exchange (r_out = 1): column n of GEMM row m goes to peers[n][m].
+// A lane holds rows (g, g + 8) x columns (n, n + 1); one shuffle with the lane
+// of the neighbouring row (g ^ 1) gives each lane two consecutive rows of ONE
+// column, stored as one 16-byte peer store (NVLink: half the transactions of
+// 8-byte stores).  M and the part's slot offset are even, so the pair never
+// straddles the end of a slot.
 template <int NBC>
 __device__ __forceinline__ void scatter_store(const double (&c)[NBC][4], const LevelArgs& p, int64_t m_first,
                                               int n_first, int lane) {
   const int g = lane >> 2, t0 = lane & 3;
+  const bool odd = g & 1;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int64_t m = m_first + g + 8 * h;
-    if (m >= p.M) continue;
+    const int64_t m_even = m_first + (g & ~1) + 8 * h;
 #pragma unroll
     for (int nb = 0; nb < NBC; ++nb) {
-      const int n = n_first + nb * 8 + 2 * t0;
-      if (n < p.nout) p.peers[n][p.peer_offset + m] = c[nb][2 * h];
-      if (n + 1 < p.nout) p.peers[n + 1][p.peer_offset + m] = c[nb][2 * h + 1];
+      const double v0 = c[nb][2 * h], v1 = c[nb][2 * h + 1];   // (row g, col n), (row g, col n + 1)
+      const double recv = __shfl_xor_sync(0xffffffffu, odd ? v0 : v1, 4);
+      const int n = n_first + nb * 8 + 2 * t0 + (odd ? 1 : 0);
+      if (m_even < p.M && n < p.nout) {
+        double* dst = p.peers[n] + p.peer_offset + m_even;
+        *reinterpret_cast<double2*>(dst) = odd ? make_double2(recv, v1) : make_double2(v0, recv);
+      }
     }
   }
 }
@@ -390,14 +399,14 @@ __global__ void __launch_bounds__(128) split_reduce_kernel(const LevelArgs p) {
 // same k permutation as the resident kernel, so two k4 MMAs per load) and its
 // 4 n-blocks x 2 B values as two contiguous 32-byte pieces of the packed
 // operand (pack_small: [cb][p][lane][s][nb], s = the k4 step within the 8).
-__global__ void __launch_bounds__(kSmallWarps * 32) small_dmma_kernel(const LevelArgs p) {
-  pdl_wait();
-  const int lane = threadIdx.x & 31;
-  const int64_t wt = int64_t(blockIdx.x) * kSmallWarps + (threadIdx.x >> 5);
+// One 16 x 32 warp tile of a small stage.  COHERENT: the A rows were written
+// earlier in the same kernel (the fused apply below), so they are read through
+// L2 (ld.global.cg), never through the non-coherent/L1 path.
+template <bool COHERENT, class P>
+__device__ __forceinline__ void small_tile(const P& p, int64_t wt, int lane) {
   const int64_t mt = wt / p.ncb;
   const int cb = int(wt - mt * p.ncb);
   const int64_t m0 = mt * kSmallRows;
-  if (m0 >= p.M) return;
   const int g = lane >> 2, t0 = lane & 3;
   const int K = p.K;
   const bool ok0 = m0 + g < p.M, ok1 = m0 + g + 8 < p.M;
@@ -412,11 +421,16 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_dmma_kernel(const Leve
     const int k = q * kSmallK + 2 * t0;
     double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
     if (k + 1 < K) {
-      if (ok0) x = __ldg(reinterpret_cast<const double2*>(a0 + q * kSmallK));
-      if (ok1) y = __ldg(reinterpret_cast<const double2*>(a1 + q * kSmallK));
+      if (COHERENT) {
+        if (ok0) x = __ldcg(reinterpret_cast<const double2*>(a0 + q * kSmallK));
+        if (ok1) y = __ldcg(reinterpret_cast<const double2*>(a1 + q * kSmallK));
+      } else {
+        if (ok0) x = __ldg(reinterpret_cast<const double2*>(a0 + q * kSmallK));
+        if (ok1) y = __ldg(reinterpret_cast<const double2*>(a1 + q * kSmallK));
+      }
     } else if (k < K) {
-      if (ok0) x.x = __ldg(a0 + q * kSmallK);
-      if (ok1) y.x = __ldg(a1 + q * kSmallK);
+      if (ok0) x.x = COHERENT ? __ldcg(a0 + q * kSmallK) : __ldg(a0 + q * kSmallK);
+      if (ok1) y.x = COHERENT ? __ldcg(a1 + q * kSmallK) : __ldg(a1 + q * kSmallK);
     }
     const double4 b0 = bp[int64_t(q) * 64], b1 = bp[int64_t(q) * 64 + 1];
     const double bs0[4] = {b0.x, b0.y, b0.z, b0.w}, bs1[4] = {b1.x, b1.y, b1.z, b1.w};
@@ -432,6 +446,62 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_dmma_kernel(const Leve
     }
   }
   tile_store<4>(c, p, m0, cb * kSmallCols, lane);
+}
+
+__global__ void __launch_bounds__(kSmallWarps * 32) small_dmma_kernel(const LevelArgs p) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t wt = int64_t(blockIdx.x) * kSmallWarps + (threadIdx.x >> 5);
+  if (wt / p.ncb * kSmallRows >= p.M) return;
+  small_tile<false>(p, wt, lane);
+}
+
+// Grid-wide barrier of the fused apply (all CTAs co-resident: cooperative
+// launch).  bar[0] counts arrivals and is left at 0 by the last arriver, which
+// then bumps the generation bar[1] the others wait on, so the barrier needs no
+// re-initialisation between barriers or launches (bar[0] must be 0 at the
+// first launch).  Thread 0 arrives after the CTA barrier with a gpu-scope
+// release (the CTA's stage output) and leaves with an acquire; the next
+// stage reads the intermediate with ld.global.cg (L2, coherent).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire_u32(bar + 1);
+    __threadfence();
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == nblocks - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(bar), "r"(0u) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
+    } else {
+      while (ld_acquire_u32(bar + 1) == gen) {
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// The whole apply of a latency-bound problem in ONE persistent launch
+// (variant kFused): the plan's stages run one after another, each as 16 x 32
+// warp tiles straight from L2 (the small variant's tile)
+// spread over every warp of the grid, separated by grid barriers instead of
+// kernel boundaries.  The intermediates (two ping-pong buffers) stay in L2.
+__global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const FusedArgs a) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = int64_t(blockIdx.x) * kFusedWarps + (threadIdx.x >> 5);
+  const int64_t nwarps = int64_t(gridDim.x) * kFusedWarps;
+  for (int s = 0; s < a.nstages; ++s) {
+    const FusedStage& p = a.st[s];
+    const int64_t wts = (p.M + kSmallRows - 1) / kSmallRows * p.ncb;
+    for (int64_t wt = warp; wt < wts; wt += nwarps) {
+      if (s == 0)
+        small_tile<false>(p, wt, lane);
+      else
+        small_tile<true>(p, wt, lane);
+    }
+    if (s + 1 < a.nstages) grid_barrier(a.bar, gridDim.x);
+  }
 }
 
 using KernelFn = void (*)(const LevelArgs, const CUtensorMap);
@@ -564,6 +634,23 @@ cudaError_t launch_small(const LevelArgs& a, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, wide::small_dmma_kernel, a);
+}
+
+cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st) {
+  if (grid < 1 || a.nstages < 1 || a.nstages > kFusedMaxStages) return cudaErrorInvalidValue;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;     // co-residency for the grid barrier
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kFusedWarps * 32);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, wide::fused_small_kernel, a);
 }
 
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,

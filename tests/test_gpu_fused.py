@@ -1,0 +1,156 @@
+"""The fused apply (variant 'fused'): every stage of a
+latency-bound apply in ONE persistent launch, grid barriers between stages.
+
+Parity against the CPU oracle (Alg. 2) and the closed forms, on
+the default plans of c1 / c2 (where the cost model picks it), on random
+profiles with d <= 15 forced through it (QTT_FORCE_FUSED=1, subprocess: the
+switch is read once per process), through both entry points (cached
+workspace, caller workspace), across RHS counts, and bitwise against the
+per-stage launches of the same handle (stage timing runs those).
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+from qtt_workload import closed_forms as CF
+from qtt_workload import generate, random_case
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def qtt():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    import paper_1511_06029_b200 as q
+    q._lib.load()
+    return q
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_default_plan_is_one_launch(qtt, name):
+    cfg, cores, x = generate(name)
+    with qtt.QttOperator(cores) as op:
+        assert op.launches(1) == 1
+        st = op.stages(1)
+        assert st and all(s["variant"] == "fused" for s in st)
+        assert st[0]["k_first"] == 1 and st[-1]["k_last"] == cfg.d
+        assert all(a["k_last"] + 1 == b["k_first"] for a, b in zip(st, st[1:]))
+        y = op.apply(torch.from_numpy(x).cuda())
+        # the per-stage launches of the same handle (stage timing runs those)
+        op.set_stage_timing(True)
+        assert op.launches(1) > 1
+        y2 = op.apply(torch.from_numpy(x).cuda())
+        op.set_stage_timing(False)
+        op.stage_times()
+        torch.cuda.synchronize()
+        y, y2 = y.cpu().numpy(), y2.cpu().numpy()
+    ref = oracle.apply_blas_sweep(cores, x)
+    oracle.assert_close(y, ref)
+    oracle.assert_close(y2, ref)
+    if name == "c1":
+        oracle.assert_close(y, oracle.apply_dense(cores, x))
+
+
+def test_fused_entry_points_and_repeats(qtt):
+    """Cached workspace (barrier words kept at 0 between launches) and caller
+    workspace (cleared per apply); 50 back-to-back applies with alternating
+    inputs, bitwise reproducible."""
+    cfg, cores, x = generate("c2")
+    x2 = np.ascontiguousarray(x[:, ::-1])
+    with qtt.QttOperator(cores) as op:
+        assert op.launches(1) == 1
+        xa, xb = torch.from_numpy(x).cuda(), torch.from_numpy(x2).cuda()
+        ra, rb = op.apply(xa), op.apply(xb)
+        ws = torch.empty(op.workspace_size(1) // 8 + 64, dtype=torch.float64, device="cuda")
+        ws.fill_(np.nan)                       # garbage in the caller's workspace
+        ya, yb = torch.empty_like(xa), torch.empty_like(xb)
+        for i in range(50):
+            if i % 2:
+                op.apply(xa, out=ya)
+                op.apply(xb, out=yb, workspace=ws)
+            else:
+                op.apply(xb, out=yb)
+                op.apply(xa, out=ya, workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(ya, ra) and torch.equal(yb, rb)
+    oracle.assert_close(ra.cpu().numpy(), oracle.apply_blas_sweep(cores, x))
+
+
+@pytest.mark.parametrize("nrhs", [2, 3, 4])
+def test_fused_multi_rhs(qtt, nrhs):
+    cfg, cores, _ = generate("c1")
+    x = np.random.default_rng(nrhs).standard_normal((nrhs, cfg.N))
+    with qtt.QttOperator(cores) as op:
+        y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        y1 = op.apply(torch.from_numpy(np.ascontiguousarray(x[:1])).cuda()).cpu().numpy()
+        both_fused = op.launches(nrhs) == 1 and op.launches(1) == 1
+    oracle.assert_close(y, oracle.apply_blas_sweep(cores, x))
+    if both_fused:
+        np.testing.assert_array_equal(y[0], y1[0])      # the same stage split: batch-invariant
+
+
+def test_fused_closed_forms(qtt):
+    """Exact closed forms through the fused launch: identity and the cyclic
+    shift, bitwise."""
+    d = 13
+    x = np.random.default_rng(0).standard_normal((2, 1 << d))
+    for cores, ref in ((CF.identity_cores(d), x), (CF.shift_cores(d, 777), np.roll(x, 777, axis=1))):
+        with qtt.QttOperator(cores) as op:
+            y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        np.testing.assert_array_equal(y, ref)
+
+
+_FORCE_FUSED_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1511_06029_b200 as q
+import oracle
+from qtt_workload import random_case
+from qtt_workload import closed_forms as CF
+cases = [(1, 1, 1, 1), (2, 2, 2, 5), (3, 3, 3, 7), (4, 6, 7, 3), (5, 9, 13, 2), (6, 10, 24, 1),
+         (7, 12, 33, 1), (8, 13, 48, 2), (9, 14, 5, 4), (10, 15, 16, 1), (13, 11, 64, 1), (14, 9, 100, 1),
+         (15, 15, 31, 1), (16, 8, 3, 16)]
+n_fused = 0
+for seed, d, r, nrhs in cases:
+    _, cores, x = random_case(seed + 1900, d, r, nrhs)
+    with q.QttOperator(cores) as op:
+        fused = op.launches(nrhs) == 1 and op.stages(nrhs)[0]["variant"] == "fused"
+        n_fused += fused
+        xt = torch.from_numpy(x).cuda()
+        y = op.apply(xt).cpu().numpy()
+        ws = torch.empty(op.workspace_size(nrhs) // 8 + 64, dtype=torch.float64, device="cuda")
+        yw = op.apply(xt, workspace=ws).cpu().numpy()
+    oracle.assert_close(y, oracle.apply_alg2(cores, x))
+    assert np.array_equal(y, yw), (seed, d, r)
+for d in (4, 11, 15):
+    x = np.random.default_rng(d).standard_normal((1, 1 << d))
+    with q.QttOperator(CF.shift_cores(d, 5)) as op:
+        assert op.launches(1) == 1
+        assert np.array_equal(op.apply(torch.from_numpy(x).cuda()).cpu().numpy(), np.roll(x, 5, axis=1))
+assert n_fused >= 12, n_fused
+print("ok", n_fused)
+"""
+
+
+def test_fused_forced_random_profiles():
+    env = dict(os.environ, QTT_FORCE_FUSED="1")
+    r = subprocess.run([sys.executable, "-c", _FORCE_FUSED_SCRIPT, ROOT], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_fused_disabled_switch():
+    code = ("import sys; sys.path.insert(0, sys.argv[1]); import paper_1511_06029_b200 as q; "
+            "from qtt_workload import generate; cfg, cores, x = generate('c1'); op = q.QttOperator(cores); "
+            "print('launches', op.launches(1), op.stages(1)[0]['variant'])")
+    r = subprocess.run([sys.executable, "-c", code, ROOT], env=dict(os.environ, QTT_NO_FUSED="1"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert "fused" not in r.stdout and "launches 1 " not in r.stdout, r.stdout
