@@ -222,7 +222,10 @@ struct FusedArgs {
   FusedStage st[kFusedMaxStages];
   int nstages = 0;
   unsigned* bar = nullptr;         // [count, generation]; count 0 at launch
+  unsigned long long* prof = nullptr;   // diagnostic (QTT_FUSED_PROFILE): per CTA, %globaltimer
+                                        // at start and after each stage's tiles / barrier
 };
+constexpr int kFusedProfSlots = 2 * kFusedMaxStages + 2;
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st);
 // y[s][c] = sum_g recv[g][s][c] (fixed order g = 0..parts-1), qtt_wide_kernel.cu
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,

@@ -510,9 +510,39 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
     const cudaError_t e = cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st);
     if (e != cudaSuccess) return from_cuda(e);
   }
+  // diagnostic: QTT_FUSED_PROFILE=1 times every stage and barrier inside the
+  // launch (per CTA %globaltimer) and prints min/max over CTAs to stderr
+  static const bool fprof = std::getenv("QTT_FUSED_PROFILE") != nullptr;
+  static unsigned long long* d_prof = nullptr;
+  if (fprof && !d_prof &&
+      cudaMalloc(&d_prof, size_t(h->num_sms) * qtt::kFusedProfSlots * sizeof(unsigned long long)) != cudaSuccess)
+    d_prof = nullptr;
+  if (fprof && !stream_is_capturing(st)) a.prof = d_prof;
   nvtxRangePushA("qtt fused apply");
-  const cudaError_t e = qtt::launch_fused(a, grid, st);
+  cudaError_t e = qtt::launch_fused(a, grid, st);
   nvtxRangePop();
+  if (e == cudaSuccess && a.prof) {
+    std::vector<unsigned long long> hp(size_t(grid) * qtt::kFusedProfSlots);
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(hp.data(), d_prof, hp.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) {
+      unsigned long long t0 = ~0ull;
+      for (int b = 0; b < grid; ++b) t0 = std::min(t0, hp[size_t(b) * qtt::kFusedProfSlots]);
+      std::fprintf(stderr, "qtt fused profile (grid %d, ns from the first CTA start; min/max over CTAs):", grid);
+      for (int slot = 0; slot <= 2 * a.nstages; ++slot) {
+        unsigned long long lo = ~0ull, hi = 0;
+        for (int b = 0; b < grid; ++b) {
+          const unsigned long long v = hp[size_t(b) * qtt::kFusedProfSlots + slot] - t0;
+          lo = std::min(lo, v);
+          hi = std::max(hi, v);
+        }
+        std::fprintf(stderr, " %s%d=%llu/%llu", slot == 0 ? "start" : (slot % 2 ? "tiles" : "bar"),
+                     slot == 0 ? 0 : (slot - 1) / 2, lo, hi);
+      }
+      std::fprintf(stderr, "\n");
+    }
+  }
   if (e != cudaSuccess) {
     if (std::getenv("QTT_DEBUG"))
       std::fprintf(stderr, "qtt: fused apply (%d stages, grid %d) launch failed: %s\n", a.nstages, grid,

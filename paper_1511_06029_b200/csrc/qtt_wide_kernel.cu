@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace qtt {
 namespace wide {
@@ -486,8 +487,16 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
 // warp tiles straight from L2 (the small variant's tile)
 // spread over every warp of the grid, separated by grid barriers instead of
 // kernel boundaries.  The intermediates (two ping-pong buffers) stay in L2.
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const FusedArgs a) {
   pdl_wait();
+  unsigned long long* prof = a.prof ? a.prof + size_t(blockIdx.x) * kFusedProfSlots : nullptr;
+  if (prof && threadIdx.x == 0) prof[0] = globaltimer();
   const int lane = threadIdx.x & 31;
   const int64_t warp = int64_t(blockIdx.x) * kFusedWarps + (threadIdx.x >> 5);
   const int64_t nwarps = int64_t(gridDim.x) * kFusedWarps;
@@ -500,7 +509,12 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const Fus
       else
         small_tile<true>(p, wt, lane);
     }
+    if (prof) {
+      __syncthreads();
+      if (threadIdx.x == 0) prof[1 + 2 * s] = globaltimer();
+    }
     if (s + 1 < a.nstages) grid_barrier(a.bar, gridDim.x);
+    if (prof && threadIdx.x == 0) prof[2 + 2 * s] = globaltimer();
   }
 }
 
@@ -638,9 +652,10 @@ cudaError_t launch_small(const LevelArgs& a, cudaStream_t st) {
 
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st) {
   if (grid < 1 || a.nstages < 1 || a.nstages > kFusedMaxStages) return cudaErrorInvalidValue;
+  static const bool no_coop = std::getenv("QTT_FUSED_NOCOOP") != nullptr;   // diagnostic (A/B of launch cost)
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;     // co-residency for the grid barrier
-  attr[0].val.cooperative = 1;
+  attr[0].val.cooperative = no_coop ? 0 : 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
