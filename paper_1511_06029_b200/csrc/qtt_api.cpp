@@ -137,6 +137,9 @@ static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, 
         }
         const double er = qtt::plan_seconds(
             qtt::plan_stages(dl, ranks, h->smem_optin, max_stage_levels, diag.data(), h->N * p));
+        if (std::getenv("QTT_DEBUG"))
+          std::fprintf(stderr, "qtt: fused plan (%zu stages) at %lld RHS: est %.2f us vs per-stage plan %.2f us\n",
+                       fp.size(), (long long)p, ef * 1e6, er * 1e6);
         if (!(ef < er) && !force_fused) break;
         pmax = p;
       }

@@ -208,6 +208,7 @@ cudaError_t launch_small(const LevelArgs& a, cudaStream_t st);
 constexpr int kFusedWarps = 8;        // warps per CTA (two per SM sub-partition)
 constexpr int kFusedMaxStages = 16;
 constexpr size_t kFusedMaxCoreBytes = size_t(4) << 20;   // a fused stage's packed super-core, read from L2
+constexpr size_t kFusedMaxBBytes = size_t(128) << 10;    // one column block of it in smem: K <= 512
 constexpr size_t kFusedMaxL2Bytes = size_t(40) << 20;    // both intermediate buffers of a fused apply
 constexpr size_t kFusedBarOffset = 192;                  // grid-barrier words in the workspace header
 struct FusedStage {
@@ -217,15 +218,21 @@ struct FusedStage {
   int64_t M = 0;                   // GEMM rows: nrhs * N / n_i
   int64_t out_limit = 0;           // QTT_BOUNDS_CHECK builds
   int log2_q = 0, n_i = 2, r_out = 0, nout = 0, K = 0, nchunks = 0, ncb = 0;
+  int ks = 1;                      // warps per tile (intra-CTA split of the k-steps; 1, 2, 4 or 8)
 };
 struct FusedArgs {
   FusedStage st[kFusedMaxStages];
   int nstages = 0;
-  unsigned* bar = nullptr;         // [count, generation]; count 0 at launch
+  unsigned* bar = nullptr;         // arrival counter, 0 at launch (left at 0 by every launch)
+  size_t smem = 0;                 // dynamic smem: the largest super-core block (K x 32 doubles)
+  int repeat = 1;                  // diagnostic (QTT_FUSED_REPEAT): run every stage this many times
   unsigned long long* prof = nullptr;   // diagnostic (QTT_FUSED_PROFILE): per CTA, %globaltimer
-                                        // at start and after each stage's tiles / barrier
+                                        // at start and after each stage's tiles / barrier, then for
+                                        // the CTA's first unit of each stage: start, super-core block
+                                        // in smem, MMAs done, tile stored
 };
-constexpr int kFusedProfSlots = 2 * kFusedMaxStages + 2;
+constexpr int kFusedProfSlots = 2 * kFusedMaxStages + 2 + 4 * kFusedMaxStages;
+cudaError_t fused_prepare();   // sets the kernel's max dynamic smem
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st);
 // y[s][c] = sum_g recv[g][s][c] (fixed order g = 0..parts-1), qtt_wide_kernel.cu
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,

@@ -370,14 +370,20 @@ double env_or(const char* name, double v) {
 }  // namespace
 
 double fused_stage_seconds(const int64_t* ranks, int k0, int k1, double rows, StagePlan* sp) {
-  static const double kStep = env_or("QTT_FUSED_STEP", 0.13e-6);
-  static const double kLat = env_or("QTT_FUSED_LAT", 0.6e-6);
-  static const double kBar = env_or("QTT_FUSED_BAR", 0.7e-6);
+  // calibrated on c1 / c2 (round 2, QTT_FUSED_PROFILE): a k-step of a warp
+  // tile with two warps per sub-partition ~0.16 us; per stage ~2 us of
+  // operand latency + epilogue, ~1 us more for the split-K reduction, ~1.5 us
+  // for the grid barrier (store drain, release, polling)
+  static const double kStep = env_or("QTT_FUSED_STEP", 0.16e-6);
+  static const double kLat = env_or("QTT_FUSED_LAT", 2.0e-6);
+  static const double kRed = env_or("QTT_FUSED_RED", 1.0e-6);
+  static const double kBar = env_or("QTT_FUSED_BAR", 1.5e-6);
   const int L = k1 - k0 + 1;
   const int n_i = 1 << L;
   const int r_in = int(ranks[k0 - 1]), r_out = int(ranks[k1]);
   const int K = n_i * r_in, nout = n_i * r_out;
   if (double(K) * nout * 8.0 > double(kFusedMaxCoreBytes)) return -1.0;
+  if (size_t((K + kSmallK - 1) / kSmallK) * 128 * 16 > kFusedMaxBBytes) return -1.0;   // the smem block
   *sp = StagePlan{};
   sp->k0 = k0;
   sp->k1 = k1;
@@ -390,14 +396,21 @@ double fused_stage_seconds(const int64_t* ranks, int k0, int k1, double rows, St
   sp->NB = 4;
   sp->ncb = (nout + kSmallCols - 1) / kSmallCols;
   sp->nchunks = (K + kSmallK - 1) / kSmallK;
-  const double wt = std::ceil(rows / n_i / kSmallRows) * sp->ncb;
-  const double slots = kSms * 4;
-  sp->est_seconds = std::ceil(wt / slots) * sp->nchunks * kStep + kLat + kBar;
+  const double tiles = std::ceil(rows / n_i / kSmallRows) * sp->ncb;
+  // warps per tile: split the k-steps over up to all warps of a CTA while the
+  // grid's warps outnumber the tiles (fixed here, at plan time, for every nrhs)
+  const double warps = kSms * kFusedWarps;
+  int ks = 1;
+  while (ks * 2 <= kFusedWarps && ks * 2 <= sp->nchunks && tiles * ks * 2 <= warps) ks *= 2;
+  sp->ksplit = ks;
+  const double per_smsp = std::ceil(tiles * ks / (kSms * 4));   // warp tiles one sub-partition runs
+  const double steps = std::ceil(double(sp->nchunks) / ks);
+  sp->est_seconds = per_smsp * steps * kStep + kLat + (ks > 1 ? kRed : 0.0) + kBar;
   return sp->est_seconds;
 }
 
 double fused_launch_seconds() {
-  static const double v = env_or("QTT_FUSED_LAUNCH", 2.0e-6);
+  static const double v = env_or("QTT_FUSED_LAUNCH", 3.0e-6);   // cooperative launch
   return v;
 }
 

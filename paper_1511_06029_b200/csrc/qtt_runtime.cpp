@@ -139,6 +139,16 @@ std::vector<double> pack_small(const double* W, const qtt::StagePlan& sp) {
   });
 }
 
+std::vector<double> pack_fused(const double* W, const qtt::StagePlan& sp) {
+  const int r_in = sp.r_in, r_out = sp.r_out, n_i = sp.n_i, K = sp.K, nout = sp.n_i * sp.r_out;
+  return pack_fused_fn(sp, [=](int kk, int n) {
+    if (kk >= K || n >= nout) return 0.0;
+    const int jj = kk / r_in, a = kk % r_in;
+    const int ii = n / r_out, b = n % r_out;
+    return W[((size_t(a) * n_i + ii) * n_i + jj) * r_out + b];
+  });
+}
+
 // Top-bit sharding: projection vectors of part g onto every
 // output block h, c_{h,g}[alpha] = [G_{d-s+1}(alpha, h_1, g_1, :) ... G_d(:, h_s, g_s, 0)],
 // written as Wp[h * r + alpha], r = ranks[d-s].
@@ -307,7 +317,11 @@ qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
     const std::vector<double> W = sp.k0 == sp.k1
                                       ? std::vector<double>(cores[sp.k0 - 1], cores[sp.k0 - 1] + size_t(sp.r_in) * 4 * sp.r_out)
                                       : super_core(cores, h->ranks.data(), sp.k0, sp.k1);
-    const std::vector<double> pk = pack_small(W.data(), sp);
+    if (sp.variant == qtt::kFused) {
+      cudaError_t e = qtt::fused_prepare();
+      if (e != cudaSuccess) return from_cuda(e);
+    }
+    const std::vector<double> pk = sp.variant == qtt::kFused ? pack_fused(W.data(), sp) : pack_small(W.data(), sp);
     cudaError_t e = cudaMalloc(&S.d_bpack, pk.size() * sizeof(double));
     if (e != cudaSuccess) return from_cuda(e);
     return from_cuda(cudaMemcpy(S.d_bpack, pk.data(), pk.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -502,13 +516,28 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
     f.K = sp.K;
     f.nchunks = sp.nchunks;
     f.ncb = sp.ncb;
-    max_wt = std::max<int64_t>(max_wt, (f.M + qtt::kSmallRows - 1) / qtt::kSmallRows * f.ncb);
+    f.ks = std::max(1, sp.ksplit);
+    a.smem = std::max<size_t>(a.smem, size_t(sp.nchunks) * 128 * 16);
+    max_wt = std::max<int64_t>(max_wt, (f.M + qtt::kSmallRows - 1) / qtt::kSmallRows * f.ncb * f.ks);
     in = f.out;
   }
+  // enough CTAs for the widest stage's (tile, k-part) warps, at most one per SM
   const int grid = int(std::min<int64_t>(h->num_sms, (max_wt + qtt::kFusedWarps - 1) / qtt::kFusedWarps));
-  if (zero_bar) {
-    const cudaError_t e = cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st);
-    if (e != cudaSuccess) return from_cuda(e);
+  if (zero_bar) {   // a stream memory op (no kernel) clears the arrival counter
+    using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    static const WriteValueFn wv = [] {
+      void* f = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        f = nullptr;
+      cudaGetLastError();
+      return reinterpret_cast<WriteValueFn>(f);
+    }();
+    if (!wv || wv(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(a.bar), 0, 0) != CUDA_SUCCESS) {
+      const cudaError_t e = cudaMemsetAsync(a.bar, 0, sizeof(unsigned), st);
+      if (e != cudaSuccess) return from_cuda(e);
+    }
   }
   // diagnostic: QTT_FUSED_PROFILE=1 times every stage and barrier inside the
   // launch (per CTA %globaltimer) and prints min/max over CTAs to stderr
@@ -518,6 +547,8 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
       cudaMalloc(&d_prof, size_t(h->num_sms) * qtt::kFusedProfSlots * sizeof(unsigned long long)) != cudaSuccess)
     d_prof = nullptr;
   if (fprof && !stream_is_capturing(st)) a.prof = d_prof;
+  static const int frep = std::getenv("QTT_FUSED_REPEAT") ? std::atoi(std::getenv("QTT_FUSED_REPEAT")) : 1;
+  a.repeat = std::max(1, frep);
   nvtxRangePushA("qtt fused apply");
   cudaError_t e = qtt::launch_fused(a, grid, st);
   nvtxRangePop();
@@ -539,6 +570,12 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
         }
         std::fprintf(stderr, " %s%d=%llu/%llu", slot == 0 ? "start" : (slot % 2 ? "tiles" : "bar"),
                      slot == 0 ? 0 : (slot - 1) / 2, lo, hi);
+      }
+      std::fprintf(stderr, "\n  CTA 0, first unit of each stage (ns from its start): ");
+      for (int s2 = 0; s2 < a.nstages; ++s2) {
+        const unsigned long long* d = &hp[2 * qtt::kFusedMaxStages + 2 + 4 * s2];
+        std::fprintf(stderr, " s%d: B-in-smem %lld mma %lld stored %lld;", s2, (long long)(d[1] - d[0]),
+                     (long long)(d[2] - d[0]), (long long)(d[3] - d[0]));
       }
       std::fprintf(stderr, "\n");
     }

@@ -191,12 +191,30 @@ std::vector<double> pack_small_fn(const qtt::StagePlan& sp, F bmat) {
   return out;
 }
 
+// B operand of a fused stage (qtt_wide_kernel.cu fused_small_kernel), per
+// 32-column block a contiguous run the kernel copies to smem whole:
+//   pack[cb][q][s][h][lane][e] = Bmat(q*8 + 2*(lane%4) + s, cb*32 + (2h + e)*8 + lane/4)
+template <class F>
+std::vector<double> pack_fused_fn(const qtt::StagePlan& sp, F bmat) {
+  std::vector<double> out(size_t(sp.ncb) * sp.nchunks * 256, 0.0);
+  for (int cb = 0; cb < sp.ncb; ++cb)
+    for (int q = 0; q < sp.nchunks; ++q)
+      for (int s = 0; s < 2; ++s)
+        for (int h = 0; h < 2; ++h)
+          for (int lane = 0; lane < 32; ++lane)
+            for (int e = 0; e < 2; ++e)
+              out[((((size_t(cb) * sp.nchunks + q) * 2 + s) * 2 + h) * 32 + lane) * 2 + e] =
+                  bmat(q * qtt::kSmallK + 2 * (lane % 4) + s, cb * qtt::kSmallCols + (2 * h + e) * 8 + lane / 4);
+  return out;
+}
+
 qtt_status_t from_cuda(cudaError_t e);
 bool is_device_ptr(const void* p, int dev = -1);
 std::vector<double> super_core(const double* const* cores, const int64_t* ranks, int k0, int k1);
 std::vector<double> pack_dmma(const double* W, const qtt::StagePlan& sp);
 std::vector<double> pack_wide(const double* W, const qtt::StagePlan& sp);
 std::vector<double> pack_small(const double* W, const qtt::StagePlan& sp);
+std::vector<double> pack_fused(const double* W, const qtt::StagePlan& sp);
 std::vector<double> shard_projection(int d, const int64_t* ranks, const double* const* cores, int s, int g);
 size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs);
 size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs);

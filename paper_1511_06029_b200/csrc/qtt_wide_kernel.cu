@@ -457,65 +457,262 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_dmma_kernel(const Leve
   small_tile<false>(p, wt, lane);
 }
 
-// Grid-wide barrier of the fused apply (all CTAs co-resident: cooperative
-// launch).  bar[0] counts arrivals and is left at 0 by the last arriver, which
-// then bumps the generation bar[1] the others wait on, so the barrier needs no
-// re-initialisation between barriers or launches (bar[0] must be 0 at the
-// first launch).  Thread 0 arrives after the CTA barrier with a gpu-scope
-// release (the CTA's stage output) and leaves with an acquire; the next
-// stage reads the intermediate with ld.global.cg (L2, coherent).
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+// ---- the fused apply (variant kFused)
+//
+// Grid-wide barrier: all CTAs are co-resident (cooperative launch).  bar[0]
+// counts arrivals monotonically within a launch: barrier b (1-based) is
+// passed once it reaches b * gridDim.x.  Thread 0 arrives after the CTA
+// barrier with a gpu-scope release (the CTA's stage output, ordered before it
+// by bar.sync) and polls with acquire loads; the next stage reads the
+// intermediate with ld.global.cg (L2, coherent).  At exit every CTA adds one
+// more arrival and the last one resets the counter to 0 for the next launch
+// (all CTAs have passed every barrier by then; the next launch is
+// stream-ordered after this one).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire_u32(bar + 1);
-    __threadfence();
-    unsigned old;
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
-    if (old == nblocks - 1) {
-      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(bar), "r"(0u) : "memory");
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
-    } else {
-      while (ld_acquire_u32(bar + 1) == gen) {
-      }
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    while (int(ld_acquire_u32(bar) - target) < 0) {
     }
   }
   __syncthreads();
 }
 
-// The whole apply of a latency-bound problem in ONE persistent launch
-// (variant kFused): the plan's stages run one after another, each as 16 x 32
-// warp tiles straight from L2 (the small variant's tile)
-// spread over every warp of the grid, separated by grid barriers instead of
-// kernel boundaries.  The intermediates (two ping-pong buffers) stay in L2.
+// The same barrier split in two (thread 0 only; the caller brackets it with
+// __syncthreads): arrive, then -- after work that needs nobody else's output
+// -- wait.
+__device__ __forceinline__ void grid_arrive(unsigned* bar) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+}
+__device__ __forceinline__ void grid_wait(unsigned* bar, unsigned target) {
+  while (int(ld_acquire_u32(bar) - target) < 0) {
+  }
+}
+
+__device__ __forceinline__ void grid_exit(unsigned* bar, unsigned total) {
+  if (threadIdx.x == 0) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == total - 1) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(bar), "r"(0u) : "memory");
+  }
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
 
+// Partial product of one 16 x 32 warp tile over k-steps [q0, q1) (k-steps of
+// 8).  B comes from shared memory: the CTA's block of the stage's super-core
+// for this tile's 32 columns, fragment-ordered [q][s][h][lane][2] (pack_fused)
+// so each of the four 16-byte reads per k-step is conflict-free.  A comes
+// straight from L2, software-pipelined: the next four k-steps' A fragments
+// are in flight while the current four k-steps' 64 DMMAs run.  COHERENT: the
+// A rows were written earlier in this launch -- read through L2
+// (ld.global.cg).  K is even (K = n_i r_in, n_i >= 2), so a lane's k-pair is
+// wholly inside K or wholly past it.
+constexpr int kFusedG = 4;
+struct FusedA {
+  double2 x[kFusedG], y[kFusedG];
+};
+
+template <bool COHERENT>
+__device__ __forceinline__ void fused_load_a(FusedA& o, const double* a0, const double* a1, int q, int q1, int K,
+                                             int t0, bool ok0, bool ok1) {
+#pragma unroll
+  for (int j = 0; j < kFusedG; ++j) {
+    const int qq = q + j;
+    const bool vk = qq < q1 && (qq * kSmallK + 2 * t0 < K);
+    o.x[j] = make_double2(0.0, 0.0);
+    o.y[j] = make_double2(0.0, 0.0);
+    const double2* pa0 = reinterpret_cast<const double2*>(a0 + qq * kSmallK);
+    const double2* pa1 = reinterpret_cast<const double2*>(a1 + qq * kSmallK);
+    if (vk && ok0) o.x[j] = COHERENT ? __ldcg(pa0) : __ldg(pa0);
+    if (vk && ok1) o.y[j] = COHERENT ? __ldcg(pa1) : __ldg(pa1);
+  }
+}
+
+__device__ __forceinline__ void fused_mma(const FusedA& o, const double2* sB, int q, int q1, int lane,
+                                          double (&c)[4][4]) {
+#pragma unroll
+  for (int j = 0; j < kFusedG; ++j) {
+    const int qq = q + j;
+    if (qq >= q1) break;
+    const double2* b = sB + size_t(qq) * 128 + lane;      // [q][s][h][lane]
+    const double2 b00 = b[0], b01 = b[32], b10 = b[64], b11 = b[96];
+    const double bs0[4] = {b00.x, b00.y, b01.x, b01.y}, bs1[4] = {b10.x, b10.y, b11.x, b11.y};
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      dmma_884(c[nb][0], c[nb][1], o.x[j].x, bs0[nb]);
+      dmma_884(c[nb][2], c[nb][3], o.y[j].x, bs0[nb]);
+    }
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      dmma_884(c[nb][0], c[nb][1], o.x[j].y, bs1[nb]);
+      dmma_884(c[nb][2], c[nb][3], o.y[j].y, bs1[nb]);
+    }
+  }
+}
+
+// One stage of the fused apply.  A unit of work is one 32-column block cb of
+// the stage's output and kFusedWarps / ks row tiles of 16 rows: the CTA
+// copies the super-core block of cb (K x 32 doubles) into shared memory with
+// one bulk copy, and its warps take the row tiles, ks warps per tile, each
+// over a contiguous 1/ks of the k-steps; the ks partial tiles meet in shared
+// memory and the first warp of each tile adds them in the fixed order
+// 0..ks-1 (deterministic; ks is fixed per plan, so results do not depend on
+// nrhs) and runs the row-separation epilogue.  Units go to the CTAs
+// round-robin, consecutive units sharing cb (its block stays hot in L2).
+// Work units of a fused stage: (32-column block, group of row tiles).
+__device__ __forceinline__ int64_t fused_rgroups(const FusedStage& p) {
+  const int slots = kFusedWarps / p.ks;
+  const int64_t mtiles = (p.M + kSmallRows - 1) / kSmallRows;
+  return (mtiles + slots - 1) / slots;
+}
+
+// Thread 0: bulk-copy unit u's super-core block (column block u / rgroups) into sB.
+__device__ __forceinline__ void fused_issue_b(const FusedStage& p, int64_t u, int64_t rgroups, double2* sB,
+                                              uint64_t* bar) {
+  const int cb = int(u / rgroups);
+  const uint32_t bbytes = uint32_t(p.nchunks) * 128u * 16u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // sB's generic reads before the async write
+  dmma::mbar_arrive_expect_tx(bar, bbytes);
+  dmma::bulk_g2s(sB, p.bpack + size_t(cb) * p.nchunks * 256, bbytes, bar);
+}
+
+template <bool COHERENT>
+__device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, double2* sB, uint64_t* bar,
+                                            uint32_t& nwait, bool prefetched, int lane,
+                                            unsigned long long* dprof = nullptr) {
+  const int w = threadIdx.x >> 5;
+  const int ks = p.ks;
+  const int slots = kFusedWarps / ks;
+  const int slot = w / ks, kp = w - slot * ks;
+  const int64_t mtiles = (p.M + kSmallRows - 1) / kSmallRows;
+  const int64_t rgroups = fused_rgroups(p);
+  const int64_t units = rgroups * p.ncb;
+  const int cps = (p.nchunks + ks - 1) / ks;
+  const int q0 = min(p.nchunks, kp * cps), q1 = min(p.nchunks, q0 + cps);
+  const int t0 = lane & 3, g = lane >> 2;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int cb = int(u / rgroups);
+    const int64_t mt = (u - int64_t(cb) * rgroups) * slots + slot;
+    const bool live = mt < mtiles;
+    const int64_t m0 = mt * kSmallRows;
+    const bool first = u == blockIdx.x;
+    if (!first) __syncthreads();           // the previous unit is done with sB and red
+    const bool rec = dprof && threadIdx.x == 0 && first;
+    if (rec) dprof[0] = globaltimer();
+    if (threadIdx.x == 0 && !(first && prefetched)) fused_issue_b(p, u, rgroups, sB, bar);
+    // A fragments of the first k-steps while the super-core block lands
+    const bool ok0 = live && m0 + g < p.M, ok1 = live && m0 + g + 8 < p.M;
+    const double* a0 = p.in + (m0 + g) * p.K + 2 * t0;
+    const double* a1 = a0 + int64_t(8) * p.K;
+    FusedA fa, fb;
+    if (q0 < q1) fused_load_a<COHERENT>(fa, a0, a1, q0, q1, p.K, t0, ok0, ok1);
+    double c[4][4];
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) c[nb][0] = c[nb][1] = c[nb][2] = c[nb][3] = 0.0;
+    dmma::mbar_wait(bar, nwait & 1u);
+    ++nwait;
+    if (rec) dprof[1] = globaltimer();
+    if (live) {
+      for (int q = q0; q < q1; q += 2 * kFusedG) {
+        if (q + kFusedG < q1) fused_load_a<COHERENT>(fb, a0, a1, q + kFusedG, q1, p.K, t0, ok0, ok1);
+        fused_mma(fa, sB, q, q1, lane, c);
+        if (q + kFusedG >= q1) break;
+        if (q + 2 * kFusedG < q1) fused_load_a<COHERENT>(fa, a0, a1, q + 2 * kFusedG, q1, p.K, t0, ok0, ok1);
+        fused_mma(fb, sB, q + kFusedG, q1, lane, c);
+      }
+    }
+    if (rec) dprof[2] = globaltimer() + (c[0][0] == 12345.0 ? 1 : 0);
+    if (ks == 1) {
+      if (live) tile_store<4>(c, p, m0, cb * kSmallCols, lane);
+      if (rec) dprof[3] = globaltimer();
+      continue;
+    }
+    // partials [warp][value][lane]: every access is 32 consecutive doubles (no bank conflicts)
+    double* mine = red + size_t(w) * 16 * 32 + lane;
+    if (kp) {
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) mine[(nb * 4 + v) * 32] = c[nb][v];
+    }
+    __syncthreads();
+    if (kp == 0 && live) {
+      for (int j = 1; j < ks; ++j) {
+        const double* o = red + size_t(w + j) * 16 * 32 + lane;
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) c[nb][v] += o[(nb * 4 + v) * 32];
+      }
+      tile_store<4>(c, p, m0, cb * kSmallCols, lane);
+      if (rec) dprof[3] = globaltimer();
+    }
+  }
+}
+
+// The whole apply of a latency-bound problem in ONE persistent launch: the
+// plan's stages one after another, each spread over every warp of the grid
+// (fused_stage), separated by grid barriers instead of kernel boundaries; the
+// intermediates (two ping-pong buffers) stay in L2.
 __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const FusedArgs a) {
+  __shared__ __align__(16) double red[kFusedWarps * 32 * 16];   // split-K partials, 32 KiB
+  __shared__ __align__(8) uint64_t bar;
+  extern __shared__ __align__(128) unsigned char fsm[];          // the super-core block of a unit
+  double2* sB = reinterpret_cast<double2*>(fsm);
+  if (threadIdx.x == 0) {
+    dmma::mbar_init(&bar, 1);
+    dmma::fence_mbar_init();
+  }
+  __syncthreads();
   pdl_wait();
   unsigned long long* prof = a.prof ? a.prof + size_t(blockIdx.x) * kFusedProfSlots : nullptr;
   if (prof && threadIdx.x == 0) prof[0] = globaltimer();
   const int lane = threadIdx.x & 31;
-  const int64_t warp = int64_t(blockIdx.x) * kFusedWarps + (threadIdx.x >> 5);
-  const int64_t nwarps = int64_t(gridDim.x) * kFusedWarps;
+  uint32_t nwait = 0;
+  unsigned nbar = 0;
+  bool prefetched = false;
   for (int s = 0; s < a.nstages; ++s) {
-    const FusedStage& p = a.st[s];
-    const int64_t wts = (p.M + kSmallRows - 1) / kSmallRows * p.ncb;
-    for (int64_t wt = warp; wt < wts; wt += nwarps) {
+    for (int rep = 0; rep < a.repeat; ++rep) {
+      if (prof && rep + 1 == a.repeat && rep > 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) prof[2 * s] = globaltimer();   // timing of the last repeat only
+      }
+      unsigned long long* dp = prof ? prof + 2 * kFusedMaxStages + 2 + 4 * s : nullptr;
       if (s == 0)
-        small_tile<false>(p, wt, lane);
+        fused_stage<false>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp);
       else
-        small_tile<true>(p, wt, lane);
+        fused_stage<true>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp);
+      prefetched = false;
+      if (rep + 1 < a.repeat) grid_barrier(a.bar, ++nbar * gridDim.x);
     }
     if (prof) {
       __syncthreads();
       if (threadIdx.x == 0) prof[1 + 2 * s] = globaltimer();
     }
-    if (s + 1 < a.nstages) grid_barrier(a.bar, gridDim.x);
+    if (s + 1 < a.nstages) {
+      // split barrier: arrive, start the copy of the next stage's first
+      // super-core block (static data, needs nobody's output), then wait
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        grid_arrive(a.bar);
+        const FusedStage& nx = a.st[s + 1];
+        const int64_t rg = fused_rgroups(nx);
+        if (int64_t(blockIdx.x) < rg * nx.ncb) fused_issue_b(nx, blockIdx.x, rg, sB, &bar);
+        grid_wait(a.bar, ++nbar * gridDim.x);
+      } else {
+        ++nbar;
+      }
+      prefetched = int64_t(blockIdx.x) < fused_rgroups(a.st[s + 1]) * a.st[s + 1].ncb;
+      __syncthreads();
+    }
     if (prof && threadIdx.x == 0) prof[2 + 2 * s] = globaltimer();
   }
+  grid_exit(a.bar, (nbar + 1) * gridDim.x);
 }
 
 using KernelFn = void (*)(const LevelArgs, const CUtensorMap);
@@ -650,8 +847,14 @@ cudaError_t launch_small(const LevelArgs& a, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, wide::small_dmma_kernel, a);
 }
 
+cudaError_t fused_prepare() {
+  return cudaFuncSetAttribute(wide::fused_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(kFusedMaxBBytes));
+}
+
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st) {
-  if (grid < 1 || a.nstages < 1 || a.nstages > kFusedMaxStages) return cudaErrorInvalidValue;
+  if (grid < 1 || a.nstages < 1 || a.nstages > kFusedMaxStages || a.smem > kFusedMaxBBytes)
+    return cudaErrorInvalidValue;
   static const bool no_coop = std::getenv("QTT_FUSED_NOCOOP") != nullptr;   // diagnostic (A/B of launch cost)
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;     // co-residency for the grid barrier
@@ -661,7 +864,7 @@ cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(kFusedWarps * 32);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = a.smem;
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
