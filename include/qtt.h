@@ -366,6 +366,11 @@ qtt_status_t qtt_get_stage_split(qtt_handle_t h, int s, int64_t nrhs, int* kspli
 qtt_status_t qtt_get_apply_plan(qtt_handle_t h, int64_t nrhs, int* launches, int* n_stages, int* k_first,
                                 int* k_last, int* variant);
 
+/* qtt_set_fused -- enable (1, the default) or disable (0) the fused one-launch
+ * apply on this handle; disabled, every apply runs the per-stage plan.  Host
+ * only; affects applies enqueued after the call. */
+qtt_status_t qtt_set_fused(qtt_handle_t h, int enable);
+
 /*
  * Stage timing (for the bench's roofline): when enabled, each apply records
  * a CUDA event pair around every stage launch on the apply stream.

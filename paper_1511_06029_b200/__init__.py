@@ -242,12 +242,14 @@ def morton_unpack(x, dim: int, levels: int, out=None, stream=None):
 class QttOperator:
     """A QTT matrix resident on the current CUDA device; ``apply`` computes y = A x."""
 
-    def __init__(self, cores, ranks=None, max_stage_levels: int | None = None):
+    def __init__(self, cores, ranks=None, max_stage_levels: int | None = None, fused: bool = True):
         self._h = None
         if max_stage_levels is None:
             self._h = qtt_create(cores, ranks)
         else:
             self._h = qtt_create_ex(cores, ranks, max_stage_levels)
+        if not fused:
+            self.set_fused(False)
         info = qtt_get_info(self._h)
         import torch
         self.device = torch.device("cuda", torch.cuda.current_device())   # where qtt_create put the cores
@@ -388,6 +390,10 @@ class QttOperator:
             return [dict(s_, ksplit=1) for s_ in st]
         return [dict(qtt_get_stage(self.handle, s), ksplit=qtt_get_stage_split(self.handle, s, nrhs))
                 for s in range(self.launches_per_apply)]
+
+    def set_fused(self, enable: bool = True):
+        """Allow (default) or forbid the fused one-launch apply on this handle."""
+        _lib.check("qtt_set_fused", _lib.load().qtt_set_fused(self.handle, 1 if enable else 0))
 
     def launches(self, nrhs: int = 1) -> int:
         """Kernel launches of one apply with `nrhs` RHS (1 for a fused apply)."""

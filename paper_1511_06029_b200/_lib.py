@@ -21,7 +21,7 @@ QTT_ERROR_CUDA = 4
 # every symbol include/qtt.h declares
 SYMBOLS = (
     "qtt_status_string", "qtt_create", "qtt_create_ex", "qtt_plan_stages", "qtt_plan_stages_split", "qtt_apply", "qtt_workspace_size", "qtt_apply_ws",
-    "qtt_apply_host", "qtt_get_info", "qtt_get_stage", "qtt_get_stage_split", "qtt_get_apply_plan", "qtt_set_stage_timing",
+    "qtt_apply_host", "qtt_get_info", "qtt_get_stage", "qtt_get_stage_split", "qtt_get_apply_plan", "qtt_set_fused", "qtt_set_stage_timing",
     "qtt_stage_times", "qtt_destroy", "qtt_morton_pack", "qtt_morton_unpack", "qtt_apply_grid",
     "qtt_product_create", "qtt_product_workspace_size", "qtt_product_apply", "qtt_product_apply_ws",
     "qtt_product_destroy", "qtt_compressed_matvec", "qtt_compressed_matvec_cores",
@@ -72,6 +72,8 @@ def load():
     lib.qtt_get_stage.argtypes = [h, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.qtt_get_stage_split.restype = st
     lib.qtt_get_stage_split.argtypes = [h, C.c_int, C.c_int64, C.POINTER(C.c_int)]
+    lib.qtt_set_fused.restype = st
+    lib.qtt_set_fused.argtypes = [h, C.c_int]
     lib.qtt_get_apply_plan.restype = st
     lib.qtt_get_apply_plan.argtypes = [h, C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p, C.c_void_p,
                                        C.c_void_p]

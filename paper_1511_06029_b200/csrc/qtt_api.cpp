@@ -488,6 +488,33 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
   }
 }
 
+}  // extern "C"
+
+namespace qtt {
+namespace rt {
+qtt_status_t grid_apply_fused(qtt_plan* h, const double* grid_in, double* grid_out, int64_t nrhs, int dim,
+                              cudaStream_t st) {
+  if (!use_fused(h, nrhs) || rhs_group(h, nrhs) < nrhs) return QTT_ERROR_NOT_SUPPORTED;
+  qtt_status_t s = check_apply_args(h, grid_in, grid_out, nrhs);
+  if (s != QTT_SUCCESS) return s;
+  const bool capturing = stream_is_capturing(st);
+  void* old_ws = h->ws;
+  bool grew = false;
+  s = cached_acquire(&h->ws, &h->ws_bytes, &h->ws_used, h->ws_pending, ws_bytes_for(h, nrhs), st, capturing, &grew);
+  if (grew) {
+    drop_graphs_on(h, old_ws);
+    h->ws_header_zero = false;
+  }
+  if (s == QTT_SUCCESS) s = enqueue_fused(h, grid_in, grid_out, nrhs, h->ws, st, !h->ws_header_zero, dim);
+  if (s == QTT_SUCCESS) h->ws_header_zero = true;
+  if (s == QTT_SUCCESS) s = cached_release(h->ws_used, &h->ws_pending, st, capturing);
+  return s;
+}
+}  // namespace rt
+}  // namespace qtt
+
+extern "C" {
+
 qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host, int64_t nrhs,
                             qtt_stream_t stream) {
   if (!h || !x_host || !y_host || nrhs < 1) return QTT_ERROR_INVALID_VALUE;
@@ -586,6 +613,12 @@ qtt_status_t qtt_get_apply_plan(qtt_handle_t h, int64_t nrhs, int* launches, int
     if (k_last) k_last[i] = S[i].plan.k1;
     if (variant) variant[i] = fused ? int(qtt::kFused) : S[i].plan.variant;
   }
+  return QTT_SUCCESS;
+}
+
+qtt_status_t qtt_set_fused(qtt_handle_t h, int enable) {
+  if (!h) return QTT_ERROR_INVALID_VALUE;
+  h->fused_on = enable != 0;
   return QTT_SUCCESS;
 }
 

@@ -52,6 +52,9 @@ qtt_status_t qtt_apply_grid(qtt_handle_t h, const double* grid_in, double* grid_
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   try {
     DeviceGuard g(h->device);
+    // a fused apply gathers / scatters the Morton order in its first / last
+    // stage: one launch, no staging vectors
+    if (use_fused(h, nrhs) && rhs_group(h, nrhs) >= nrhs) return grid_apply_fused(h, grid_in, grid_out, nrhs, dim, st);
     const size_t elems = size_t(h->N) * size_t(nrhs);
     const bool capturing = stream_is_capturing(st);
     // the staging vectors are shared by the handle's grid applies: order this

@@ -219,6 +219,11 @@ struct FusedStage {
   int64_t out_limit = 0;           // QTT_BOUNDS_CHECK builds
   int log2_q = 0, n_i = 2, r_out = 0, nout = 0, K = 0, nchunks = 0, ncb = 0;
   int ks = 1;                      // warps per tile (intra-CTA split of the k-steps; 1, 2, 4 or 8)
+  // Morton order fused into the grid apply (qtt_apply_grid): the first stage
+  // gathers its input from a natural-order grid (min_dim), the last stage
+  // scatters its output into one (mout_dim); 0 = QTT order.  levels per axis
+  // = log2n / dim.
+  int min_dim = 0, mout_dim = 0, log2n = 0;
 };
 struct FusedArgs {
   FusedStage st[kFusedMaxStages];
@@ -234,6 +239,15 @@ struct FusedArgs {
 constexpr int kFusedProfSlots = 2 * kFusedMaxStages + 2 + 4 * kFusedMaxStages;
 cudaError_t fused_prepare();   // sets the kernel's max dynamic smem
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st);
+// natural-grid offset of QTT index q within one RHS (Morton order, R18)
+QTT_HD inline int64_t morton_natural(int64_t q, int dim, int levels) {
+  int64_t c[3] = {0, 0, 0};
+  for (int l = 0; l < levels; ++l)
+    for (int a = 0; a < dim; ++a) c[a] |= ((q >> (dim * l + a)) & 1) << l;
+  int64_t off = 0;
+  for (int a = dim - 1; a >= 0; --a) off = (off << levels) | c[a];
+  return off;
+}
 // y[s][c] = sum_g recv[g][s][c] (fixed order g = 0..parts-1), qtt_wide_kernel.cu
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,
                                 int num_sms);

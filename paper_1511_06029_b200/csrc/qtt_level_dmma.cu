@@ -180,6 +180,94 @@ __global__ void __launch_bounds__(256) diag_out_kernel(const LevelArgs p) {
   }
 }
 
+// Diagonal stage, streaming form (r_out <= 8): the input rows are one
+// contiguous stream -- chunks of kDiagChunk consecutive rows (chunk c = rows
+// c*128 .. c*128+127 of all nrhs*M*n_i input rows) move HBM -> smem with one
+// TMA bulk copy each, kDiagStages chunks in flight per CTA (persistent CTAs,
+// chunks round-robin), so every byte of x is read once, in full lines, with
+// the copy engine doing the addressing.  Two threads per row: thread h of
+// row r sums a = h, h + 2, ... (fixed order), the pair adds its halves with
+// one shuffle (commutative: both lanes hold the same sum), the even lane
+// stores the row's r_out outputs.  D[ii] (ii = row mod n_i; consecutive rows,
+// consecutive ii) is read from L2.
+constexpr int kDiagChunk = 128;
+constexpr int kDiagStages = 3;
+
+__global__ void __launch_bounds__(256) diag_stream_kernel(const LevelArgs p) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t full[kDiagStages];
+  const int r_in = p.r_in, r_out = p.r_out, n_i = p.n_i;
+  const int64_t rows = p.M * n_i;
+  const int64_t chunks = (rows + kDiagChunk - 1) / kDiagChunk;
+  const size_t stage_bytes = size_t(kDiagChunk) * r_in * sizeof(double);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDiagStages; ++s) dmma::mbar_init(&full[s], 1);
+    dmma::fence_mbar_init();
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  auto issue = [&](int64_t c, int s) {
+    const int64_t r0 = c * kDiagChunk;
+    const int64_t nr = rows - r0 < kDiagChunk ? rows - r0 : kDiagChunk;   // even (rows = nrhs 2^d)
+    const uint32_t bytes = uint32_t(nr * r_in * sizeof(double));
+    dmma::mbar_arrive_expect_tx(&full[s], bytes);
+    dmma::bulk_g2s(dsm + size_t(s) * stage_bytes, p.in + r0 * r_in, bytes, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kDiagStages; ++s) {
+      const int64_t c = blockIdx.x + int64_t(s) * gridDim.x;
+      if (c < chunks) issue(c, s);
+    }
+  const int r = threadIdx.x >> 1, h = threadIdx.x & 1;
+  uint32_t phase = 0;
+  int s = 0;
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    dmma::mbar_wait(&full[s], phase);
+    const int64_t R = c * kDiagChunk + r;
+    const bool live = R < rows;
+    const int64_t m = live ? R / n_i : 0;
+    const int ii = live ? int(R - m * n_i) : 0;
+    const double* xr = reinterpret_cast<const double*>(dsm + size_t(s) * stage_bytes) + size_t(r) * r_in;
+    const double* D = p.core + size_t(ii) * r_in * r_out;
+    double acc[kDiagMaxROut];
+#pragma unroll
+    for (int b = 0; b < kDiagMaxROut; ++b) acc[b] = 0.0;
+    if (live) {
+#pragma unroll 4
+      for (int a = h; a < r_in; a += 2) {
+        const double xa = xr[a];
+#pragma unroll
+        for (int b = 0; b < kDiagMaxROut; ++b)
+          if (b < r_out) acc[b] = fma(xa, __ldg(D + size_t(a) * r_out + b), acc[b]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kDiagMaxROut; ++b)
+      if (b < r_out) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], 1);
+    if (live && h == 0) {
+      const int64_t row = m + (((m >> p.log2_q) * (n_i - 1)) << p.log2_q) + (int64_t(ii) << p.log2_q);
+#pragma unroll
+      for (int b = 0; b < kDiagMaxROut; ++b)
+        if (b < r_out) {
+          QTT_CHECK_OUT(p, p.out + row * r_out + b, 1);
+          p.out[row * r_out + b] = acc[b];
+        }
+    }
+    __syncthreads();                        // stage s consumed
+    if (threadIdx.x == 0) {
+      const int64_t cn = c + int64_t(kDiagStages) * gridDim.x;
+      if (cn < chunks) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(cn, s);
+      }
+    }
+    if (++s == kDiagStages) {
+      s = 0;
+      phase ^= 1u;
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms) {
@@ -199,6 +287,27 @@ cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms) {
     co.attrs = attro;
     co.numAttrs = 1;
     return cudaLaunchKernelEx(&co, diag_out_kernel, a);
+  }
+  static const bool no_stream = std::getenv("QTT_DIAG_NO_STREAM") != nullptr;   // diagnostic (A/B)
+  if (!no_stream) {   // the streaming form (TMA chunks of consecutive input rows)
+    const size_t smem = size_t(kDiagStages) * kDiagChunk * a.r_in * sizeof(double);
+    static cudaError_t attr_ok = cudaFuncSetAttribute(diag_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      int(kDiagStages * kDiagChunk * kDiagMaxRin * sizeof(double)));
+    if (attr_ok != cudaSuccess) return attr_ok;
+    const int64_t chunks = (a.M * a.n_i + kDiagChunk - 1) / kDiagChunk;
+    int64_t blocks = chunks < num_sms ? chunks : num_sms;
+    if (blocks < 1) blocks = 1;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cudaLaunchConfig_t cs = {};
+    cs.gridDim = dim3(unsigned(blocks));
+    cs.blockDim = dim3(256);
+    cs.dynamicSmemBytes = smem;
+    cs.stream = st;
+    cs.attrs = attrs;
+    cs.numAttrs = 1;
+    return cudaLaunchKernelEx(&cs, diag_stream_kernel, a);
   }
   const bool lane_ii = a.M < 32;
   const int64_t warps = lane_ii ? a.M * ((a.n_i + 31) / 32) : (a.M + 31) / 32 * a.n_i;

@@ -486,11 +486,11 @@ qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void
 }
 
 bool use_fused(const qtt_plan* h, int64_t nrhs) {
-  return !h->fstages.empty() && nrhs <= h->fused_max_nrhs && !h->timing && h->shard_bits == 0;
+  return h->fused_on && !h->fstages.empty() && nrhs <= h->fused_max_nrhs && !h->timing && h->shard_bits == 0;
 }
 
 qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
-                           bool zero_bar) {
+                           bool zero_bar, int morton_dim) {
   unsigned char* base = static_cast<unsigned char*>(ws);
   const size_t bb = ws_buf_bytes(h, nrhs);
   double* buf[2] = {reinterpret_cast<double*>(base + kWsHeader), reinterpret_cast<double*>(base + kWsHeader + bb)};
@@ -517,6 +517,9 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
     f.nchunks = sp.nchunks;
     f.ncb = sp.ncb;
     f.ks = std::max(1, sp.ksplit);
+    f.log2n = h->d;
+    f.min_dim = s == 0 ? morton_dim : 0;
+    f.mout_dim = last ? morton_dim : 0;
     a.smem = std::max<size_t>(a.smem, size_t(sp.nchunks) * 128 * 16);
     max_wt = std::max<int64_t>(max_wt, (f.M + qtt::kSmallRows - 1) / qtt::kSmallRows * f.ncb * f.ks);
     in = f.out;

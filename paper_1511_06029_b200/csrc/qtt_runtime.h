@@ -59,6 +59,7 @@ struct qtt_plan {
   std::vector<Stage> fstages;
   int64_t fused_max_nrhs = 0;
   bool ws_header_zero = false;     // the cached workspace's grid-barrier words are 0
+  bool fused_on = true;            // qtt_set_fused
   // cached workspace (qtt_apply, qtt_apply_host, shard applies) and the event
   // recorded after the last apply that used it (cross-stream ordering; no
   // caller stream is kept beyond a call)
@@ -246,7 +247,11 @@ qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nr
 // grid-barrier words first (a workspace not known to hold them at 0)
 bool use_fused(const qtt_plan* h, int64_t nrhs);
 qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
-                           bool zero_bar);
+                           bool zero_bar, int morton_dim = 0);
+// qtt_apply_grid through the fused apply: the Morton gather / scatter happen
+// in its first / last stage (qtt_api.cpp); NOT_SUPPORTED when the apply is not fused
+qtt_status_t grid_apply_fused(qtt_plan* h, const double* grid_in, double* grid_out, int64_t nrhs, int dim,
+                              cudaStream_t st);
 // true while `st` is being captured into a CUDA graph (ours or the caller's)
 bool stream_is_capturing(cudaStream_t st);
 // Grow-only device buffers cached per handle (workspace, grid staging,

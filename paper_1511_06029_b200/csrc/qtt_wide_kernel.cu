@@ -104,10 +104,40 @@ __device__ __forceinline__ void chunk_mma(double (&c)[NBC][4], const unsigned ch
 
 // Row-separation epilogue (Alg. 2 line 8 for all L levels): column n = ii*r_out + b
 // of GEMM row m goes to out[(m + Q*(s*(n_i-1) + ii)) * r_out + b], s = m / Q.
+__device__ __forceinline__ int mout_dim(const LevelArgs&) { return 0; }
+__device__ __forceinline__ int mout_dim(const FusedStage& p) { return p.mout_dim; }
+__device__ __forceinline__ int mout_log2n(const LevelArgs&) { return 0; }
+__device__ __forceinline__ int mout_log2n(const FusedStage& p) { return p.log2n; }
+
 template <int NBC, class P>
 __device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const P& p, int64_t m_first,
                                            int n_first, int lane) {
   const int g = lane >> 2, t0 = lane & 3;
+  const int md = mout_dim(p);
+  if (md) {
+    // last stage of a fused grid apply (r_out = 1): output row o of RHS s goes
+    // to the natural-order grid at s N + morton_natural(o mod N)
+    const int log2n = mout_log2n(p);
+    const int64_t nmask = (int64_t(1) << log2n) - 1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t m = m_first + g + 8 * h;
+      if (m >= p.M) continue;
+      const int64_t rowbase = m + (((m >> p.log2_q) * (p.n_i - 1)) << p.log2_q);
+#pragma unroll
+      for (int nb = 0; nb < NBC; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = n_first + nb * 8 + 2 * t0 + e;
+          if (n >= p.nout) continue;
+          const int64_t o = rowbase + (int64_t(n) << p.log2_q);
+          double* dst = p.out + (o & ~nmask) + morton_natural(o & nmask, md, log2n / md);
+          QTT_CHECK_OUT(p, dst, 1);
+          *dst = c[nb][2 * h + e];
+        }
+    }
+    return;
+  }
   const int r_out = p.r_out;
   const bool vec = (r_out % 2) == 0;
   // (ii, b) of this lane's first column, then advanced by 8 columns per n-block
@@ -517,9 +547,18 @@ struct FusedA {
   double2 x[kFusedG], y[kFusedG];
 };
 
+// Morton gather (first stage of a fused grid apply, r_in = 1): A element at
+// flat QTT offset f of the input is the grid value at morton_natural(f);
+// f even, so (f, f + 1) differ in the x bit 0 and stay one aligned double2.
+__device__ __forceinline__ const double* morton_src(const double* base, const double* ptr, const FusedStage& p) {
+  const int64_t f = ptr - base;
+  const int64_t nmask = (int64_t(1) << p.log2n) - 1;
+  return base + (f & ~nmask) + morton_natural(f & nmask, p.min_dim, p.log2n / p.min_dim);
+}
+
 template <bool COHERENT>
 __device__ __forceinline__ void fused_load_a(FusedA& o, const double* a0, const double* a1, int q, int q1, int K,
-                                             int t0, bool ok0, bool ok1) {
+                                             int t0, bool ok0, bool ok1, const FusedStage& p) {
 #pragma unroll
   for (int j = 0; j < kFusedG; ++j) {
     const int qq = q + j;
@@ -528,6 +567,10 @@ __device__ __forceinline__ void fused_load_a(FusedA& o, const double* a0, const 
     o.y[j] = make_double2(0.0, 0.0);
     const double2* pa0 = reinterpret_cast<const double2*>(a0 + qq * kSmallK);
     const double2* pa1 = reinterpret_cast<const double2*>(a1 + qq * kSmallK);
+    if (!COHERENT && p.min_dim) {
+      pa0 = reinterpret_cast<const double2*>(morton_src(p.in, a0 + qq * kSmallK, p));
+      pa1 = reinterpret_cast<const double2*>(morton_src(p.in, a1 + qq * kSmallK, p));
+    }
     if (vk && ok0) o.x[j] = COHERENT ? __ldcg(pa0) : __ldg(pa0);
     if (vk && ok1) o.y[j] = COHERENT ? __ldcg(pa1) : __ldg(pa1);
   }
@@ -610,7 +653,7 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
     const double* a0 = p.in + (m0 + g) * p.K + 2 * t0;
     const double* a1 = a0 + int64_t(8) * p.K;
     FusedA fa, fb;
-    if (q0 < q1) fused_load_a<COHERENT>(fa, a0, a1, q0, q1, p.K, t0, ok0, ok1);
+    if (q0 < q1) fused_load_a<COHERENT>(fa, a0, a1, q0, q1, p.K, t0, ok0, ok1, p);
     double c[4][4];
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb) c[nb][0] = c[nb][1] = c[nb][2] = c[nb][3] = 0.0;
@@ -619,10 +662,10 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
     if (rec) dprof[1] = globaltimer();
     if (live) {
       for (int q = q0; q < q1; q += 2 * kFusedG) {
-        if (q + kFusedG < q1) fused_load_a<COHERENT>(fb, a0, a1, q + kFusedG, q1, p.K, t0, ok0, ok1);
+        if (q + kFusedG < q1) fused_load_a<COHERENT>(fb, a0, a1, q + kFusedG, q1, p.K, t0, ok0, ok1, p);
         fused_mma(fa, sB, q, q1, lane, c);
         if (q + kFusedG >= q1) break;
-        if (q + 2 * kFusedG < q1) fused_load_a<COHERENT>(fa, a0, a1, q + 2 * kFusedG, q1, p.K, t0, ok0, ok1);
+        if (q + 2 * kFusedG < q1) fused_load_a<COHERENT>(fa, a0, a1, q + 2 * kFusedG, q1, p.K, t0, ok0, ok1, p);
         fused_mma(fb, sB, q + kFusedG, q1, lane, c);
       }
     }

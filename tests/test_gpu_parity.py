@@ -25,8 +25,15 @@ def qtt():
     return q
 
 
+def _per_stage(q, *a, **k):
+    """An operator whose applies run the per-stage plan: these tests exercise
+    the stage kernels (the fused one-launch apply has tests/test_gpu_fused.py)."""
+    k.setdefault("fused", False)
+    return q.QttOperator(*a, **k)
+
+
 def gpu_apply(q, cores, x, max_stage_levels=None, **kw):
-    op = q.QttOperator(cores, max_stage_levels=max_stage_levels)
+    op = _per_stage(q, cores, max_stage_levels=max_stage_levels)
     try:
         xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
         y = op.apply(xt, **kw)
@@ -135,7 +142,7 @@ SPLIT_CASES = [
 def test_split_k_stages(qtt, d, r, nrhs):
     ranks = [1] + [r] * (d - 1) + [1]
     _, cores, x = random_case(5000 + 7 * d + r, d, r, nrhs, ranks=ranks)
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         splits = op.stage_splits(nrhs)
         assert max(splits) > 1, (op.stages(), splits)
@@ -160,7 +167,7 @@ def test_repeated_applies_alternating_inputs_bitwise(qtt):
     alternating inputs; every result bitwise equal to the first of its input."""
     cfg, cores, x = generate("c3")
     x2 = np.ascontiguousarray(x[:, ::-1])
-    with qtt.QttOperator(cores) as op:
+    with _per_stage(qtt, cores) as op:
         assert max(op.stage_splits(1)) > 1
         xs = [torch.from_numpy(x).cuda(), torch.from_numpy(x2).cuda()]
         refs = [op.apply(v).clone() for v in xs]
@@ -182,7 +189,7 @@ def test_repeated_applies_split_stage_bie_y(qtt):
     from qtt_workload import bie_case
     _, _, _, Y, x = bie_case(0, 21, 9, 95, 50, 1)
     x2 = np.ascontiguousarray(x[:, ::-1])
-    with qtt.QttOperator(Y) as op:
+    with _per_stage(qtt, Y) as op:
         assert max(op.stage_splits(1)) > 1
         xs = [torch.from_numpy(v).cuda() for v in (x, x2)]
         refs = [op.apply(v).clone() for v in xs]
@@ -201,7 +208,7 @@ def test_split_k_matches_unsplit_host_path(qtt):
     d, r = 18, 64
     ranks = [1] + [r] * (d - 1) + [1]
     _, cores, x = random_case(6061, d, r, 1, ranks=ranks)
-    with qtt.QttOperator(cores) as op:
+    with _per_stage(qtt, cores) as op:
         assert max(op.stage_splits(1)) > 1
         yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
         yh = op.apply_host(x)
@@ -256,7 +263,7 @@ def test_diagonal_stage_host_apply_bitwise(qtt):
     offsets): bitwise equal to the device apply."""
     from qtt_workload import bie_case
     _, M, _, _, x = bie_case(4, 16, 9, 12, 8, 1)
-    with qtt.QttOperator(M) as op:
+    with _per_stage(qtt, M) as op:
         assert op.stages()[-1]["variant"] == "diag", op.stages()
         yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
         np.testing.assert_array_equal(op.apply_host(x), yd)
@@ -288,7 +295,7 @@ def test_merged_stage_limits(qtt, maxL, seed, d, maxr, nrhs):
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
 def test_config_plan_has_merged_stages(qtt, name):
     cfg, cores, _ = generate(name, with_x=False)
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         st = op.stages()
     finally:
@@ -330,7 +337,7 @@ from test_gpu_parity import WIDE_CASES
 for ranks, nrhs in WIDE_CASES:
     d = len(ranks) - 1
     _, cores, x = random_case(300 + d + nrhs, d, max(ranks), nrhs, ranks=ranks)
-    with q.QttOperator(cores) as op:
+    with q.QttOperator(cores, fused=False) as op:
         st = op.stages()
         assert any(s["variant"] == "wide" for s in st) and not any(s["variant"] == "small" for s in st), st
         y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
@@ -427,7 +434,7 @@ def test_full_size_kronecker_vector(qtt, name):
 # ------------------------------------------------------------------ determinism, streams, ABI
 def test_determinism_and_stream(qtt):
     _, cores, x = generate("c2")
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     xt = torch.from_numpy(x).cuda()
     y1 = op.apply(xt)
     s = torch.cuda.Stream()
@@ -451,7 +458,7 @@ def test_abi_errors(qtt):
     lib = qtt._lib.load()
     import ctypes as C
     _, cores, x = generate("c1")
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     h = op.handle
     N = op.N
     xt = torch.from_numpy(x).cuda()
@@ -493,7 +500,7 @@ def test_apply_does_not_block_the_host(qtt):
     host call (graph replay after the first apply) returns in a small fraction."""
     import time
     cfg, cores, x = generate("c4")
-    with qtt.QttOperator(cores) as op:
+    with _per_stage(qtt, cores) as op:
         xt = torch.from_numpy(x).cuda()
         y = torch.empty_like(xt)
         op.apply(xt, out=y)
@@ -514,7 +521,7 @@ def test_core_arrays_may_be_freed_after_create(qtt):
     arrays afterwards does not change the operator."""
     _, cores, x = random_case(4321, 12, 9, 2)
     keep = [c.copy() for c in cores]
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         for c in cores:
             c.fill(np.nan)
@@ -529,7 +536,7 @@ def test_transpose_of(qtt):
     """QttOperator.transpose_of(cores) applies A^T: against the oracle on the
     pinned transpose (oracle.transpose), and <u, A v> = <A^T u, v>."""
     _, cores, x = random_case(4545, 12, 9, 2)
-    with qtt.QttOperator.transpose_of(cores) as opT, qtt.QttOperator(cores) as op:
+    with qtt.QttOperator.transpose_of(cores) as opT, _per_stage(qtt, cores) as op:
         xt = torch.from_numpy(x).cuda()
         yT = opT.apply(xt).cpu().numpy()
         y = op.apply(xt).cpu().numpy()
@@ -547,7 +554,7 @@ def test_operator_from_ttb1_file(qtt, tmp_path):
     _, cores, x = generate("c2")
     ttb1.save(tmp_path / "c2.ttb1", cores)
     xt = torch.from_numpy(x).cuda()
-    with qtt.QttOperator.from_ttb1(tmp_path / "c2.ttb1") as a, qtt.QttOperator(cores) as b:
+    with qtt.QttOperator.from_ttb1(tmp_path / "c2.ttb1") as a, _per_stage(qtt, cores) as b:
         assert torch.equal(a.apply(xt), b.apply(xt))
 
 
@@ -557,7 +564,7 @@ def test_perf_regression_c4(qtt):
     runs at ~105% on that basis (55.2 ms), so the bound only catches gross
     regressions.  Median of 5 applies, CUDA events."""
     cfg, cores, x = generate("c4")
-    with qtt.QttOperator(cores) as op:
+    with _per_stage(qtt, cores) as op:
         xt = torch.from_numpy(x).cuda()
         y = torch.empty_like(xt)
         ts = []
@@ -616,7 +623,7 @@ def test_caller_graph_capture(qtt):
     _, cores, x = generate("c2")
     xt = torch.from_numpy(x).cuda()
     s = torch.cuda.Stream()
-    with qtt.QttOperator(cores) as op:
+    with _per_stage(qtt, cores) as op:
         ref = op.apply(xt).clone()
         torch.cuda.synchronize()
         y = torch.empty_like(xt)
@@ -630,7 +637,7 @@ def test_caller_graph_capture(qtt):
             assert torch.equal(y, ref)
         assert torch.equal(op.apply(xt), ref)
         del g
-    with qtt.QttOperator(cores) as op:
+    with _per_stage(qtt, cores) as op:
         g = torch.cuda.CUDAGraph()
         y = torch.empty_like(xt)
         with pytest.raises(qtt.QttError):
@@ -645,7 +652,7 @@ def test_graph_replay_matches_plain_enqueue(qtt):
     bitwise that of the plain per-stage enqueue (stage timing on disables graphs),
     across alternating buffers, RHS counts and a non-default stream."""
     _, cores, x = random_case(31, 12, 9, 3)
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         xs = [torch.from_numpy(x).cuda(), torch.from_numpy(x[::-1].copy()).cuda(), torch.from_numpy(x[:1].copy()).cuda()]
         op.set_stage_timing(True)
@@ -676,7 +683,7 @@ def test_apply_host_pipelined_bitwise(qtt, name):
     with the last stage (chunked launches of the same kernels): bitwise equal
     to the device apply."""
     cfg, cores, x = generate(name)
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
         xh = torch.from_numpy(x).pin_memory()
@@ -703,7 +710,7 @@ for name, dr in cases:
     else:
         d, r = dr
         _, cores, x = random_case(6061, d, r, 1, ranks=[1] + [r] * (d - 1) + [1])
-    with q.QttOperator(cores) as op:
+    with q.QttOperator(cores, fused=False) as op:
         yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
         for _ in range(2):
             yh = op.apply_host(x)
@@ -738,7 +745,7 @@ cases = [(1, 1, 1, 1), (2, 2, 2, 5), (3, 3, 3, 7), (4, 6, 7, 3), (5, 9, 13, 2), 
 n_small = 0
 for seed, d, r, nrhs in cases:
     _, cores, x = random_case(seed + 900, d, r, nrhs)
-    with q.QttOperator(cores) as op:
+    with q.QttOperator(cores, fused=False) as op:
         n_small += sum(s["variant"] == "small" for s in op.stages())
         y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
     oracle.assert_close(y, oracle.apply_alg2(cores, x))
@@ -767,7 +774,7 @@ def test_shift_large_d_bitwise(qtt, d, s, nrhs):
     rank-2 cyclic shift is np.roll / torch.roll bitwise."""
     gen = torch.Generator(device="cuda").manual_seed(d)
     x = torch.randn((nrhs, 1 << d), dtype=torch.float64, device="cuda", generator=gen)
-    op = qtt.QttOperator(CF.shift_cores(d, s))
+    op = _per_stage(qtt, CF.shift_cores(d, s))
     try:
         y = op.apply(x)
         torch.cuda.synchronize()
@@ -783,7 +790,7 @@ def test_back_to_back_applies_on_two_streams(qtt):
     one on stream A (no host sync between) is ordered after it by the library."""
     cfg, cores, x = generate("c3")
     x2 = np.ascontiguousarray(x[:, ::-1])
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         ref1 = op.apply(torch.from_numpy(x).cuda())
         ref2 = op.apply(torch.from_numpy(x2).cuda())
@@ -807,7 +814,7 @@ def test_cached_ws_ordered_across_caller_ws_apply(qtt):
     C is ordered after A (the cached workspace's own event), not after B."""
     cfg, cores, x = generate("c3")
     xs = [x, np.ascontiguousarray(x[:, ::-1]), np.ascontiguousarray(-x)]
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         refs = [op.apply(torch.from_numpy(v).cuda()) for v in xs]
         torch.cuda.synchronize()
@@ -834,13 +841,13 @@ def test_cached_ws_grows_on_another_stream(qtt):
     on b after a's apply (stream-ordered), and both results are right."""
     cfg, cores, x = generate("c3")
     x4 = np.ascontiguousarray(np.concatenate([x, -x, 2 * x, x[:, ::-1]]))
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         ref1 = op.apply(torch.from_numpy(x).cuda())
         ref4 = op.apply(torch.from_numpy(x4).cuda())
         torch.cuda.synchronize()
         for _ in range(2):
-            op2 = qtt.QttOperator(cores)            # a fresh handle: workspace sized for nrhs = 1
+            op2 = _per_stage(qtt, cores)            # a fresh handle: workspace sized for nrhs = 1
             a, b = torch.cuda.Stream(), torch.cuda.Stream()
             xa, xb = torch.from_numpy(x).cuda(), torch.from_numpy(x4).cuda()
             torch.cuda.synchronize()
@@ -862,7 +869,7 @@ def test_grid_apply_two_streams(qtt):
     rng = np.random.default_rng(1)
     g1 = rng.standard_normal((1, 1 << d))
     g2 = rng.standard_normal((1, 1 << d))
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         r1 = op.apply_grid(torch.from_numpy(g1).cuda(), dim=3)
         r2 = op.apply_grid(torch.from_numpy(g2).cuda(), dim=3)
@@ -882,7 +889,7 @@ def test_grid_apply_two_streams(qtt):
 
 def test_apply_host_out_validation(qtt):
     _, cores, x = random_case(5, 8, 4, nrhs=2)
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         ref = op.apply_host(x)
         for bad in (np.empty(x.shape, dtype=np.float32), np.empty((x.shape[1],)),
@@ -953,7 +960,7 @@ def test_graph_cache_eviction_and_workspace_growth(qtt):
     workspace is reallocated and graphs on the old one dropped): every result
     stays bitwise equal to the plain enqueue."""
     _, cores, x = random_case(41, 13, 20, 4)
-    op = qtt.QttOperator(cores)
+    op = _per_stage(qtt, cores)
     try:
         xs = [torch.from_numpy(np.ascontiguousarray(np.roll(x, k, axis=1))).cuda() for k in range(11)]
         op.set_stage_timing(True)

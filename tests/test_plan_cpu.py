@@ -168,3 +168,29 @@ def test_super_core_is_the_qtt_definition(q, ranks, k0, k1):
             last = sub[-1][..., b:b + 1]
             closed = [first] + sub[1:-1] + [last] if L > 1 else [sub[0][a:a + 1, :, :, b:b + 1]]
             np.testing.assert_allclose(W[a, :, :, b], oracle.dense_matrix(closed), rtol=1e-12, atol=1e-12)
+
+
+def test_forced_stage_split_switch():
+    """QTT_PLAN_FORCE_STAGES (A/B diagnostic, read once per process) forces the
+    partition when it covers 1..d with coverable stages, and is ignored
+    otherwise (the default plan stays)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, sys.argv[1]); import paper_1511_06029_b200 as q; "
+            "from qtt_workload import configs; r = configs.config_ranks('c4'); "
+            "print([(a, b) for a, b, _ in q.qtt_plan_stages(r, 0, 10)])")
+    def run(spec):
+        env = dict(os.environ)
+        if spec is not None:
+            env["QTT_PLAN_FORCE_STAGES"] = spec
+        r = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        return eval(r.stdout.strip().splitlines()[-1])
+    default = run(None)
+    pairs = "1-7,8-9,10-11,12-13,14-15,16-17,18-24"
+    assert run(pairs) == [(1, 7), (8, 9), (10, 11), (12, 13), (14, 15), (16, 17), (18, 24)]
+    assert run("1-7,8-9") == default            # does not reach d = 24
+    assert run("2-24") == default               # does not start at level 1
+    assert run("garbage") == default
