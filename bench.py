@@ -552,6 +552,7 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
         out["product_c4xc4"] = {"ms_per_apply": pm, "gflops_alg2": F / (pm * 1e-3) / 1e9}
         gm, _ = time_applies(lambda: M.apply_grid(x, 3, out=y, stream=stream), 5, 2, stream)
         out["grid_apply_c4"] = {"ms_per_apply": gm, "gflops_alg2": M.flops_per_rhs / (gm * 1e-3) / 1e9}
+        del x, y, ws
     # grid apply at the latency-bound sizes (16^3, 32^3): the fused apply gathers /
     # scatters the Morton order in its first / last stage, against the plain apply
     for name in ("c1", "c2"):
@@ -566,7 +567,6 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
                                          "note": "natural-order 3-D grid in and out (Morton pack/unpack "
                                                  "inside the one fused launch)" if op_.launches(1) == 1 else
                                                  "Morton pack + stages + unpack"}
-        del x, y, ws
     # boundary-integral preconditioner shape (Table 3's largest case, qtt_workload.bie_case):
     # X = M Y, N = 2^21 = 4096 surfaces x 512 points, Y ranks <= 95, block-diagonal M ranks <= 50
     from qtt_workload import bie_case

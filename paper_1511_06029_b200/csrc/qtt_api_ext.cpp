@@ -233,7 +233,10 @@ qtt_status_t qtt_product_apply_ws(qtt_product_t p, const double* x, double* y, i
       // F_{n-1} first; each factor's stages read the previous factor's output
       for (int i = n - 1, step = 0; i >= 0; --i, ++step) {
         double* out = (i == 0) ? y + off : tmp[step & 1];
-        s = enqueue(p->factors[i], in, out, gr, fws, reinterpret_cast<cudaStream_t>(stream));
+        // each factor runs the plan a plain apply of it would (fused one-launch or per-stage)
+        s = use_fused(p->factors[i], gr)
+                ? enqueue_fused(p->factors[i], in, out, gr, fws, reinterpret_cast<cudaStream_t>(stream), true)
+                : enqueue(p->factors[i], in, out, gr, fws, reinterpret_cast<cudaStream_t>(stream));
         if (s != QTT_SUCCESS) return s;
         in = out;
       }

@@ -238,6 +238,7 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
   double c[NBC][4];
   int chunk = 0;
   int tile_nch = p.nchunks;
+
   for (int it = 0;; ++it) {
     const int s = it % kWideStages;
     const uint32_t ph = uint32_t(it / kWideStages) & 1u;
