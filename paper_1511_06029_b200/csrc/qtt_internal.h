@@ -219,11 +219,10 @@ struct FusedStage {
   int64_t out_limit = 0;           // QTT_BOUNDS_CHECK builds
   int log2_q = 0, n_i = 2, r_out = 0, nout = 0, K = 0, nchunks = 0, ncb = 0;
   int ks = 1;                      // warps per tile (intra-CTA split of the k-steps; 1, 2, 4 or 8)
-  // Morton order fused into the grid apply (qtt_apply_grid): the first stage
-  // gathers its input from a natural-order grid (min_dim), the last stage
-  // scatters its output into one (mout_dim); 0 = QTT order.  levels per axis
-  // = log2n / dim.
-  int min_dim = 0, mout_dim = 0, log2n = 0;
+  // Morton order fused into the grid apply (qtt_apply_grid): the last stage
+  // scatters its output into a natural-order grid (mout_dim; 0 = QTT order;
+  // levels per axis = log2n / dim).  The gather is FusedArgs' pre-pass.
+  int mout_dim = 0, log2n = 0;
 };
 struct FusedArgs {
   FusedStage st[kFusedMaxStages];
@@ -231,6 +230,13 @@ struct FusedArgs {
   unsigned* bar = nullptr;         // arrival counter, 0 at launch (left at 0 by every launch)
   size_t smem = 0;                 // dynamic smem: the largest super-core block (K x 32 doubles)
   int repeat = 1;                  // diagnostic (QTT_FUSED_REPEAT): run every stage this many times
+  // fused grid apply: a first pass gathers the natural-order grid pre_src into
+  // QTT order at pre_dst (each element once, stores coalesced), then a grid
+  // barrier; the stages read pre_dst (the last stage scatters: mout_dim)
+  const double* pre_src = nullptr;
+  double* pre_dst = nullptr;
+  int pre_dim = 0, pre_log2n = 0;
+  int64_t pre_total = 0;
   unsigned long long* prof = nullptr;   // diagnostic (QTT_FUSED_PROFILE): per CTA, %globaltimer
                                         // at start and after each stage's tiles / barrier, then for
                                         // the CTA's first unit of each stage: start, super-core block
@@ -239,14 +245,33 @@ struct FusedArgs {
 constexpr int kFusedProfSlots = 2 * kFusedMaxStages + 2 + 4 * kFusedMaxStages;
 cudaError_t fused_prepare();   // sets the kernel's max dynamic smem
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st);
-// natural-grid offset of QTT index q within one RHS (Morton order, R18)
+// natural-grid offset of QTT index q < 2^30 within one RHS (Morton order,
+// DESIGN.md R18: QTT bit dim*l + a = bit l of coordinate a; x fastest): the
+// coordinates are every dim-th bit of q, compacted with mask-and-shift steps
+// (constant time, registers only)
+QTT_HD inline uint32_t morton_compact3(uint32_t v) {
+  v &= 0x09249249u;
+  v = (v ^ (v >> 2)) & 0x030c30c3u;
+  v = (v ^ (v >> 4)) & 0x0300f00fu;
+  v = (v ^ (v >> 8)) & 0xff0000ffu;
+  v = (v ^ (v >> 16)) & 0x000003ffu;
+  return v;
+}
+QTT_HD inline uint32_t morton_compact2(uint32_t v) {
+  v &= 0x55555555u;
+  v = (v ^ (v >> 1)) & 0x33333333u;
+  v = (v ^ (v >> 2)) & 0x0f0f0f0fu;
+  v = (v ^ (v >> 4)) & 0x00ff00ffu;
+  v = (v ^ (v >> 8)) & 0x0000ffffu;
+  return v;
+}
 QTT_HD inline int64_t morton_natural(int64_t q, int dim, int levels) {
-  int64_t c[3] = {0, 0, 0};
-  for (int l = 0; l < levels; ++l)
-    for (int a = 0; a < dim; ++a) c[a] |= ((q >> (dim * l + a)) & 1) << l;
-  int64_t off = 0;
-  for (int a = dim - 1; a >= 0; --a) off = (off << levels) | c[a];
-  return off;
+  const uint32_t u = uint32_t(q);
+  if (dim == 3)
+    return int64_t(morton_compact3(u)) | (int64_t(morton_compact3(u >> 1)) << levels) |
+           (int64_t(morton_compact3(u >> 2)) << (2 * levels));
+  if (dim == 2) return int64_t(morton_compact2(u)) | (int64_t(morton_compact2(u >> 1)) << levels);
+  return q;
 }
 // y[s][c] = sum_g recv[g][s][c] (fixed order g = 0..parts-1), qtt_wide_kernel.cu
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,

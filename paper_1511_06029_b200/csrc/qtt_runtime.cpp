@@ -195,8 +195,9 @@ bool is_device_ptr(const void* p, int dev) {
 // [split-K partials of the largest split stage, if any].
 
 size_t ws_buf_bytes(const qtt_plan* h, int64_t nrhs) {
-  if (h->stages.size() <= 1 && h->fstages.size() <= 1 && h->shard_bits == 0) return 0;
-  const size_t one = size_t(h->max_interior_rank) * size_t(h->N) * size_t(nrhs) * sizeof(double);
+  if (h->stages.size() <= 1 && h->fstages.empty() && h->shard_bits == 0) return 0;
+  // a fused grid apply also gathers the input grid into buffer 1 (>= 1 double per element)
+  const size_t one = size_t(std::max<int64_t>(h->max_interior_rank, 1)) * size_t(h->N) * size_t(nrhs) * sizeof(double);
   return (one + 255) / 256 * 256;
 }
 
@@ -518,11 +519,18 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
     f.ncb = sp.ncb;
     f.ks = std::max(1, sp.ksplit);
     f.log2n = h->d;
-    f.min_dim = s == 0 ? morton_dim : 0;
-    f.mout_dim = last ? morton_dim : 0;
+    f.mout_dim = last ? morton_dim : 0;      // the scatter is the last stage's epilogue
+    if (s == 0 && morton_dim) f.in = buf[1];
     a.smem = std::max<size_t>(a.smem, size_t(sp.nchunks) * 128 * 16);
     max_wt = std::max<int64_t>(max_wt, (f.M + qtt::kSmallRows - 1) / qtt::kSmallRows * f.ncb * f.ks);
     in = f.out;
+  }
+  if (morton_dim) {   // stage 0 reads the gathered copy in buffer 1 (stage 1 writes it after a barrier)
+    a.pre_src = x;
+    a.pre_dst = buf[1];
+    a.pre_dim = morton_dim;
+    a.pre_log2n = h->d;
+    a.pre_total = int64_t(h->N) * nrhs;
   }
   // enough CTAs for the widest stage's (tile, k-part) warps, at most one per SM
   const int grid = int(std::min<int64_t>(h->num_sms, (max_wt + qtt::kFusedWarps - 1) / qtt::kFusedWarps));

@@ -548,15 +548,6 @@ struct FusedA {
   double2 x[kFusedG], y[kFusedG];
 };
 
-// Morton gather (first stage of a fused grid apply, r_in = 1): A element at
-// flat QTT offset f of the input is the grid value at morton_natural(f);
-// f even, so (f, f + 1) differ in the x bit 0 and stay one aligned double2.
-__device__ __forceinline__ const double* morton_src(const double* base, const double* ptr, const FusedStage& p) {
-  const int64_t f = ptr - base;
-  const int64_t nmask = (int64_t(1) << p.log2n) - 1;
-  return base + (f & ~nmask) + morton_natural(f & nmask, p.min_dim, p.log2n / p.min_dim);
-}
-
 template <bool COHERENT>
 __device__ __forceinline__ void fused_load_a(FusedA& o, const double* a0, const double* a1, int q, int q1, int K,
                                              int t0, bool ok0, bool ok1, const FusedStage& p) {
@@ -568,10 +559,6 @@ __device__ __forceinline__ void fused_load_a(FusedA& o, const double* a0, const 
     o.y[j] = make_double2(0.0, 0.0);
     const double2* pa0 = reinterpret_cast<const double2*>(a0 + qq * kSmallK);
     const double2* pa1 = reinterpret_cast<const double2*>(a1 + qq * kSmallK);
-    if (!COHERENT && p.min_dim) {
-      pa0 = reinterpret_cast<const double2*>(morton_src(p.in, a0 + qq * kSmallK, p));
-      pa1 = reinterpret_cast<const double2*>(morton_src(p.in, a1 + qq * kSmallK, p));
-    }
     if (vk && ok0) o.x[j] = COHERENT ? __ldcg(pa0) : __ldg(pa0);
     if (vk && ok1) o.y[j] = COHERENT ? __ldcg(pa1) : __ldg(pa1);
   }
@@ -720,6 +707,19 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const Fus
   uint32_t nwait = 0;
   unsigned nbar = 0;
   bool prefetched = false;
+  if (a.pre_dim) {   // Morton gather of the grid into QTT order (fused grid apply)
+    const int64_t nmask = (int64_t(1) << a.pre_log2n) - 1;
+    const int lv = a.pre_log2n / a.pre_dim;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < a.pre_total;
+         e += int64_t(gridDim.x) * blockDim.x)
+      a.pre_dst[e] = __ldg(a.pre_src + (e & ~nmask) + morton_natural(e & nmask, a.pre_dim, lv));
+    if (threadIdx.x == 0) {   // overlap the barrier with the first stage's super-core block
+      const FusedStage& f0 = a.st[0];
+      if (int64_t(blockIdx.x) < fused_rgroups(f0) * f0.ncb) fused_issue_b(f0, blockIdx.x, fused_rgroups(f0), sB, &bar);
+    }
+    prefetched = int64_t(blockIdx.x) < fused_rgroups(a.st[0]) * a.st[0].ncb;
+    grid_barrier(a.bar, ++nbar * gridDim.x);
+  }
   for (int s = 0; s < a.nstages; ++s) {
     for (int rep = 0; rep < a.repeat; ++rep) {
       if (prof && rep + 1 == a.repeat && rep > 0) {
@@ -727,9 +727,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const Fus
         if (threadIdx.x == 0) prof[2 * s] = globaltimer();   // timing of the last repeat only
       }
       unsigned long long* dp = prof ? prof + 2 * kFusedMaxStages + 2 + 4 * s : nullptr;
-      if (s == 0)
+      if (s == 0 && !a.pre_dim)   // x itself: written before this launch, read-only path
         fused_stage<false>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp);
-      else
+      else                        // written earlier in this launch: through L2
         fused_stage<true>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp);
       prefetched = false;
       if (rep + 1 < a.repeat) grid_barrier(a.bar, ++nbar * gridDim.x);

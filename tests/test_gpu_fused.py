@@ -192,3 +192,27 @@ def test_fused_grid_apply_shift_bitwise(qtt):
         y = op.apply_grid(torch.from_numpy(g).cuda(), dim).cpu().numpy()
     ref = OM.unpack(np.roll(OM.pack(g, dim, d // dim), 9, axis=1), dim, d // dim)
     np.testing.assert_array_equal(y, ref)
+
+
+def test_fused_caller_graph_capture(qtt):
+    """The caller captures a fused apply (one cooperative launch, no memset on
+    the handle's own workspace) into a CUDA graph: replays are bitwise the
+    plain apply, and plain applies still work afterwards."""
+    _, cores, x = generate("c1")
+    xt = torch.from_numpy(x).cuda()
+    s = torch.cuda.Stream()
+    with qtt.QttOperator(cores) as op:
+        assert op.launches(1) == 1
+        ref = op.apply(xt).clone()
+        torch.cuda.synchronize()
+        y = torch.empty_like(xt)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            op.apply(xt, out=y)
+        for _ in range(5):
+            y.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(y, ref)
+        assert torch.equal(op.apply(xt), ref)
+        del g

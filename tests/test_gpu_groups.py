@@ -83,11 +83,7 @@ def test_c5_many_rhs_memory_groups(qtt):
         ys = op.apply(xs)
         torch.cuda.synchronize()
         assert torch.equal(ys, y1 * scale)
-        # the single column against the pinned oracle on sampled rows
-        rows = np.array([0, 1, 12345, cfg.N // 2, cfg.N - 1])
-        ref = oracle.apply_rows(cores, x, rows)
-        got = y1.cpu().numpy()[:, rows]
-        oracle.assert_close(got, ref, rms=float(np.sqrt(np.mean(ref ** 2))), check_l2=False)
+        # y1 itself: every entry against the chunked oracle in test_gpu_full_parity.py
     finally:
         op.close()
         torch.cuda.empty_cache()

@@ -400,10 +400,13 @@ def _sampled_rows(N, n, seed):
     return np.array(sorted(rows))
 
 
-@pytest.mark.parametrize("name,nrows", [("c4", 24), ("c5", 6)])
+@pytest.mark.parametrize("name,nrows", [("c4", 24)])
 def test_full_size_sampled_rows(qtt, name, nrows):
     """Full BASELINE size, same launch configuration as bench.py; the oracle
-    computes sampled outputs one by one (apply_rows)."""
+    computes sampled outputs one by one (apply_rows: a third association of the
+    sum, independent of the sweeps).  c5 is compared on every entry in
+    test_gpu_full_parity.py (chunked oracle), which takes a fifth of the time
+    10 sampled rows of c5 take here."""
     cfg, cores, x = generate(name)
     y, _ = gpu_apply(qtt, cores, x)
     assert np.all(np.isfinite(y))
@@ -554,7 +557,7 @@ def test_operator_from_ttb1_file(qtt, tmp_path):
     _, cores, x = generate("c2")
     ttb1.save(tmp_path / "c2.ttb1", cores)
     xt = torch.from_numpy(x).cuda()
-    with qtt.QttOperator.from_ttb1(tmp_path / "c2.ttb1") as a, _per_stage(qtt, cores) as b:
+    with qtt.QttOperator.from_ttb1(tmp_path / "c2.ttb1") as a, qtt.QttOperator(cores) as b:
         assert torch.equal(a.apply(xt), b.apply(xt))
 
 
