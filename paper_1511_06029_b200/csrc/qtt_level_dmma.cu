@@ -191,14 +191,19 @@ __global__ void __launch_bounds__(256) diag_out_kernel(const LevelArgs p) {
 // per row: thread h sums a = h, h + 2, ... (fixed order), the pair adds its
 // halves with one shuffle (commutative: both hold the same sum), the even
 // thread stores the row's r_out outputs (one of the 2^L output streams per ii).
-// (Measured on the BIE factor M's levels 10-21, r_in 50, 2^21 rows: 0.213 ms
-// = 4.0 TB/s, against 0.34 ms for diag_kernel; 64-row items with 6 in flight
-// 0.35 ms; a warp per row with lanes over a, D from L2, 2.1 ms; a producer
-// warp with full/empty mbarriers instead of the CTA barrier per item 0.220 ms.)
+// The kernel is instantiated per r_out (1..8) so its inner loop carries no
+// predicates.  (Measured on the BIE factor M's levels 10-21, r_in 50, 2^21
+// rows: 0.145 ms = 5.9 TB/s, 91% of the measured HBM peak, against 0.34 ms
+// for diag_kernel; with r_out a runtime bound of a predicated 8-wide loop
+// 0.213 ms (41% issue-active: instruction-bound); 64-row items with 6 in
+// flight 0.35 ms; a warp per row with lanes over a, D from L2, 2.1 ms; a
+// producer warp with full/empty mbarriers instead of the CTA barrier per item
+// 0.220 ms.)
 constexpr int kDiagChunk = 128;
 constexpr int kDiagStages = 3;
 constexpr size_t kDiagStreamSmem = 220 * 1024;
 
+template <int RO>   // r_out, exact: the inner loops carry no predicates
 __global__ void __launch_bounds__(256) diag_stream_kernel(const LevelArgs p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kDiagStages];
@@ -245,29 +250,26 @@ __global__ void __launch_bounds__(256) diag_stream_kernel(const LevelArgs p) {
     }
     dmma::mbar_wait(&full[s], phase);
     const double* xr = reinterpret_cast<const double*>(sx + size_t(s) * xbytes) + size_t(r) * r_in;
-    const double* D = sD + size_t(r) * r_in * r_out;
-    double acc[kDiagMaxROut];
+    const double* D = sD + size_t(r) * r_in * RO;
+    double acc[RO];
 #pragma unroll
-    for (int b = 0; b < kDiagMaxROut; ++b) acc[b] = 0.0;
-#pragma unroll 4
+    for (int b = 0; b < RO; ++b) acc[b] = 0.0;
+#pragma unroll 8
     for (int a = h; a < r_in; a += 2) {
       const double xa = xr[a];
 #pragma unroll
-      for (int b = 0; b < kDiagMaxROut; ++b)
-        if (b < r_out) acc[b] = fma(xa, D[size_t(a) * r_out + b], acc[b]);
+      for (int b = 0; b < RO; ++b) acc[b] = fma(xa, D[a * RO + b], acc[b]);
     }
 #pragma unroll
-    for (int b = 0; b < kDiagMaxROut; ++b)
-      if (b < r_out) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], 1);
+    for (int b = 0; b < RO; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], 1);
     if (h == 0) {
       const int64_t ii = ib * kDiagChunk + r;
       const int64_t row = m + (((m >> p.log2_q) * (n_i - 1)) << p.log2_q) + (ii << p.log2_q);
 #pragma unroll
-      for (int b = 0; b < kDiagMaxROut; ++b)
-        if (b < r_out) {
-          QTT_CHECK_OUT(p, p.out + row * r_out + b, 1);
-          p.out[row * r_out + b] = acc[b];
-        }
+      for (int b = 0; b < RO; ++b) {
+        QTT_CHECK_OUT(p, p.out + row * RO + b, 1);
+        p.out[row * RO + b] = acc[b];
+      }
     }
     __syncthreads();                        // stage s consumed
     if (threadIdx.x == 0 && it + kDiagStages < i1) {
@@ -304,9 +306,19 @@ cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms) {
   static const bool no_stream = std::getenv("QTT_DIAG_NO_STREAM") != nullptr;   // diagnostic (A/B)
   const size_t xb = size_t(kDiagChunk) * a.r_in * sizeof(double);
   const size_t smem_s = xb * (a.r_out + kDiagStages);
-  if (!no_stream && a.n_i >= kDiagChunk && smem_s <= kDiagStreamSmem) {
-    static cudaError_t attr_ok = cudaFuncSetAttribute(diag_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                      int(kDiagStreamSmem));
+  if (!no_stream && a.n_i >= kDiagChunk && a.r_out <= kDiagMaxROut && smem_s <= kDiagStreamSmem) {
+    using DiagFn = void (*)(const LevelArgs);
+    static const DiagFn fns[kDiagMaxROut] = {diag_stream_kernel<1>, diag_stream_kernel<2>, diag_stream_kernel<3>,
+                                             diag_stream_kernel<4>, diag_stream_kernel<5>, diag_stream_kernel<6>,
+                                             diag_stream_kernel<7>, diag_stream_kernel<8>};
+    static const cudaError_t attr_ok = [] {
+      cudaError_t e = cudaSuccess;
+      for (DiagFn f : fns)
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kDiagStreamSmem));
+      return e;
+    }();
     if (attr_ok != cudaSuccess) return attr_ok;
     const int64_t items = int64_t(a.n_i / kDiagChunk) * a.M;
     int64_t blocks = items < num_sms ? items : num_sms;
@@ -321,7 +333,7 @@ cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms) {
     cs.stream = st;
     cs.attrs = attrs;
     cs.numAttrs = 1;
-    return cudaLaunchKernelEx(&cs, diag_stream_kernel, a);
+    return cudaLaunchKernelEx(&cs, fns[a.r_out - 1], a);
   }
   const bool lane_ii = a.M < 32;
   const int64_t warps = lane_ii ? a.M * ((a.n_i + 31) / 32) : (a.M + 31) / 32 * a.n_i;
