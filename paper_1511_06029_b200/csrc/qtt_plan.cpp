@@ -287,6 +287,7 @@ static bool diag_shape(const int64_t* ranks, int k0, int k1, int64_t n, StagePla
 }
 
 // Diagnostic (A/B of stage splits): QTT_PLAN_FORCE_STAGES="1-7,8-9,...,18-24"
+// ("k" alone = the one-level stage k-k)
 // forces the partition of levels 1..d into stages (each gets its cheapest
 // kernel instance); ignored unless it covers exactly 1..d with coverable stages.
 static bool forced_stages(int d, const int64_t* ranks, size_t smem_optin, int64_t n, std::vector<StagePlan>* out) {
@@ -298,10 +299,14 @@ static bool forced_stages(int d, const int64_t* ranks, size_t smem_optin, int64_
   while (*c) {
     char* e = nullptr;
     const long a = std::strtol(c, &e, 10);
-    if (e == c || *e != '-') return false;
-    c = e + 1;
-    const long b = std::strtol(c, &e, 10);
-    if (e == c || a != next || b < a || b > d || b - a + 1 > kMaxStageLevels) return false;
+    if (e == c) return false;
+    long b = a;                    // "k" alone is the one-level stage k-k
+    if (*e == '-') {
+      c = e + 1;
+      b = std::strtol(c, &e, 10);
+      if (e == c) return false;
+    }
+    if (a != next || b < a || b > d || b - a + 1 > kMaxStageLevels) return false;
     StagePlan sp;
     if (!stage_shape(ranks, int(a), int(b), n, smem_optin, &sp)) return false;
     p.push_back(sp);

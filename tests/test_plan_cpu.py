@@ -191,6 +191,8 @@ def test_forced_stage_split_switch():
     default = run(None)
     pairs = "1-7,8-9,10-11,12-13,14-15,16-17,18-24"
     assert run(pairs) == [(1, 7), (8, 9), (10, 11), (12, 13), (14, 15), (16, 17), (18, 24)]
+    singles = "1-7," + ",".join(str(k) for k in range(8, 18)) + ",18-24"   # "k" = the stage k-k
+    assert run(singles) == [(1, 7)] + [(k, k) for k in range(8, 18)] + [(18, 24)]
     assert run("1-7,8-9") == default            # does not reach d = 24
     assert run("2-24") == default               # does not start at level 1
     assert run("garbage") == default
