@@ -606,6 +606,19 @@ def run_reference(args):
     from qtt_workload import generate
     cfg, cores, x = generate(args.config)
     nrhs = cfg.nrhs
+    # torchrun sets OMP_NUM_THREADS=1 for every worker; rank 0 runs the oracle
+    # alone, on all of the host's cores
+    import contextlib
+    try:
+        from threadpoolctl import threadpool_limits
+        blas_ctx = threadpool_limits(limits=_affinity() or os.cpu_count() or 1)
+    except Exception:
+        blas_ctx = contextlib.nullcontext()
+    with blas_ctx:
+        return _run_reference_timed(args, world, cfg, cores, x, nrhs)
+
+
+def _run_reference_timed(args, world, cfg, cores, x, nrhs):
     for _ in range(args.warmup):
         oracle_warm_sample(cores, x, cfg)
     secs = []

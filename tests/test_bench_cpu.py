@@ -94,3 +94,24 @@ def test_multi_gpu_mode_defaults():
     assert bench.parallelism_desc("sharded", 2) == "top-bit shards x2 + NCCL reduce-scatter"
     assert bench.parallelism_desc("sharded", 1) == "single GPU"
     assert bench.parallelism_desc("replicas", 4).startswith("replicas x4")
+
+
+def test_reference_arm_under_torchrun_uses_all_cores():
+    """Under torchrun (OMP_NUM_THREADS=1 per worker) rank 0 alone runs the oracle
+    and prints the line, on all host cores; rank 1 exits without work."""
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--impl", "reference",
+                        "--gpus", "2", "--steps", "1", "--warmup", "3", "--config", "c2"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
