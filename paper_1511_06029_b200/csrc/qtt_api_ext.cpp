@@ -54,7 +54,11 @@ qtt_status_t qtt_apply_grid(qtt_handle_t h, const double* grid_in, double* grid_
     DeviceGuard g(h->device);
     // a fused apply gathers / scatters the Morton order in its first / last
     // stage: one launch, no staging vectors
-    if (use_fused(h, nrhs) && rhs_group(h, nrhs) >= nrhs) return grid_apply_fused(h, grid_in, grid_out, nrhs, dim, st);
+    if (use_fused(h, nrhs) && rhs_group(h, nrhs) >= nrhs) {
+      const qtt_status_t fs = grid_apply_fused(h, grid_in, grid_out, nrhs, dim, st);
+      // a refused cooperative launch disables the fused plan: take the staged path below
+      if (fs != QTT_ERROR_NOT_SUPPORTED || use_fused(h, nrhs)) return fs;
+    }
     const size_t elems = size_t(h->N) * size_t(nrhs);
     const bool capturing = stream_is_capturing(st);
     // the staging vectors are shared by the handle's grid applies: order this

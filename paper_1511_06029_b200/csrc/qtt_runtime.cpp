@@ -563,6 +563,16 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
   nvtxRangePushA("qtt fused apply");
   cudaError_t e = qtt::launch_fused(a, grid, st);
   nvtxRangePop();
+  if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorLaunchOutOfResources || e == cudaErrorNotSupported) {
+    // the device cannot co-schedule the grid here (e.g. under MPS limits): this
+    // handle runs its per-stage plan from now on
+    cudaGetLastError();
+    if (std::getenv("QTT_DEBUG"))
+      std::fprintf(stderr, "qtt: fused launch refused (%s); falling back to the per-stage plan\n",
+                   cudaGetErrorString(e));
+    h->fused_on = false;
+    return morton_dim ? QTT_ERROR_NOT_SUPPORTED : enqueue(h, x, y, nrhs, ws, st);
+  }
   if (e == cudaSuccess && a.prof) {
     std::vector<unsigned long long> hp(size_t(grid) * qtt::kFusedProfSlots);
     e = cudaStreamSynchronize(st);
