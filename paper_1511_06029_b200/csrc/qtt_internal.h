@@ -230,6 +230,7 @@ struct FusedArgs {
   unsigned* bar = nullptr;         // arrival counter, 0 at launch (left at 0 by every launch)
   size_t smem = 0;                 // dynamic smem: the largest super-core block (K x 32 doubles)
   int repeat = 1;                  // diagnostic (QTT_FUSED_REPEAT): run every stage this many times
+  int early_trigger = 1;           // griddepcontrol.launch_dependents at the last stage (QTT_FUSED_NO_TRIGGER=1: off)
   // fused grid apply: a first pass gathers the natural-order grid pre_src into
   // QTT order at pre_dst (each element once, stores coalesced), then a grid
   // barrier; the stages read pre_dst (the last stage scatters: mout_dim)

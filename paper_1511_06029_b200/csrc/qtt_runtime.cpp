@@ -560,6 +560,8 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
   if (fprof && !stream_is_capturing(st)) a.prof = d_prof;
   static const int frep = std::getenv("QTT_FUSED_REPEAT") ? std::atoi(std::getenv("QTT_FUSED_REPEAT")) : 1;
   a.repeat = std::max(1, frep);
+  static const bool no_trigger = std::getenv("QTT_FUSED_NO_TRIGGER") != nullptr;
+  a.early_trigger = no_trigger ? 0 : 1;
   nvtxRangePushA("qtt fused apply");
   cudaError_t e = qtt::launch_fused(a, grid, st);
   nvtxRangePop();

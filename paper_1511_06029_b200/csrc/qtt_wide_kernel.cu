@@ -700,27 +700,31 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const Fus
     dmma::fence_mbar_init();
   }
   __syncthreads();
+  // the first stage's super-core block is static (written at qtt_create, never
+  // by a kernel): its copy starts before griddepcontrol.wait, overlapping the
+  // previous kernel on the stream
+  const bool prefetch0 = int64_t(blockIdx.x) < fused_rgroups(a.st[0]) * a.st[0].ncb;
+  if (threadIdx.x == 0 && prefetch0) fused_issue_b(a.st[0], blockIdx.x, fused_rgroups(a.st[0]), sB, &bar);
   pdl_wait();
   unsigned long long* prof = a.prof ? a.prof + size_t(blockIdx.x) * kFusedProfSlots : nullptr;
   if (prof && threadIdx.x == 0) prof[0] = globaltimer();
   const int lane = threadIdx.x & 31;
   uint32_t nwait = 0;
   unsigned nbar = 0;
-  bool prefetched = false;
+  bool prefetched = prefetch0;
   if (a.pre_dim) {   // Morton gather of the grid into QTT order (fused grid apply)
     const int64_t nmask = (int64_t(1) << a.pre_log2n) - 1;
     const int lv = a.pre_log2n / a.pre_dim;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < a.pre_total;
          e += int64_t(gridDim.x) * blockDim.x)
       a.pre_dst[e] = __ldg(a.pre_src + (e & ~nmask) + morton_natural(e & nmask, a.pre_dim, lv));
-    if (threadIdx.x == 0) {   // overlap the barrier with the first stage's super-core block
-      const FusedStage& f0 = a.st[0];
-      if (int64_t(blockIdx.x) < fused_rgroups(f0) * f0.ncb) fused_issue_b(f0, blockIdx.x, fused_rgroups(f0), sB, &bar);
-    }
-    prefetched = int64_t(blockIdx.x) < fused_rgroups(a.st[0]) * a.st[0].ncb;
     grid_barrier(a.bar, ++nbar * gridDim.x);
   }
   for (int s = 0; s < a.nstages; ++s) {
+    // the last stage: let the next kernel on the stream launch onto the SMs
+    // this grid leaves free (it only stages its static super-core block before
+    // its own griddepcontrol.wait, which waits for this grid to complete)
+    if (s + 1 == a.nstages && a.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int rep = 0; rep < a.repeat; ++rep) {
       if (prof && rep + 1 == a.repeat && rep > 0) {
         __syncthreads();
