@@ -419,8 +419,47 @@ double fused_launch_seconds() {
   return v;
 }
 
+// Diagnostic (A/B): QTT_FUSED_FORCE_STAGES="1-7,8-10,11-15" forces the fused
+// plan's split (ignored unless it covers 1..d with stages a fused launch can run).
+static bool forced_fused(int d, const int64_t* ranks, int64_t rows, std::vector<StagePlan>* out, double* est) {
+  static const char* spec = std::getenv("QTT_FUSED_FORCE_STAGES");
+  if (!spec) return false;
+  std::vector<StagePlan> p;
+  double t = fused_launch_seconds();
+  int next = 1;
+  const char* c = spec;
+  while (*c) {
+    char* e = nullptr;
+    const long a = std::strtol(c, &e, 10);
+    if (e == c) return false;
+    long b = a;
+    if (*e == '-') {
+      c = e + 1;
+      b = std::strtol(c, &e, 10);
+      if (e == c) return false;
+    }
+    if (a != next || b < a || b > d || int(p.size()) >= kFusedMaxStages) return false;
+    StagePlan sp;
+    const double ts = fused_stage_seconds(ranks, int(a), int(b), double(rows), &sp);
+    if (ts < 0) return false;
+    t += ts;
+    p.push_back(sp);
+    next = int(b) + 1;
+    c = e;
+    if (*c == ',') ++c;
+  }
+  if (next != d + 1) return false;
+  *out = p;
+  if (est) *est = t;
+  return true;
+}
+
 std::vector<StagePlan> plan_stages_fused(int d, const int64_t* ranks, int max_stage_levels, int64_t rows,
                                          double* est) {
+  {
+    std::vector<StagePlan> forced;
+    if (forced_fused(d, ranks, rows, &forced, est)) return forced;
+  }
   const double kLaunchF = fused_launch_seconds();
   const int maxL = std::max(1, std::min(max_stage_levels, kMaxStageLevels));
   std::vector<double> best(d + 1, std::numeric_limits<double>::infinity());
