@@ -74,6 +74,14 @@ int main(int argc, char** argv) {
     return 1;
   }
   cudaMemcpy(dx, x, N * sizeof(double), cudaMemcpyHostToDevice);
+  {   /* what one apply launches: at this size one fused persistent launch */
+    int launches = 0, n = 0, kf[D], kl[D], var[D];
+    if (qtt_get_apply_plan(h, 1, &launches, &n, kf, kl, var) == QTT_SUCCESS) {
+      printf("apply plan: %d launch(es), %d stage(s):", launches, n);
+      for (int i = 0; i < n; ++i) printf(" [%d-%d v%d]", kf[i], kl[i], var[i]);
+      printf("\n");
+    }
+  }
   s = qtt_apply(h, dx, dy, 1, NULL);
   if (s == QTT_SUCCESS && cudaDeviceSynchronize() != cudaSuccess) s = QTT_ERROR_CUDA;
   cudaMemcpy(y, dy, N * sizeof(double), cudaMemcpyDeviceToHost);

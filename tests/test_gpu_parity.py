@@ -997,3 +997,4 @@ def test_plain_c_program_applies_the_shift(qtt, tmp_path):
     exe, env = mod._build_c_example(tmp_path, qtt)
     r = subprocess.run([exe], capture_output=True, text=True, env=env, timeout=120)
     assert r.returncode == 0 and " 0 of " in r.stdout, r.stdout + r.stderr
+    assert "apply plan: 1 launch(es)" in r.stdout, r.stdout       # d = 12: the fused one-launch apply
