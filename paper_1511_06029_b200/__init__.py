@@ -222,6 +222,8 @@ def morton_pack(grid, dim: int, levels: int, out=None, stream=None):
     N = 1 << (dim * levels)
     y = torch.empty((nrhs, N), dtype=torch.float64, device=grid.device) if out is None else out
     _grid_args(y, dim, levels)
+    if y.numel() != grid.numel():
+        raise ValueError("out must have as many elements as grid")
     _lib.check("qtt_morton_pack", _lib.load().qtt_morton_pack(
         _ptr(grid), _ptr(y), int(dim), int(levels), int(nrhs), _stream_handle(stream)))
     return y
@@ -233,6 +235,8 @@ def morton_unpack(x, dim: int, levels: int, out=None, stream=None):
     nrhs = _grid_args(x, dim, levels)
     y = torch.empty_like(x) if out is None else out
     _grid_args(y, dim, levels)
+    if y.numel() != x.numel():
+        raise ValueError("out must have as many elements as x")
     _lib.check("qtt_morton_unpack", _lib.load().qtt_morton_unpack(
         _ptr(x), _ptr(y), int(dim), int(levels), int(nrhs), _stream_handle(stream)))
     return y

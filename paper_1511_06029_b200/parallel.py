@@ -254,6 +254,11 @@ class ShardedQttOperator:
 
     def apply(self, x_local, out=None, stream=None, workspace=None, send=None):
         import torch
+        if out is not None:
+            nr = 1 if x_local.dim() == 1 else x_local.shape[0]
+            if (not isinstance(out, torch.Tensor) or out.dtype != torch.float64 or not out.is_cuda
+                    or not out.is_contiguous() or out.numel() != nr * self.n):
+                raise ValueError(f"out must be a contiguous float64 CUDA tensor of {nr} x {self.n} entries")
         if self._op is not None:
             return self._op.apply(x_local, out=out, stream=stream, workspace=workspace)
         if self.fused:

@@ -92,3 +92,14 @@ def test_pack_unaligned_pointers(qtt):
     assert lib.qtt_morton_pack(g.data_ptr(), out.data_ptr(), dim, levels, 1, None) == 0
     torch.cuda.synchronize()
     np.testing.assert_array_equal(out.cpu().numpy(), OM.pack(g.cpu().numpy()[None, :], dim, levels)[0])
+
+
+def test_morton_out_validation(qtt):
+    """A caller's `out` of the wrong size is refused before the kernel runs."""
+    g = torch.zeros((2, 1 << 12), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        qtt.morton_pack(g, 3, 4, out=torch.empty((1, 1 << 12), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        qtt.morton_unpack(g, 3, 4, out=torch.empty((3, 1 << 12), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        qtt.morton_pack(g, 3, 4, out=torch.empty((2, 1 << 12), dtype=torch.float32, device="cuda"))
