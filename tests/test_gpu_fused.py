@@ -216,3 +216,14 @@ def test_fused_caller_graph_capture(qtt):
             assert torch.equal(y, ref)
         assert torch.equal(op.apply(xt), ref)
         del g
+
+
+def test_stage_cap_disables_fused(qtt):
+    """A caller-capped stage length (qtt_create_ex, e.g. 1 = Alg. 2 level by
+    level) asks for that launch structure: no fused plan is built."""
+    cfg, cores, x = generate("c1")
+    with qtt.QttOperator(cores, max_stage_levels=1) as op:
+        assert op.launches(1) == cfg.d
+        assert all(s["variant"] != "fused" for s in op.stages(1))
+        y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    oracle.assert_close(y, oracle.apply_dense(cores, x))
