@@ -29,3 +29,18 @@ def load_golden(name):
 @pytest.fixture
 def golden():
     return load_golden
+
+
+# Full-size parity metrics (tests/test_gpu_full_parity.py) are reported at the
+# end of the run, so they appear in a quiet (-q) run's summary as well.
+PARITY_RECORDS = []
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    if not PARITY_RECORDS:
+        return
+    terminalreporter.write_sep("-", "full-vector parity at BASELINE sizes (every entry vs the CPU oracle)")
+    for name, worst, oracle_s in PARITY_RECORDS:
+        terminalreporter.write_line(
+            f"{name:10s} rel_l2 {worst['rel_l2']:.2e}  elem(RMS floor) {worst['elem_floor']:.2e}  "
+            f"raw offenders {worst['raw_offenders']} (near-zero entries)  oracle {oracle_s:.1f} s")
