@@ -82,7 +82,7 @@ def _check(name, y, ref, oracle_s, stages):
     oracle.assert_close(y, ref)
 
 
-@pytest.mark.parametrize("name", ["c3", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
 def test_full_vector_blas_oracle(qtt, name):
     cfg, cores, x = generate(name)
     y, stages = _gpu_apply(qtt, cores, x)
