@@ -311,15 +311,18 @@ cudaError_t launch_diag(const LevelArgs& a, cudaStream_t st, int num_sms) {
     static const DiagFn fns[kDiagMaxROut] = {diag_stream_kernel<1>, diag_stream_kernel<2>, diag_stream_kernel<3>,
                                              diag_stream_kernel<4>, diag_stream_kernel<5>, diag_stream_kernel<6>,
                                              diag_stream_kernel<7>, diag_stream_kernel<8>};
-    static const cudaError_t attr_ok = [] {
-      cudaError_t e = cudaSuccess;
-      for (DiagFn f : fns)
-        if (e == cudaSuccess)
-          e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kDiagStreamSmem));
-      return e;
-    }();
-    if (attr_ok != cudaSuccess) return attr_ok;
+    // the smem attribute is per device: set once for each device this process uses
+    static bool attr_set[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+      for (DiagFn f : fns) {
+        const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDiagStreamSmem));
+        if (e != cudaSuccess) return e;
+      }
+      if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    }
     const int64_t items = int64_t(a.n_i / kDiagChunk) * a.M;
     int64_t blocks = items < num_sms ? items : num_sms;
     if (blocks < 1) blocks = 1;
