@@ -245,7 +245,7 @@ struct FusedArgs {
 };
 constexpr int kFusedProfSlots = 2 * kFusedMaxStages + 2 + 4 * kFusedMaxStages;
 cudaError_t fused_prepare();   // sets the kernel's max dynamic smem
-cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st, bool pdl = true);
 // natural-grid offset of QTT index q < 2^30 within one RHS (Morton order,
 // DESIGN.md R18: QTT bit dim*l + a = bit l of coordinate a; x fastest): the
 // coordinates are every dim-th bit of q, compacted with mask-and-shift steps

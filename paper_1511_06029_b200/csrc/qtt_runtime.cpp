@@ -534,7 +534,11 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
   }
   // enough CTAs for the widest stage's (tile, k-part) warps, at most one per SM
   const int grid = int(std::min<int64_t>(h->num_sms, (max_wt + qtt::kFusedWarps - 1) / qtt::kFusedWarps));
-  if (zero_bar) {   // a stream memory op (no kernel) clears the arrival counter
+  const bool capturing = stream_is_capturing(st);
+  if (zero_bar && capturing) {   // inside a graph: a memset node
+    const cudaError_t e = cudaMemsetAsync(a.bar, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return from_cuda(e);
+  } else if (zero_bar) {   // a stream memory op (no kernel) clears the arrival counter
     using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
     static const WriteValueFn wv = [] {
       void* f = nullptr;
@@ -557,13 +561,14 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
   if (fprof && !d_prof &&
       cudaMalloc(&d_prof, size_t(h->num_sms) * qtt::kFusedProfSlots * sizeof(unsigned long long)) != cudaSuccess)
     d_prof = nullptr;
-  if (fprof && !stream_is_capturing(st)) a.prof = d_prof;
+  if (fprof && !capturing) a.prof = d_prof;
   static const int frep = std::getenv("QTT_FUSED_REPEAT") ? std::atoi(std::getenv("QTT_FUSED_REPEAT")) : 1;
   a.repeat = std::max(1, frep);
   static const bool no_trigger = std::getenv("QTT_FUSED_NO_TRIGGER") != nullptr;
   a.early_trigger = no_trigger ? 0 : 1;
   nvtxRangePushA("qtt fused apply");
-  cudaError_t e = qtt::launch_fused(a, grid, st);
+  static const bool graph_nopdl = std::getenv("QTT_FUSED_GRAPH_NOPDL") != nullptr;   // A/B
+  cudaError_t e = qtt::launch_fused(a, grid, st, !(graph_nopdl && st == h->capture_stream));
   nvtxRangePop();
   if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorLaunchOutOfResources || e == cudaErrorNotSupported) {
     // the device cannot co-schedule the grid here (e.g. under MPS limits): this
@@ -609,23 +614,33 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
                    cudaGetErrorString(e));
     return from_cuda(e);
   }
-  if (!stream_is_capturing(st)) cudaEventRecord(h->last, st);
+  if (!capturing) cudaEventRecord(h->last, st);
   return QTT_SUCCESS;
 }
 
-// enqueue() through a cached CUDA graph: captured once per (x, y, ws, nrhs) on
-// an internal stream, then replayed on `st` with one launch.  Falls back to a
-// plain enqueue while stage timing is on, when `st` is itself being captured,
-// or with QTT_NO_GRAPH set.
-qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st) {
+// enqueue() (kind 0) or enqueue_fused() (kind 1, 2 = with the barrier reset)
+// through a cached CUDA graph: captured once per (x, y, ws, nrhs, kind) on an
+// internal stream, then replayed on `st` with one launch.  A graph launch costs
+// the host and the GPU front end less than the cooperative launch it holds
+// (DESIGN.md 6.11).  Falls back to a plain enqueue while stage timing is on,
+// when `st` is itself being captured, or with QTT_NO_GRAPH set.
+qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
+                             int kind) {
   static const bool no_graph = std::getenv("QTT_NO_GRAPH") != nullptr;
+  static const bool fused_direct = std::getenv("QTT_FUSED_NO_GRAPH") != nullptr ||
+                                   std::getenv("QTT_FUSED_PROFILE") != nullptr;
+  static bool capture_broken[3] = {false, false, false};   // the driver refused to capture this kind once
+  auto plain = [&](cudaStream_t s2) {
+    return kind ? enqueue_fused(h, x, y, nrhs, ws, s2, kind == 2) : enqueue(h, x, y, nrhs, ws, s2);
+  };
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (no_graph || h->timing || cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+  if (no_graph || h->timing || (kind && (fused_direct || capture_broken[kind])) ||
+      cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
-    return enqueue(h, x, y, nrhs, ws, st);
+    return plain(st);
   }
   for (auto& g : h->graphs)
-    if (g.x == x && g.y == y && g.ws == ws && g.nrhs == nrhs) {
+    if (g.x == x && g.y == y && g.ws == ws && g.nrhs == nrhs && g.kind == kind) {
       nvtxRangePushA("qtt apply (graph replay)");
       cudaError_t e = cudaGraphLaunch(g.exec, st);
       nvtxRangePop();
@@ -636,24 +651,36 @@ qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nr
     return QTT_ERROR_CUDA;
   cudaError_t e = cudaStreamBeginCapture(h->capture_stream, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return from_cuda(e);
-  const qtt_status_t s = enqueue(h, x, y, nrhs, ws, h->capture_stream);
+  const bool fused_before = h->fused_on;
+  const qtt_status_t s = plain(h->capture_stream);
   cudaGraph_t graph = nullptr;
   e = cudaStreamEndCapture(h->capture_stream, &graph);
-  if (s != QTT_SUCCESS) {
-    if (graph) cudaGraphDestroy(graph);
-    return s;
-  }
-  if (e != cudaSuccess) return from_cuda(e);
   cudaGraphExec_t exec = nullptr;
-  e = cudaGraphInstantiate(&exec, graph, 0);
-  cudaGraphDestroy(graph);
-  if (e != cudaSuccess) return from_cuda(e);
+  if (s == QTT_SUCCESS && e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (kind && (s != QTT_SUCCESS || e != cudaSuccess || h->fused_on != fused_before)) {
+    // the cooperative launch could not be captured (or fell back to the per-stage
+    // plan inside the capture): launch it directly from now on
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaGetLastError();
+    capture_broken[kind] = true;
+    h->fused_on = fused_before;
+    if (std::getenv("QTT_DEBUG")) std::fprintf(stderr, "qtt: fused launch not capturable; launching directly\n");
+    return plain(st);
+  }
+  if (s != QTT_SUCCESS) return s;
+  if (e != cudaSuccess) {
+    if (std::getenv("QTT_DEBUG")) std::fprintf(stderr, "qtt: graph capture failed: %s\n", cudaGetErrorString(e));
+    return from_cuda(e);
+  }
   if (h->graphs.size() >= 8) {
     cudaGraphExecDestroy(h->graphs.front().exec);
     h->graphs.erase(h->graphs.begin());
   }
-  h->graphs.push_back({x, y, ws, nrhs, exec});
+  h->graphs.push_back({x, y, ws, nrhs, exec, kind});
   e = cudaGraphLaunch(exec, st);
+  if (e != cudaSuccess && std::getenv("QTT_DEBUG"))
+    std::fprintf(stderr, "qtt: graph launch (kind %d) failed: %s\n", kind, cudaGetErrorString(e));
   if (e == cudaSuccess) e = cudaEventRecord(h->last, st);
   return from_cuda(e);
 }

@@ -89,6 +89,7 @@ struct qtt_plan {
     void* ws;
     int64_t nrhs;
     cudaGraphExec_t exec;
+    int kind;          // 0 per-stage plan, 1 fused launch, 2 fused launch + barrier reset
   };
   std::vector<Graph> graphs;
   cudaStream_t capture_stream = nullptr;
@@ -242,7 +243,8 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
                          const SplitScratch* split = nullptr);
 qtt_status_t enqueue(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
                      bool fused = false);
-qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st);
+qtt_status_t enqueue_graphed(qtt_plan* h, const double* x, double* y, int64_t nrhs, void* ws, cudaStream_t st,
+                             int kind = 0);
 // the fused apply (one persistent launch); zero_bar: clear the workspace's
 // grid-barrier words first (a workspace not known to hold them at 0)
 bool use_fused(const qtt_plan* h, int64_t nrhs);

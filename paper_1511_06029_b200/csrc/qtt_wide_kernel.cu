@@ -900,7 +900,7 @@ cudaError_t fused_prepare() {
                               int(kFusedMaxBBytes));
 }
 
-cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st, bool pdl) {
   if (grid < 1 || a.nstages < 1 || a.nstages > kFusedMaxStages || a.smem > kFusedMaxBBytes)
     return cudaErrorInvalidValue;
   static const bool no_coop = std::getenv("QTT_FUSED_NOCOOP") != nullptr;   // diagnostic (A/B of launch cost)
@@ -908,7 +908,7 @@ cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributeCooperative;     // co-residency for the grid barrier
   attr[0].val.cooperative = no_coop ? 0 : 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl && pdl_enabled() ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(kFusedWarps * 32);

@@ -4,7 +4,7 @@
 set -u
 TAG=${1:-q}
 KEXPR=${2:-}
-shift 2 2>/dev/null
+set -- "${@:3}"
 O=gpurun_out
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/${TAG}_smoke.log 2>&1
