@@ -223,6 +223,7 @@ struct FusedStage {
   // scatters its output into a natural-order grid (mout_dim; 0 = QTT order;
   // levels per axis = log2n / dim).  The gather is FusedArgs' pre-pass.
   int mout_dim = 0, log2n = 0;
+  int runs = 0;                    // run-wise smem epilogue (r_out | 32, Q % 16 == 0, QTT-order output)
 };
 struct FusedArgs {
   FusedStage st[kFusedMaxStages];
@@ -243,7 +244,10 @@ struct FusedArgs {
                                         // the CTA's first unit of each stage: start, super-core block
                                         // in smem, MMAs done, tile stored
 };
-constexpr int kFusedProfSlots = 2 * kFusedMaxStages + 2 + 4 * kFusedMaxStages;
+constexpr int kFusedProfBase = 2 * kFusedMaxStages + 2 + 4 * kFusedMaxStages;
+// then per stage and warp of the CTA's first unit: A fragment arrived, MMAs done,
+// past the split-K __syncthreads, tile stored (ns, %globaltimer)
+constexpr int kFusedProfSlots = kFusedProfBase + kFusedMaxStages * kFusedWarps * 4;
 cudaError_t fused_prepare();   // sets the kernel's max dynamic smem
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st, bool pdl = true);
 // natural-grid offset of QTT index q < 2^30 within one RHS (Morton order,

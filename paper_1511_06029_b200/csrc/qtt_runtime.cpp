@@ -520,6 +520,8 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
     f.ks = std::max(1, sp.ksplit);
     f.log2n = h->d;
     f.mout_dim = last ? morton_dim : 0;      // the scatter is the last stage's epilogue
+    static const bool no_runs = std::getenv("QTT_FUSED_NO_RUNS") != nullptr;   // A/B
+    f.runs = !no_runs && f.mout_dim == 0 && sp.r_out <= 32 && (32 % sp.r_out) == 0 && f.log2_q >= 4 ? 1 : 0;
     if (s == 0 && morton_dim) f.in = buf[1];
     a.smem = std::max<size_t>(a.smem, size_t(sp.nchunks) * 128 * 16);
     max_wt = std::max<int64_t>(max_wt, (f.M + qtt::kSmallRows - 1) / qtt::kSmallRows * f.ncb * f.ks);
@@ -561,7 +563,10 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
   if (fprof && !d_prof &&
       cudaMalloc(&d_prof, size_t(h->num_sms) * qtt::kFusedProfSlots * sizeof(unsigned long long)) != cudaSuccess)
     d_prof = nullptr;
-  if (fprof && !capturing) a.prof = d_prof;
+  if (fprof && !capturing && d_prof) {
+    a.prof = d_prof;
+    cudaMemsetAsync(d_prof, 0, size_t(h->num_sms) * qtt::kFusedProfSlots * sizeof(unsigned long long), st);
+  }
   static const int frep = std::getenv("QTT_FUSED_REPEAT") ? std::atoi(std::getenv("QTT_FUSED_REPEAT")) : 1;
   a.repeat = std::max(1, frep);
   static const bool no_trigger = std::getenv("QTT_FUSED_NO_TRIGGER") != nullptr;
@@ -606,6 +611,21 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
                      (long long)(d[2] - d[0]), (long long)(d[3] - d[0]));
       }
       std::fprintf(stderr, "\n");
+      // per-warp stamps of the first unit of each stage, CTA 0 and the last CTA
+      for (int b : {0, grid - 1})
+        for (int s2 = 0; s2 < a.nstages; ++s2) {
+          const unsigned long long* d = &hp[size_t(b) * qtt::kFusedProfSlots + 2 * qtt::kFusedMaxStages + 2 + 4 * s2];
+          const unsigned long long* w = &hp[size_t(b) * qtt::kFusedProfSlots + qtt::kFusedProfBase +
+                                            size_t(s2) * qtt::kFusedWarps * 4];
+          std::fprintf(stderr, "  CTA %d s%d (ks %d) warp: A-in / mma / sync / stored (ns from unit start):", b, s2,
+                       a.st[s2].ks);
+          for (int w2 = 0; w2 < qtt::kFusedWarps; ++w2) {
+            auto rel = [&](unsigned long long v) { return v ? (long long)(v - d[0]) : -1ll; };
+            std::fprintf(stderr, " [%lld %lld %lld %lld]", rel(w[4 * w2]), rel(w[4 * w2 + 1]), rel(w[4 * w2 + 2]),
+                         rel(w[4 * w2 + 3]));
+          }
+          std::fprintf(stderr, "\n");
+        }
     }
   }
   if (e != cudaSuccess) {

@@ -177,6 +177,46 @@ __device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const P& p
   }
 }
 
+// Fused-stage epilogue through shared memory (r_out divides 32, Q a multiple
+// of 16): the 16 x 32 warp tile covers 32 / r_out whole ii blocks, and each
+// block's output is ONE contiguous run of 16 r_out doubles (rows m0..m0+15 of
+// one RHS, b fastest).  The warp writes its tile into its private smem slot
+// `ws` (512 doubles) in run order, then stores the runs with 16-byte stores,
+// 512 contiguous bytes per warp instruction -- instead of 8-byte scattered
+// stores (r_out = 1: 16 instructions of 4 x 64-byte pieces each).
+__device__ __forceinline__ void tile_store_runs(const double (&c)[4][4], const FusedStage& p, int64_t m0, int n_first,
+                                                int lane, double* ws) {
+  const int g = lane >> 2, t0 = lane & 3;
+  const int r = p.r_out;
+  const int lr = __ffs(r) - 1;                      // r = 2^lr
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = nb * 8 + 2 * t0 + e, row = g + 8 * h;
+        const int b = col & (r - 1);
+        ws[((col - b) << 4) + (row << lr) + b] = c[nb][2 * h + e];
+      }
+  __syncwarp();
+  const int64_t rowbase = m0 + (((m0 >> p.log2_q) * (p.n_i - 1)) << p.log2_q);
+  const int ii0 = n_first >> lr;
+  const int lrun = lr + 4;                          // log2 of a run's length (16 r doubles)
+  const double2* ws2 = reinterpret_cast<const double2*>(ws);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int e2 = (k * 32 + lane) * 2;             // first double of this lane's piece
+    const int ii = ii0 + (e2 >> lrun);
+    if (ii < p.n_i) {
+      double* dst = p.out + ((rowbase + (int64_t(ii) << p.log2_q)) << lr) + (e2 & ((1 << lrun) - 1));
+      QTT_CHECK_OUT(p, dst, 2);
+      *reinterpret_cast<double2*>(dst) = ws2[k * 32 + lane];
+    }
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -533,6 +573,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// the timer read after v is available (v is an input of the asm: the read
+// waits on v's scoreboard, e.g. the last DMMA into an accumulator)
+__device__ __forceinline__ unsigned long long globaltimer_after(double v) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "d"(v));
+  return t;
+}
 
 // Partial product of one 16 x 32 warp tile over k-steps [q0, q1) (k-steps of
 // 8).  B comes from shared memory: the CTA's block of the stage's super-core
@@ -612,10 +659,11 @@ __device__ __forceinline__ void fused_issue_b(const FusedStage& p, int64_t u, in
   dmma::bulk_g2s(sB, p.bpack + size_t(cb) * p.nchunks * 256, bbytes, bar);
 }
 
-template <bool COHERENT>
+template <bool COHERENT, bool PROF>
 __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, double2* sB, uint64_t* bar,
                                             uint32_t& nwait, bool prefetched, int lane,
-                                            unsigned long long* dprof = nullptr) {
+                                            unsigned long long* dprof = nullptr,
+                                            unsigned long long* wprof = nullptr) {
   const int w = threadIdx.x >> 5;
   const int ks = p.ks;
   const int slots = kFusedWarps / ks;
@@ -633,7 +681,7 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
     const int64_t m0 = mt * kSmallRows;
     const bool first = u == blockIdx.x;
     if (!first) __syncthreads();           // the previous unit is done with sB and red
-    const bool rec = dprof && threadIdx.x == 0 && first;
+    const bool rec = PROF && dprof && threadIdx.x == 0 && first;
     if (rec) dprof[0] = globaltimer();
     if (threadIdx.x == 0 && !(first && prefetched)) fused_issue_b(p, u, rgroups, sB, bar);
     // A fragments of the first k-steps while the super-core block lands
@@ -648,6 +696,8 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
     dmma::mbar_wait(bar, nwait & 1u);
     ++nwait;
     if (rec) dprof[1] = globaltimer();
+    unsigned long long* wp = (PROF && wprof && first) ? wprof + w * 4 : nullptr;   // per-warp stamps (lane 0)
+    if (wp && lane == 0) wp[0] = globaltimer_after(fa.x[0].x);
     if (live) {
       for (int q = q0; q < q1; q += 2 * kFusedG) {
         if (q + kFusedG < q1) fused_load_a<COHERENT>(fb, a0, a1, q + kFusedG, q1, p.K, t0, ok0, ok1, p);
@@ -657,10 +707,18 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
         fused_mma(fb, sB, q + kFusedG, q1, lane, c);
       }
     }
-    if (rec) dprof[2] = globaltimer() + (c[0][0] == 12345.0 ? 1 : 0);
+    if (rec) dprof[2] = globaltimer_after(c[0][0]);
+    if (wp && lane == 0) wp[1] = globaltimer_after(c[3][3] + c[0][0]);
+    // run-wise epilogue: every row of the tile in one RHS (Q % 16 == 0), r_out | 32
+    const bool runs = p.runs;
+    double* wslot = red + size_t(w) * 16 * 32;     // this warp's own partial slot (unused by it otherwise)
     if (ks == 1) {
-      if (live) tile_store<4>(c, p, m0, cb * kSmallCols, lane);
+      if (live) {
+        if (runs) tile_store_runs(c, p, m0, cb * kSmallCols, lane, wslot);
+        else tile_store<4>(c, p, m0, cb * kSmallCols, lane);
+      }
       if (rec) dprof[3] = globaltimer();
+      if (wp && lane == 0) wp[3] = globaltimer();
       continue;
     }
     // partials [warp][value][lane]: every access is 32 consecutive doubles (no bank conflicts)
@@ -672,6 +730,7 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
         for (int v = 0; v < 4; ++v) mine[(nb * 4 + v) * 32] = c[nb][v];
     }
     __syncthreads();
+    if (wp && lane == 0) wp[2] = globaltimer();
     if (kp == 0 && live) {
       for (int j = 1; j < ks; ++j) {
         const double* o = red + size_t(w + j) * 16 * 32 + lane;
@@ -680,8 +739,11 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
 #pragma unroll
           for (int v = 0; v < 4; ++v) c[nb][v] += o[(nb * 4 + v) * 32];
       }
-      tile_store<4>(c, p, m0, cb * kSmallCols, lane);
+      if (wp && lane == 0) wp[2] = globaltimer_after(c[3][3] + c[0][0]);   // reduced
+      if (runs) tile_store_runs(c, p, m0, cb * kSmallCols, lane, wslot);
+      else tile_store<4>(c, p, m0, cb * kSmallCols, lane);
       if (rec) dprof[3] = globaltimer();
+      if (wp && lane == 0) wp[3] = globaltimer();
     }
   }
 }
@@ -690,6 +752,9 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
 // plan's stages one after another, each spread over every warp of the grid
 // (fused_stage), separated by grid barriers instead of kernel boundaries; the
 // intermediates (two ping-pong buffers) stay in L2.
+// PROF: the diagnostic instance (QTT_FUSED_PROFILE) with %globaltimer stamps;
+// the production instance carries no profiling code.
+template <bool PROF>
 __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const FusedArgs a) {
   __shared__ __align__(16) double red[kFusedWarps * 32 * 16];   // split-K partials, 32 KiB
   __shared__ __align__(8) uint64_t bar;
@@ -706,7 +771,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const Fus
   const bool prefetch0 = int64_t(blockIdx.x) < fused_rgroups(a.st[0]) * a.st[0].ncb;
   if (threadIdx.x == 0 && prefetch0) fused_issue_b(a.st[0], blockIdx.x, fused_rgroups(a.st[0]), sB, &bar);
   pdl_wait();
-  unsigned long long* prof = a.prof ? a.prof + size_t(blockIdx.x) * kFusedProfSlots : nullptr;
+  unsigned long long* prof = (PROF && a.prof) ? a.prof + size_t(blockIdx.x) * kFusedProfSlots : nullptr;
   if (prof && threadIdx.x == 0) prof[0] = globaltimer();
   const int lane = threadIdx.x & 31;
   uint32_t nwait = 0;
@@ -731,10 +796,11 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const Fus
         if (threadIdx.x == 0) prof[2 * s] = globaltimer();   // timing of the last repeat only
       }
       unsigned long long* dp = prof ? prof + 2 * kFusedMaxStages + 2 + 4 * s : nullptr;
+      unsigned long long* wpp = prof ? prof + kFusedProfBase + s * kFusedWarps * 4 : nullptr;
       if (s == 0 && !a.pre_dim)   // x itself: written before this launch, read-only path
-        fused_stage<false>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp);
+        fused_stage<false, PROF>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp, wpp);
       else                        // written earlier in this launch: through L2
-        fused_stage<true>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp);
+        fused_stage<true, PROF>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp, wpp);
       prefetched = false;
       if (rep + 1 < a.repeat) grid_barrier(a.bar, ++nbar * gridDim.x);
     }
@@ -896,7 +962,10 @@ cudaError_t launch_small(const LevelArgs& a, cudaStream_t st) {
 }
 
 cudaError_t fused_prepare() {
-  return cudaFuncSetAttribute(wide::fused_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const cudaError_t e = cudaFuncSetAttribute(wide::fused_small_kernel<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedMaxBBytes));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(wide::fused_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(kFusedMaxBBytes));
 }
 
@@ -916,7 +985,8 @@ cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st, bool pdl
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, wide::fused_small_kernel, a);
+  return a.prof ? cudaLaunchKernelEx(&cfg, wide::fused_small_kernel<true>, a)
+                : cudaLaunchKernelEx(&cfg, wide::fused_small_kernel<false>, a);
 }
 
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,
