@@ -412,7 +412,12 @@ qtt_status_t qtt_workspace_size(qtt_handle_t h, int64_t nrhs, size_t* bytes) {
 // pair would only churn the cache at these sizes).
 static qtt_status_t enqueue_groups(qtt_plan* h, const double* x, double* y, int64_t nrhs, int64_t group, void* ws,
                                    cudaStream_t st, bool bar_zero = false) {
-  if (group >= nrhs && use_fused(h, nrhs)) return enqueue_graphed(h, x, y, nrhs, ws, st, bar_zero ? 1 : 2);
+  if (group >= nrhs && use_fused(h, nrhs)) {
+    // a cooperative launch is cheaper from a cached graph; the default
+    // (non-cooperative, PDL) launch runs back to back with the previous kernel
+    if (qtt::fused_cooperative()) return enqueue_graphed(h, x, y, nrhs, ws, st, bar_zero ? 1 : 2);
+    return enqueue_fused(h, x, y, nrhs, ws, st, !bar_zero);
+  }
   if (group >= nrhs) return enqueue_graphed(h, x, y, nrhs, ws, st);
   for (int64_t r0 = 0; r0 < nrhs; r0 += group) {
     const int64_t g = std::min(group, nrhs - r0);

@@ -206,7 +206,7 @@ cudaError_t launch_wide(const LevelArgs& a, cudaStream_t st);
 cudaError_t launch_small(const LevelArgs& a, cudaStream_t st);
 // fused apply (variant kFused): the stages of one apply in one cooperative launch
 constexpr int kFusedWarps = 8;        // warps per CTA (two per SM sub-partition)
-constexpr int kFusedMaxStages = 16;
+constexpr int kFusedMaxStages = 6;
 constexpr size_t kFusedMaxCoreBytes = size_t(4) << 20;   // a fused stage's packed super-core, read from L2
 constexpr size_t kFusedMaxBBytes = size_t(128) << 10;    // one column block of it in smem: K <= 512
 constexpr size_t kFusedMaxL2Bytes = size_t(40) << 20;    // both intermediate buffers of a fused apply
@@ -249,6 +249,7 @@ constexpr int kFusedProfBase = 2 * kFusedMaxStages + 2 + 4 * kFusedMaxStages;
 // past the split-K __syncthreads, tile stored (ns, %globaltimer)
 constexpr int kFusedProfSlots = kFusedProfBase + kFusedMaxStages * kFusedWarps * 4;
 cudaError_t fused_prepare();   // sets the kernel's max dynamic smem
+bool fused_cooperative();       // QTT_FUSED_COOP=1: launch with the cooperative attribute
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st, bool pdl = true);
 // natural-grid offset of QTT index q < 2^30 within one RHS (Morton order,
 // DESIGN.md R18: QTT bit dim*l + a = bit l of coordinate a; x fastest): the

@@ -539,12 +539,29 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_dmma_kernel(const Leve
 // more arrival and the last one resets the counter to 0 for the next launch
 // (all CTAs have passed every barrier by then; the next launch is
 // stream-ordered after this one).
+// Poll until the counter reaches target.  Watchdog: the default launch is not
+// cooperative, so a grid that the device cannot co-schedule
+// (an SM-limited context) would spin forever -- after 4 s the kernel traps
+// instead, and the apply returns a CUDA error (QTT_FUSED_COOP=1 or
+// qtt_set_fused(h, 0) avoid it there).
+__device__ __forceinline__ void grid_spin(const unsigned* bar, unsigned target) {
+  unsigned n = 0;
+  unsigned long long t0 = 0;
+  while (int(ld_acquire_u32(bar) - target) < 0) {
+    if ((++n & 1023u) == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (!t0) t0 = t;
+      else if (t - t0 > 4000000000ull) __trap();
+    }
+  }
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    while (int(ld_acquire_u32(bar) - target) < 0) {
-    }
+    grid_spin(bar, target);
   }
   __syncthreads();
 }
@@ -555,10 +572,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
 __device__ __forceinline__ void grid_arrive(unsigned* bar) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
 }
-__device__ __forceinline__ void grid_wait(unsigned* bar, unsigned target) {
-  while (int(ld_acquire_u32(bar) - target) < 0) {
-  }
-}
+__device__ __forceinline__ void grid_wait(unsigned* bar, unsigned target) { grid_spin(bar, target); }
 
 __device__ __forceinline__ void grid_exit(unsigned* bar, unsigned total) {
   if (threadIdx.x == 0) {
@@ -961,6 +975,11 @@ cudaError_t launch_small(const LevelArgs& a, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, wide::small_dmma_kernel, a);
 }
 
+bool fused_cooperative() {
+  static const bool coop = std::getenv("QTT_FUSED_COOP") != nullptr;
+  return coop;
+}
+
 cudaError_t fused_prepare() {
   const cudaError_t e = cudaFuncSetAttribute(wide::fused_small_kernel<false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedMaxBBytes));
@@ -972,10 +991,15 @@ cudaError_t fused_prepare() {
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st, bool pdl) {
   if (grid < 1 || a.nstages < 1 || a.nstages > kFusedMaxStages || a.smem > kFusedMaxBBytes)
     return cudaErrorInvalidValue;
-  static const bool no_coop = std::getenv("QTT_FUSED_NOCOOP") != nullptr;   // diagnostic (A/B of launch cost)
+  // Not a cooperative launch by default: a cooperative launch costs ~5 us more
+  // host time and waits for the previous kernel to drain (no PDL overlap):
+  // c1 12.3 vs 9.4 us per back-to-back apply.  Co-residency holds without it:
+  // grid <= SMs at one CTA per SM (the kernel's registers fill an SM), and
+  // the grid's own PDL dependents launch only after every CTA of this grid
+  // ran its trigger.  QTT_FUSED_COOP=1 restores the cooperative attribute.
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;     // co-residency for the grid barrier
-  attr[0].val.cooperative = no_coop ? 0 : 1;
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = fused_cooperative() ? 1 : 0;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = pdl && pdl_enabled() ? 1 : 0;
   cudaLaunchConfig_t cfg = {};

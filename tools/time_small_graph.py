@@ -28,6 +28,14 @@ for name in names:
         for _ in range(300):
             op.apply(xt, out=y, stream=st)
         res["host_us"] = round((time.perf_counter() - t0) / 300 * 1e6, 2)
+        # the C ABI alone (ctypes call with prepared arguments, no torch validation)
+        lib = q._lib.load()
+        hx, hy, hs = xt.data_ptr(), y.data_ptr(), st.cuda_stream
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(300):
+            lib.qtt_apply(op.handle, hx, hy, cfg.nrhs, hs)
+        res["host_c_us"] = round((time.perf_counter() - t0) / 300 * 1e6, 2)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
