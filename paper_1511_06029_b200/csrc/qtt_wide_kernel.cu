@@ -180,14 +180,13 @@ __device__ __forceinline__ void tile_store(const double (&c)[NBC][4], const P& p
 // Fused-stage epilogue through shared memory (r_out divides 32, Q a multiple
 // of 16): the 16 x 32 warp tile covers 32 / r_out whole ii blocks, and each
 // block's output is ONE contiguous run of 16 r_out doubles (rows m0..m0+15 of
-// one RHS, b fastest).  The warp writes its tile into its private smem slot
-// `ws` (512 doubles) in run order, then stores the runs with 16-byte stores,
-// 512 contiguous bytes per warp instruction -- instead of 8-byte scattered
-// stores (r_out = 1: 16 instructions of 4 x 64-byte pieces each).
-__device__ __forceinline__ void tile_store_runs(const double (&c)[4][4], const FusedStage& p, int64_t m0, int n_first,
-                                                int lane, double* ws) {
+// one RHS, b fastest).  A warp writes its tile (or its split-K partial) into
+// its smem slot `ws` (512 doubles) in run order; the tile then leaves as 8
+// pieces of 32 16-byte stores, 512 contiguous bytes per warp instruction --
+// instead of 8-byte scattered stores (r_out = 1: 16 instructions of 4 x 64-byte
+// pieces each).
+__device__ __forceinline__ void runs_write(const double (&c)[4][4], int r, double* ws, int lane) {
   const int g = lane >> 2, t0 = lane & 3;
-  const int r = p.r_out;
   const int lr = __ffs(r) - 1;                      // r = 2^lr
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -199,21 +198,31 @@ __device__ __forceinline__ void tile_store_runs(const double (&c)[4][4], const F
         const int b = col & (r - 1);
         ws[((col - b) << 4) + (row << lr) + b] = c[nb][2 * h + e];
       }
-  __syncwarp();
-  const int64_t rowbase = m0 + (((m0 >> p.log2_q) * (p.n_i - 1)) << p.log2_q);
-  const int ii0 = n_first >> lr;
+}
+
+// Store piece k (double2 k*32 + lane of the run-ordered tile) of the tile at
+// rows m0.., columns n_first.. .
+__device__ __forceinline__ void runs_store_piece(const FusedStage& p, int64_t m0, int n_first, int k, int lane,
+                                                 double2 v) {
+  const int lr = __ffs(p.r_out) - 1;
   const int lrun = lr + 4;                          // log2 of a run's length (16 r doubles)
+  const int e2 = (k * 32 + lane) * 2;               // first double of this lane's piece
+  const int ii = (n_first >> lr) + (e2 >> lrun);
+  if (ii < p.n_i) {
+    const int64_t rowbase = m0 + (((m0 >> p.log2_q) * (p.n_i - 1)) << p.log2_q);
+    double* dst = p.out + ((rowbase + (int64_t(ii) << p.log2_q)) << lr) + (e2 & ((1 << lrun) - 1));
+    QTT_CHECK_OUT(p, dst, 2);
+    *reinterpret_cast<double2*>(dst) = v;
+  }
+}
+
+__device__ __forceinline__ void tile_store_runs(const double (&c)[4][4], const FusedStage& p, int64_t m0, int n_first,
+                                                int lane, double* ws) {
+  runs_write(c, p.r_out, ws, lane);
+  __syncwarp();
   const double2* ws2 = reinterpret_cast<const double2*>(ws);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int e2 = (k * 32 + lane) * 2;             // first double of this lane's piece
-    const int ii = ii0 + (e2 >> lrun);
-    if (ii < p.n_i) {
-      double* dst = p.out + ((rowbase + (int64_t(ii) << p.log2_q)) << lr) + (e2 & ((1 << lrun) - 1));
-      QTT_CHECK_OUT(p, dst, 2);
-      *reinterpret_cast<double2*>(dst) = ws2[k * 32 + lane];
-    }
-  }
+  for (int k = 0; k < 8; ++k) runs_store_piece(p, m0, n_first, k, lane, ws2[k * 32 + lane]);
   __syncwarp();
 }
 
@@ -735,6 +744,30 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
       if (wp && lane == 0) wp[3] = globaltimer();
       continue;
     }
+    if (runs) {
+      // split-K with the run-wise epilogue: every warp of the tile writes its
+      // partial in run order, then the tile's ks warps each reduce and store
+      // 8 / ks of its 8 pieces (sum in the fixed order 0..ks-1: the same
+      // values, bitwise, as one warp adding the partials in that order)
+      runs_write(c, p.r_out, wslot, lane);
+      __syncthreads();
+      if (wp && lane == 0) wp[2] = globaltimer();
+      if (live) {
+        const double2* base = reinterpret_cast<const double2*>(red + size_t(slot) * ks * 16 * 32);
+        for (int k = kp; k < 8; k += ks) {
+          double2 acc = base[k * 32 + lane];
+          for (int j = 1; j < ks; ++j) {
+            const double2 o = base[j * 256 + k * 32 + lane];
+            acc.x += o.x;
+            acc.y += o.y;
+          }
+          runs_store_piece(p, m0, cb * kSmallCols, k, lane, acc);
+        }
+      }
+      if (rec) dprof[3] = globaltimer();
+      if (wp && lane == 0) wp[3] = globaltimer();
+      continue;
+    }
     // partials [warp][value][lane]: every access is 32 consecutive doubles (no bank conflicts)
     double* mine = red + size_t(w) * 16 * 32 + lane;
     if (kp) {
@@ -754,8 +787,7 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
           for (int v = 0; v < 4; ++v) c[nb][v] += o[(nb * 4 + v) * 32];
       }
       if (wp && lane == 0) wp[2] = globaltimer_after(c[3][3] + c[0][0]);   // reduced
-      if (runs) tile_store_runs(c, p, m0, cb * kSmallCols, lane, wslot);
-      else tile_store<4>(c, p, m0, cb * kSmallCols, lane);
+      tile_store<4>(c, p, m0, cb * kSmallCols, lane);
       if (rec) dprof[3] = globaltimer();
       if (wp && lane == 0) wp[3] = globaltimer();
     }
@@ -769,7 +801,7 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
 // PROF: the diagnostic instance (QTT_FUSED_PROFILE) with %globaltimer stamps;
 // the production instance carries no profiling code.
 template <bool PROF>
-__global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const FusedArgs a) {
+__global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const __grid_constant__ FusedArgs a) {
   __shared__ __align__(16) double red[kFusedWarps * 32 * 16];   // split-K partials, 32 KiB
   __shared__ __align__(8) uint64_t bar;
   extern __shared__ __align__(128) unsigned char fsm[];          // the super-core block of a unit
