@@ -368,7 +368,15 @@ qtt_status_t qtt_get_apply_plan(qtt_handle_t h, int64_t nrhs, int* launches, int
 
 /* qtt_set_fused -- enable (1, the default) or disable (0) the fused one-launch
  * apply on this handle; disabled, every apply runs the per-stage plan.  Host
- * only; affects applies enqueued after the call. */
+ * only; affects applies enqueued after the call.
+ * The fused launch is NOT a cooperative launch (its grid is at most one CTA
+ * per SM, which a whole device co-schedules).  On a device
+ * partition with fewer SMs than the device reports (an SM-limited MPS client
+ * or green context) its grid barrier could never complete: after 4 s it traps
+ * and the apply's stream reports a CUDA error (QTT_ERROR_CUDA on the next
+ * call that checks it).  There, disable the fused apply with this call, or
+ * set QTT_FUSED_COOP=1 (cooperative launches, which fail cleanly and fall
+ * back to the per-stage plan). */
 qtt_status_t qtt_set_fused(qtt_handle_t h, int enable);
 
 /*

@@ -227,3 +227,47 @@ def test_stage_cap_disables_fused(qtt):
         assert all(s["variant"] != "fused" for s in op.stages(1))
         y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
     oracle.assert_close(y, oracle.apply_dense(cores, x))
+
+
+_MODES_SCRIPT = r"""
+import hashlib, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1511_06029_b200 as q
+from qtt_workload import generate, random_case
+h = hashlib.sha256()
+runs = []
+for name in ("c1", "c2"):
+    cfg, cores, x = generate(name)
+    runs.append((cores, x))
+for seed, d, r, nrhs in ((3, 12, 8, 2), (5, 13, 16, 1), (8, 14, 12, 3), (11, 10, 32, 1)):
+    _, cores, x = random_case(seed + 2100, d, r, nrhs)
+    runs.append((cores, x))
+n_fused = 0
+for cores, x in runs:
+    with q.QttOperator(cores) as op:
+        n_fused += op.stages(x.shape[0])[0]["variant"] == "fused"
+        xt = torch.from_numpy(x).cuda()
+        ws = torch.empty(op.workspace_size(x.shape[0]) // 8 + 64, dtype=torch.float64, device="cuda")
+        for _ in range(3):   # cached workspace (first apply clears it, later ones replay), caller workspace
+            h.update(op.apply(xt).cpu().numpy().tobytes())
+            h.update(op.apply(xt, workspace=ws).cpu().numpy().tobytes())
+print("digest", h.hexdigest(), n_fused)
+"""
+
+
+def test_fused_launch_modes_bitwise():
+    """The fused apply's launch modes give bitwise-identical results: the
+    default non-cooperative PDL launch, the cooperative launch replayed from a
+    cached graph (QTT_FUSED_COOP=1), and the scattered per-warp epilogue
+    (QTT_FUSED_NO_RUNS=1) against the run-wise smem epilogue whose split-K
+    reduction keeps the summation order 0..ks-1."""
+    out = {}
+    for tag, extra in (("default", {}), ("coop", {"QTT_FUSED_COOP": "1"}), ("noruns", {"QTT_FUSED_NO_RUNS": "1"}),
+                       ("forced", {"QTT_FORCE_FUSED": "1"})):
+        r = subprocess.run([sys.executable, "-c", _MODES_SCRIPT, ROOT], env=dict(os.environ, **extra),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "digest" in r.stdout, tag + ": " + r.stdout + r.stderr
+        dig, nf = r.stdout.split("digest")[1].split()
+        out[tag] = (dig, int(nf))
+    assert out["default"][1] >= 2 and out["forced"][1] >= 5, out
+    assert out["default"][0] == out["coop"][0] == out["noruns"][0], out
