@@ -374,7 +374,7 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
             x = torch.from_numpy(x_np).to(dev)
             y = torch.empty_like(x)
             ws = None
-            reps = 5 if name == "c5" else 20
+            reps = 5 if name == "c5" else (200 if name in ("c1", "c2") else 20)
             # the default user path: qtt_apply on the handle's cached workspace
             fn = lambda: op.apply(x, out=y, stream=stream)
             med, mn = time_applies(fn, reps, 3, stream)
