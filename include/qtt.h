@@ -372,7 +372,7 @@ qtt_status_t qtt_get_apply_plan(qtt_handle_t h, int64_t nrhs, int* launches, int
  * The fused launch is NOT a cooperative launch (its grid is at most one CTA
  * per SM, which a whole device co-schedules).  On a device
  * partition with fewer SMs than the device reports (an SM-limited MPS client
- * or green context) its grid barrier could never complete: after 4 s it traps
+ * or green context) its grid barrier could never complete: after 30 s it traps
  * and the apply's stream reports a CUDA error (QTT_ERROR_CUDA on the next
  * call that checks it).  There, disable the fused apply with this call, or
  * set QTT_FUSED_COOP=1 (cooperative launches, which fail cleanly and fall

@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_dmma_kernel(const Leve
 // stream-ordered after this one).
 // Poll until the counter reaches target.  Watchdog: the default launch is not
 // cooperative, so a grid that the device cannot co-schedule
-// (an SM-limited context) would spin forever -- after 4 s the kernel traps
+// (an SM-limited context) would spin forever -- after 30 s the kernel traps
 // instead, and the apply returns a CUDA error (QTT_FUSED_COOP=1 or
 // qtt_set_fused(h, 0) avoid it there).
 __device__ __forceinline__ void grid_spin(const unsigned* bar, unsigned target) {
@@ -561,7 +561,7 @@ __device__ __forceinline__ void grid_spin(const unsigned* bar, unsigned target) 
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (!t0) t0 = t;
-      else if (t - t0 > 4000000000ull) __trap();
+      else if (t - t0 > 30000000000ull) __trap();
     }
   }
 }
