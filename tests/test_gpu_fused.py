@@ -271,3 +271,29 @@ def test_fused_launch_modes_bitwise():
         out[tag] = (dig, int(nf))
     assert out["default"][1] >= 2 and out["forced"][1] >= 5, out
     assert out["default"][0] == out["coop"][0] == out["noruns"][0], out
+
+
+def test_fused_concurrent_with_other_kernels(qtt):
+    """The fused launch is not cooperative: its CTAs may
+    become resident at different times when other kernels hold SMs.  Run
+    fused applies on one stream while large GEMMs run on another stream of
+    the same device; every result must equal the isolated apply bitwise (and
+    the barrier must not hang)."""
+    _, cores, x = generate("c2")
+    xt = torch.from_numpy(x).cuda()
+    a = torch.randn(4096, 4096, dtype=torch.float64, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with qtt.QttOperator(cores) as op:
+        assert op.stages(1)[0]["variant"] == "fused"
+        ref = op.apply(xt).clone()
+        torch.cuda.synchronize()
+        outs = [torch.empty_like(xt) for _ in range(40)]
+        with torch.cuda.stream(s2):
+            c = a
+            for _ in range(6):
+                c = torch.mm(c, a) * 1e-3
+        for y in outs:
+            op.apply(xt, out=y, stream=s1)
+        torch.cuda.synchronize()
+    for y in outs:
+        assert torch.equal(y, ref)
