@@ -613,7 +613,10 @@ __device__ __forceinline__ unsigned long long globaltimer_after(double v) {
 // A rows were written earlier in this launch -- read through L2
 // (ld.global.cg).  K is even (K = n_i r_in, n_i >= 2), so a lane's k-pair is
 // wholly inside K or wholly past it.
-constexpr int kFusedG = 4;
+#ifndef QTT_FUSED_G
+#define QTT_FUSED_G 4
+#endif
+constexpr int kFusedG = QTT_FUSED_G;   // k-steps of A in flight per group (build knob for A/B)
 struct FusedA {
   double2 x[kFusedG], y[kFusedG];
 };
