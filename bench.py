@@ -396,7 +396,34 @@ def extra_measurements(dev, stream, P, BW, max_stage_levels=None):
                 Lf = [a_["k_last"] - a_["k_first"] + 1 for a_ in apply_plan]
                 Fx = sum(2 ** (L_ + 1) * cfg.ranks[a_["k_first"] - 1] * cfg.ranks[a_["k_last"]] * cfg.N * cfg.nrhs
                          for L_, a_ in zip(Lf, apply_plan))
-            out[name] = {"ms_per_apply": med, "ms_single_call_min": mn,
+            if name in ("c1", "c2"):
+                # latency-bound sizes: the device time of an apply without host
+                # launch gaps -- 100 applies captured in one CUDA graph, replayed
+                g = torch.cuda.CUDAGraph()
+                cap = torch.cuda.Stream(dev)           # capture needs a non-default stream
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=cap):
+                    for _ in range(100):
+                        op.apply(x, out=y)
+                with torch.cuda.stream(cap):
+                    g.replay()
+                torch.cuda.synchronize()
+                ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                best = None
+                for _ in range(3):
+                    ga.record(cap)
+                    with torch.cuda.stream(cap):
+                        g.replay()
+                    gb.record(cap)
+                    gb.synchronize()
+                    t_ = ga.elapsed_time(gb) / 100
+                    best = t_ if best is None else min(best, t_)
+                del g
+                in_graph = {"ms_per_apply_in_graph": best,
+                            "in_graph_note": "100 applies captured in one CUDA graph (device time without host launch gaps)"}
+            else:
+                in_graph = {}
+            out[name] = {"ms_per_apply": med, "ms_single_call_min": mn, **in_graph,
                          "gflops_alg2": F / (med * 1e-3) / 1e9,
                          "tflops_executed": Fx / (med * 1e-3) / 1e12, "launches": launches,
                          "apply_plan": [[a_["k_first"], a_["k_last"], a_["variant"]] for a_ in apply_plan],
