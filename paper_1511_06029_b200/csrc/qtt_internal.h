@@ -224,6 +224,15 @@ struct FusedStage {
   // levels per axis = log2n / dim).  The gather is FusedArgs' pre-pass.
   int mout_dim = 0, log2n = 0;
   int runs = 0;                    // run-wise smem epilogue (r_out | 32, Q % 16 == 0, QTT-order output)
+  // host-computed work decomposition (no integer division in the kernel):
+  int mtiles = 0;                  // 16-row tiles (M + 15) / 16
+  int rgroups = 0;                 // row groups of kFusedWarps / ks tiles; units = rgroups * ncb
+  int units = 0;
+  uint32_t rg_mul = 0;             // u / rgroups = rg_mul ? umulhi(u, rg_mul) >> rg_shr : u >> rg_shr
+  int rg_shr = 0;
+  int cps = 0;                     // k-steps per split-K part, ceil(nchunks / ks)
+  int lks = 0;                     // log2 ks
+  int lr = 0;                      // log2 r_out (run-wise epilogue)
 };
 struct FusedArgs {
   FusedStage st[kFusedMaxStages];

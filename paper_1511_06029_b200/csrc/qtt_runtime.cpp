@@ -519,6 +519,28 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
     f.ncb = sp.ncb;
     f.ks = std::max(1, sp.ksplit);
     f.log2n = h->d;
+    // work decomposition, precomputed (the kernel only multiplies and shifts)
+    f.mtiles = int((f.M + qtt::kSmallRows - 1) / qtt::kSmallRows);
+    {
+      const int slots = qtt::kFusedWarps / f.ks;
+      f.rgroups = (f.mtiles + slots - 1) / slots;
+      f.units = f.rgroups * f.ncb;
+      const uint32_t dv = uint32_t(f.rgroups);
+      int l = 0;
+      while ((uint32_t(1) << l) < dv) ++l;
+      if ((dv & (dv - 1)) == 0) {          // a power of two: a shift
+        f.rg_mul = 0;
+        f.rg_shr = l;
+      } else {                             // round-up magic number, exact for u < 2^31
+        f.rg_mul = uint32_t(((uint64_t(1) << (31 + l)) / dv) + 1);
+        f.rg_shr = l - 1;
+      }
+      f.cps = (f.nchunks + f.ks - 1) / f.ks;
+      f.lks = f.ks >= 8 ? 3 : f.ks >= 4 ? 2 : f.ks >= 2 ? 1 : 0;
+      int lr = 0;
+      while ((1 << lr) < sp.r_out) ++lr;
+      f.lr = lr;
+    }
     f.mout_dim = last ? morton_dim : 0;      // the scatter is the last stage's epilogue
     static const bool no_runs = std::getenv("QTT_FUSED_NO_RUNS") != nullptr;   // A/B
     f.runs = !no_runs && f.mout_dim == 0 && sp.r_out <= 32 && (32 % sp.r_out) == 0 && f.log2_q >= 4 ? 1 : 0;

@@ -200,32 +200,6 @@ __device__ __forceinline__ void runs_write(const double (&c)[4][4], int r, doubl
       }
 }
 
-// Store piece k (double2 k*32 + lane of the run-ordered tile) of the tile at
-// rows m0.., columns n_first.. .
-__device__ __forceinline__ void runs_store_piece(const FusedStage& p, int64_t m0, int n_first, int k, int lane,
-                                                 double2 v) {
-  const int lr = __ffs(p.r_out) - 1;
-  const int lrun = lr + 4;                          // log2 of a run's length (16 r doubles)
-  const int e2 = (k * 32 + lane) * 2;               // first double of this lane's piece
-  const int ii = (n_first >> lr) + (e2 >> lrun);
-  if (ii < p.n_i) {
-    const int64_t rowbase = m0 + (((m0 >> p.log2_q) * (p.n_i - 1)) << p.log2_q);
-    double* dst = p.out + ((rowbase + (int64_t(ii) << p.log2_q)) << lr) + (e2 & ((1 << lrun) - 1));
-    QTT_CHECK_OUT(p, dst, 2);
-    *reinterpret_cast<double2*>(dst) = v;
-  }
-}
-
-__device__ __forceinline__ void tile_store_runs(const double (&c)[4][4], const FusedStage& p, int64_t m0, int n_first,
-                                                int lane, double* ws) {
-  runs_write(c, p.r_out, ws, lane);
-  __syncwarp();
-  const double2* ws2 = reinterpret_cast<const double2*>(ws);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) runs_store_piece(p, m0, n_first, k, lane, ws2[k * 32 + lane]);
-  __syncwarp();
-}
-
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -668,48 +642,66 @@ __device__ __forceinline__ void fused_mma(const FusedA& o, const double2* sB, in
 // 0..ks-1 (deterministic; ks is fixed per plan, so results do not depend on
 // nrhs) and runs the row-separation epilogue.  Units go to the CTAs
 // round-robin, consecutive units sharing cb (its block stays hot in L2).
-// Work units of a fused stage: (32-column block, group of row tiles).
-__device__ __forceinline__ int64_t fused_rgroups(const FusedStage& p) {
-  const int slots = kFusedWarps / p.ks;
-  const int64_t mtiles = (p.M + kSmallRows - 1) / kSmallRows;
-  return (mtiles + slots - 1) / slots;
+// Work units of a fused stage: (32-column block, group of row tiles), all
+// counts precomputed on the host (FusedStage): the kernel multiplies and
+// shifts, it never divides (an integer division is ~20-70 instructions, and
+// at c1's size the stage is instruction-latency bound).
+__device__ __forceinline__ int fused_cb(const FusedStage& p, int u) {      // u / rgroups
+  return p.rg_mul ? int(__umulhi(uint32_t(u), p.rg_mul) >> p.rg_shr) : (u >> p.rg_shr);
 }
 
-// Thread 0: bulk-copy unit u's super-core block (column block u / rgroups) into sB.
-__device__ __forceinline__ void fused_issue_b(const FusedStage& p, int64_t u, int64_t rgroups, double2* sB,
-                                              uint64_t* bar) {
-  const int cb = int(u / rgroups);
+// Thread 0: bulk-copy column block cb's super-core block into sB.
+__device__ __forceinline__ void fused_issue_b(const FusedStage& p, int cb, double2* sB, uint64_t* bar) {
   const uint32_t bbytes = uint32_t(p.nchunks) * 128u * 16u;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // sB's generic reads before the async write
   dmma::mbar_arrive_expect_tx(bar, bbytes);
   dmma::bulk_g2s(sB, p.bpack + size_t(cb) * p.nchunks * 256, bbytes, bar);
 }
 
+// Run-wise epilogue pieces with the tile's row base precomputed: piece k
+// (double2 k * 32 + lane of the run-ordered tile) goes to out at run ii.
+__device__ __forceinline__ void runs_store_piece_rb(const FusedStage& p, int64_t rowbase, int ii0, int k, int lane,
+                                                    double2 v) {
+  const int lr = p.lr, lrun = lr + 4;
+  const int e2 = (k * 32 + lane) * 2;
+  const int ii = ii0 + (e2 >> lrun);
+  if (ii < p.n_i) {
+    double* dst = p.out + ((rowbase + (int64_t(ii) << p.log2_q)) << lr) + (e2 & ((1 << lrun) - 1));
+    QTT_CHECK_OUT(p, dst, 2);
+    *reinterpret_cast<double2*>(dst) = v;
+  }
+}
+
+// One stage of the fused apply.  A unit of work is one 32-column block cb of
+// the stage's output and kFusedWarps / KS row tiles of 16 rows: the CTA
+// copies the super-core block of cb (K x 32 doubles) into shared memory with
+// one bulk copy, and its warps take the row tiles, KS warps per tile, each
+// over a contiguous 1/KS of the k-steps; the KS partial tiles meet in shared
+// memory and are added in the fixed order 0..KS-1 (deterministic; KS is
+// fixed per plan, so results do not depend on nrhs) before the
+// row-separation epilogue.  Units go to the CTAs round-robin, consecutive
+// units sharing cb (its block stays hot in L2).
 template <bool COHERENT, bool PROF>
 __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, double2* sB, uint64_t* bar,
                                             uint32_t& nwait, bool prefetched, int lane,
                                             unsigned long long* dprof = nullptr,
                                             unsigned long long* wprof = nullptr) {
+  const int lks = p.lks, KS = 1 << lks;              // warps per tile (power of two)
+  const int lslots = 3 - lks;                         // log2(kFusedWarps / KS)
   const int w = threadIdx.x >> 5;
-  const int ks = p.ks;
-  const int slots = kFusedWarps / ks;
-  const int slot = w / ks, kp = w - slot * ks;
-  const int64_t mtiles = (p.M + kSmallRows - 1) / kSmallRows;
-  const int64_t rgroups = fused_rgroups(p);
-  const int64_t units = rgroups * p.ncb;
-  const int cps = (p.nchunks + ks - 1) / ks;
-  const int q0 = min(p.nchunks, kp * cps), q1 = min(p.nchunks, q0 + cps);
+  const int slot = w >> lks, kp = w & (KS - 1);
+  const int q0 = min(p.nchunks, kp * p.cps), q1 = min(p.nchunks, q0 + p.cps);
   const int t0 = lane & 3, g = lane >> 2;
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const int cb = int(u / rgroups);
-    const int64_t mt = (u - int64_t(cb) * rgroups) * slots + slot;
-    const bool live = mt < mtiles;
-    const int64_t m0 = mt * kSmallRows;
-    const bool first = u == blockIdx.x;
+  for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    const int cb = fused_cb(p, u);
+    const int mt = ((u - cb * p.rgroups) << lslots) + slot;
+    const bool live = mt < p.mtiles;
+    const int64_t m0 = int64_t(mt) * kSmallRows;
+    const bool first = u == int(blockIdx.x);
     if (!first) __syncthreads();           // the previous unit is done with sB and red
     const bool rec = PROF && dprof && threadIdx.x == 0 && first;
     if (rec) dprof[0] = globaltimer();
-    if (threadIdx.x == 0 && !(first && prefetched)) fused_issue_b(p, u, rgroups, sB, bar);
+    if (threadIdx.x == 0 && !(first && prefetched)) fused_issue_b(p, cb, sB, bar);
     // A fragments of the first k-steps while the super-core block lands
     const bool ok0 = live && m0 + g < p.M, ok1 = live && m0 + g + 8 < p.M;
     const double* a0 = p.in + (m0 + g) * p.K + 2 * t0;
@@ -735,38 +727,46 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
     }
     if (rec) dprof[2] = globaltimer_after(c[0][0]);
     if (wp && lane == 0) wp[1] = globaltimer_after(c[3][3] + c[0][0]);
-    // run-wise epilogue: every row of the tile in one RHS (Q % 16 == 0), r_out | 32
-    const bool runs = p.runs;
-    double* wslot = red + size_t(w) * 16 * 32;     // this warp's own partial slot (unused by it otherwise)
-    if (ks == 1) {
-      if (live) {
-        if (runs) tile_store_runs(c, p, m0, cb * kSmallCols, lane, wslot);
-        else tile_store<4>(c, p, m0, cb * kSmallCols, lane);
+    double* wslot = red + size_t(w) * 16 * 32;     // this warp's own partial slot
+    if (p.runs) {
+      // run-wise epilogue: every row of the tile in one RHS (Q % 16 == 0), r_out | 32
+      const int64_t rowbase = m0 + (((m0 >> p.log2_q) * (p.n_i - 1)) << p.log2_q);
+      const int ii0 = (cb * kSmallCols) >> p.lr;
+      runs_write(c, p.r_out, wslot, lane);
+      if (KS == 1) {
+        __syncwarp();
+        if (live) {
+          const double2* ws2 = reinterpret_cast<const double2*>(wslot);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) runs_store_piece_rb(p, rowbase, ii0, k, lane, ws2[k * 32 + lane]);
+        }
+        __syncwarp();
+      } else {
+        // split-K: every warp of the tile wrote its partial in run order; the
+        // tile's KS warps each reduce and store 8 / KS of its 8 pieces (sum in
+        // the fixed order 0..KS-1: the same values, bitwise, as one warp
+        // adding the partials in that order)
+        __syncthreads();
+        if (wp && lane == 0) wp[2] = globaltimer();
+        if (live) {
+          const double2* base = reinterpret_cast<const double2*>(red + size_t(slot) * KS * 16 * 32);
+          for (int k = kp; k < 8; k += KS) {
+            double2 acc = base[k * 32 + lane];
+            for (int j = 1; j < KS; ++j) {
+              const double2 o = base[j * 256 + k * 32 + lane];
+              acc.x += o.x;
+              acc.y += o.y;
+            }
+            runs_store_piece_rb(p, rowbase, ii0, k, lane, acc);
+          }
+        }
       }
       if (rec) dprof[3] = globaltimer();
       if (wp && lane == 0) wp[3] = globaltimer();
       continue;
     }
-    if (runs) {
-      // split-K with the run-wise epilogue: every warp of the tile writes its
-      // partial in run order, then the tile's ks warps each reduce and store
-      // 8 / ks of its 8 pieces (sum in the fixed order 0..ks-1: the same
-      // values, bitwise, as one warp adding the partials in that order)
-      runs_write(c, p.r_out, wslot, lane);
-      __syncthreads();
-      if (wp && lane == 0) wp[2] = globaltimer();
-      if (live) {
-        const double2* base = reinterpret_cast<const double2*>(red + size_t(slot) * ks * 16 * 32);
-        for (int k = kp; k < 8; k += ks) {
-          double2 acc = base[k * 32 + lane];
-          for (int j = 1; j < ks; ++j) {
-            const double2 o = base[j * 256 + k * 32 + lane];
-            acc.x += o.x;
-            acc.y += o.y;
-          }
-          runs_store_piece(p, m0, cb * kSmallCols, k, lane, acc);
-        }
-      }
+    if (KS == 1) {
+      if (live) tile_store<4>(c, p, m0, cb * kSmallCols, lane);
       if (rec) dprof[3] = globaltimer();
       if (wp && lane == 0) wp[3] = globaltimer();
       continue;
@@ -782,7 +782,7 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
     __syncthreads();
     if (wp && lane == 0) wp[2] = globaltimer();
     if (kp == 0 && live) {
-      for (int j = 1; j < ks; ++j) {
+      for (int j = 1; j < KS; ++j) {
         const double* o = red + size_t(w + j) * 16 * 32 + lane;
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb)
@@ -817,8 +817,8 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const __g
   // the first stage's super-core block is static (written at qtt_create, never
   // by a kernel): its copy starts before griddepcontrol.wait, overlapping the
   // previous kernel on the stream
-  const bool prefetch0 = int64_t(blockIdx.x) < fused_rgroups(a.st[0]) * a.st[0].ncb;
-  if (threadIdx.x == 0 && prefetch0) fused_issue_b(a.st[0], blockIdx.x, fused_rgroups(a.st[0]), sB, &bar);
+  const bool prefetch0 = int(blockIdx.x) < a.st[0].units;
+  if (threadIdx.x == 0 && prefetch0) fused_issue_b(a.st[0], fused_cb(a.st[0], blockIdx.x), sB, &bar);
   pdl_wait();
   unsigned long long* prof = (PROF && a.prof) ? a.prof + size_t(blockIdx.x) * kFusedProfSlots : nullptr;
   if (prof && threadIdx.x == 0) prof[0] = globaltimer();
@@ -864,13 +864,12 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const __g
       if (threadIdx.x == 0) {
         grid_arrive(a.bar);
         const FusedStage& nx = a.st[s + 1];
-        const int64_t rg = fused_rgroups(nx);
-        if (int64_t(blockIdx.x) < rg * nx.ncb) fused_issue_b(nx, blockIdx.x, rg, sB, &bar);
+        if (int(blockIdx.x) < nx.units) fused_issue_b(nx, fused_cb(nx, blockIdx.x), sB, &bar);
         grid_wait(a.bar, ++nbar * gridDim.x);
       } else {
         ++nbar;
       }
-      prefetched = int64_t(blockIdx.x) < fused_rgroups(a.st[s + 1]) * a.st[s + 1].ncb;
+      prefetched = int(blockIdx.x) < a.st[s + 1].units;
       __syncthreads();
     }
     if (prof && threadIdx.x == 0) prof[2 + 2 * s] = globaltimer();
