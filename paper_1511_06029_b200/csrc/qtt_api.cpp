@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -460,18 +461,45 @@ qtt_status_t qtt_apply_ws(qtt_handle_t h, const double* x, double* y, int64_t nr
   }
 }
 
+#ifdef QTT_HOST_PROFILE   // diagnostic build: host time per step of qtt_apply, printed every 2000 calls
+struct HostProf {
+  double t[8] = {};
+  long n = 0;
+  std::chrono::steady_clock::time_point last;
+  void mark(int i) {
+    const auto now = std::chrono::steady_clock::now();
+    if (i > 0) t[i] += std::chrono::duration<double, std::micro>(now - last).count();
+    last = now;
+  }
+  void done() {
+    if (++n % 500) return;
+    std::fprintf(stderr, "qtt host us/call: args %.2f guard+capq %.2f group %.2f acquire %.2f enqueue %.2f release %.2f\n",
+                 t[1] / n, t[2] / n, t[3] / n, t[4] / n, t[5] / n, t[6] / n);
+  }
+};
+static HostProf hprof;
+#define HP(i) hprof.mark(i)
+#else
+#define HP(i)
+#endif
+
 qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs, qtt_stream_t stream) {
+  HP(0);
   qtt_status_t s = check_apply_args(h, x, y, nrhs);
+  HP(1);
   if (s != QTT_SUCCESS) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   try {
     DeviceGuard g(h->device);
     const bool capturing = stream_is_capturing(st);
+    HP(2);
     void* old_ws = h->ws;
     bool grew = false;
     int64_t group = cached_group(h, nrhs);
+    HP(3);
     qtt_status_t so = cached_acquire(&h->ws, &h->ws_bytes, &h->ws_used, h->ws_pending, ws_bytes_for(h, group), st,
                                      capturing, &grew);
+    HP(4);
     while (so == QTT_ERROR_OUT_OF_MEMORY && group > 1 && !capturing) {   // smaller RHS groups
       group = (group + 1) / 2;
       bool g2 = false;
@@ -485,8 +513,13 @@ qtt_status_t qtt_apply(qtt_handle_t h, const double* x, double* y, int64_t nrhs,
     // the cached workspace's grid-barrier words stay 0 once cleared (every
     // fused launch leaves them so; per-stage applies clear the whole header)
     if (so == QTT_SUCCESS) so = enqueue_groups(h, x, y, nrhs, group, h->ws, st, h->ws_header_zero);
+    HP(5);
     if (so == QTT_SUCCESS) h->ws_header_zero = true;
     if (so == QTT_SUCCESS) so = cached_release(h->ws_used, &h->ws_pending, st, capturing);
+    HP(6);
+#ifdef QTT_HOST_PROFILE
+    hprof.done();
+#endif
     return so;
   } catch (...) {
     return QTT_ERROR_CUDA;
