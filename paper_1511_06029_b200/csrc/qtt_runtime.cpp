@@ -543,7 +543,12 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
     }
     f.mout_dim = last ? morton_dim : 0;      // the scatter is the last stage's epilogue
     static const bool no_runs = std::getenv("QTT_FUSED_NO_RUNS") != nullptr;   // A/B
-    f.runs = !no_runs && f.mout_dim == 0 && sp.r_out <= 32 && (32 % sp.r_out) == 0 && f.log2_q >= 4 ? 1 : 0;
+    // (a Morton-scattering last stage has r_out = 1: a piece is two consecutive
+    // QTT indices x0 = 0, 1, i.e. two adjacent grid points: one 16-byte store)
+    f.runs = !no_runs && (f.mout_dim == 0 || sp.r_out == 1) && sp.r_out <= 32 && (32 % sp.r_out) == 0 &&
+                     f.log2_q >= 4
+                 ? 1
+                 : 0;
     if (s == 0 && morton_dim) f.in = buf[1];
     a.smem = std::max<size_t>(a.smem, size_t(sp.nchunks) * 128 * 16);
     max_wt = std::max<int64_t>(max_wt, (f.M + qtt::kSmallRows - 1) / qtt::kSmallRows * f.ncb * f.ks);

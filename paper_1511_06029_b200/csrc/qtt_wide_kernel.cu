@@ -666,7 +666,12 @@ __device__ __forceinline__ void runs_store_piece_rb(const FusedStage& p, int64_t
   const int e2 = (k * 32 + lane) * 2;
   const int ii = ii0 + (e2 >> lrun);
   if (ii < p.n_i) {
-    double* dst = p.out + ((rowbase + (int64_t(ii) << p.log2_q)) << lr) + (e2 & ((1 << lrun) - 1));
+    int64_t o = ((rowbase + (int64_t(ii) << p.log2_q)) << lr) + (e2 & ((1 << lrun) - 1));
+    if (p.mout_dim) {   // fused grid apply (r_out = 1): QTT index o -> its natural-order grid point
+      const int64_t nmask = (int64_t(1) << p.log2n) - 1;
+      o = (o & ~nmask) + morton_natural(o & nmask, p.mout_dim, p.log2n / p.mout_dim);
+    }
+    double* dst = p.out + o;
     QTT_CHECK_OUT(p, dst, 2);
     *reinterpret_cast<double2*>(dst) = v;
   }
