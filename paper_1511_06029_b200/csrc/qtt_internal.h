@@ -232,6 +232,8 @@ struct FusedStage {
   int rg_shr = 0;
   int cps = 0;                     // k-steps per split-K part, ceil(nchunks / ks)
   int lks = 0;                     // log2 ks
+  int in_dim = 0;                  // the A rows come from a natural-order grid (fused grid apply, stage 0):
+                                   // each 16-byte A load gathers two adjacent grid points (Morton, R18)
   int lr = 0;                      // log2 r_out (run-wise epilogue)
 };
 struct FusedArgs {

@@ -549,12 +549,20 @@ qtt_status_t enqueue_fused(qtt_plan* h, const double* x, double* y, int64_t nrhs
                      f.log2_q >= 4
                  ? 1
                  : 0;
-    if (s == 0 && morton_dim) f.in = buf[1];
+    // fused grid apply: stage 0 gathers the natural-order grid in its A loads
+    // (QTT_FUSED_PREPASS=1: a gather pass into buffer 1 and a grid barrier, A/B)
+    // (the gather in the loads recomputes a Morton index per 16-byte load of
+    // every unit: cheaper than the pass + barrier only for small grids --
+    // c1 9.5 vs 10.3 us, c2 29.6 vs 27.6 us)
+    static const bool prepass_env = std::getenv("QTT_FUSED_PREPASS") != nullptr;
+    const bool prepass = prepass_env || int64_t(h->N) * nrhs > 8192;
+    if (s == 0 && morton_dim && prepass) f.in = buf[1];
+    f.in_dim = (s == 0 && morton_dim && !prepass) ? morton_dim : 0;
     a.smem = std::max<size_t>(a.smem, size_t(sp.nchunks) * 128 * 16);
     max_wt = std::max<int64_t>(max_wt, (f.M + qtt::kSmallRows - 1) / qtt::kSmallRows * f.ncb * f.ks);
     in = f.out;
   }
-  if (morton_dim) {   // stage 0 reads the gathered copy in buffer 1 (stage 1 writes it after a barrier)
+  if (morton_dim && a.st[0].in_dim == 0) {   // stage 0 reads the gathered copy in buffer 1 (after a barrier)
     a.pre_src = x;
     a.pre_dst = buf[1];
     a.pre_dim = morton_dim;

@@ -595,7 +595,10 @@ struct FusedA {
   double2 x[kFusedG], y[kFusedG];
 };
 
-template <bool COHERENT>
+// MORTON (fused grid apply, stage 0): a0 / a1 are QTT-order offsets of the
+// lane's two rows from p.in, which holds the natural-order grid; each 16-byte
+// load takes QTT indices 2t, 2t + 1 (x0 = 0, 1): two adjacent grid points.
+template <bool COHERENT, bool MORTON = false>
 __device__ __forceinline__ void fused_load_a(FusedA& o, const double* a0, const double* a1, int q, int q1, int K,
                                              int t0, bool ok0, bool ok1, const FusedStage& p) {
 #pragma unroll
@@ -604,8 +607,16 @@ __device__ __forceinline__ void fused_load_a(FusedA& o, const double* a0, const 
     const bool vk = qq < q1 && (qq * kSmallK + 2 * t0 < K);
     o.x[j] = make_double2(0.0, 0.0);
     o.y[j] = make_double2(0.0, 0.0);
-    const double2* pa0 = reinterpret_cast<const double2*>(a0 + qq * kSmallK);
-    const double2* pa1 = reinterpret_cast<const double2*>(a1 + qq * kSmallK);
+    const double* e0 = a0 + qq * kSmallK;
+    const double* e1 = a1 + qq * kSmallK;
+    if (MORTON) {
+      const int64_t nmask = (int64_t(1) << p.log2n) - 1, lv = p.log2n / p.in_dim;
+      const int64_t i0 = e0 - p.in, i1 = e1 - p.in;
+      e0 = p.in + ((i0 & ~nmask) + morton_natural(i0 & nmask, p.in_dim, int(lv)));
+      e1 = p.in + ((i1 & ~nmask) + morton_natural(i1 & nmask, p.in_dim, int(lv)));
+    }
+    const double2* pa0 = reinterpret_cast<const double2*>(e0);
+    const double2* pa1 = reinterpret_cast<const double2*>(e1);
     if (vk && ok0) o.x[j] = COHERENT ? __ldcg(pa0) : __ldg(pa0);
     if (vk && ok1) o.y[j] = COHERENT ? __ldcg(pa1) : __ldg(pa1);
   }
@@ -686,7 +697,7 @@ __device__ __forceinline__ void runs_store_piece_rb(const FusedStage& p, int64_t
 // fixed per plan, so results do not depend on nrhs) before the
 // row-separation epilogue.  Units go to the CTAs round-robin, consecutive
 // units sharing cb (its block stays hot in L2).
-template <bool COHERENT, bool PROF>
+template <bool COHERENT, bool PROF, bool MORTON = false>
 __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, double2* sB, uint64_t* bar,
                                             uint32_t& nwait, bool prefetched, int lane,
                                             unsigned long long* dprof = nullptr,
@@ -712,7 +723,7 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
     const double* a0 = p.in + (m0 + g) * p.K + 2 * t0;
     const double* a1 = a0 + int64_t(8) * p.K;
     FusedA fa, fb;
-    if (q0 < q1) fused_load_a<COHERENT>(fa, a0, a1, q0, q1, p.K, t0, ok0, ok1, p);
+    if (q0 < q1) fused_load_a<COHERENT, MORTON>(fa, a0, a1, q0, q1, p.K, t0, ok0, ok1, p);
     double c[4][4];
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb) c[nb][0] = c[nb][1] = c[nb][2] = c[nb][3] = 0.0;
@@ -723,10 +734,10 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
     if (wp && lane == 0) wp[0] = globaltimer_after(fa.x[0].x);
     if (live) {
       for (int q = q0; q < q1; q += 2 * kFusedG) {
-        if (q + kFusedG < q1) fused_load_a<COHERENT>(fb, a0, a1, q + kFusedG, q1, p.K, t0, ok0, ok1, p);
+        if (q + kFusedG < q1) fused_load_a<COHERENT, MORTON>(fb, a0, a1, q + kFusedG, q1, p.K, t0, ok0, ok1, p);
         fused_mma(fa, sB, q, q1, lane, c);
         if (q + kFusedG >= q1) break;
-        if (q + 2 * kFusedG < q1) fused_load_a<COHERENT>(fa, a0, a1, q + 2 * kFusedG, q1, p.K, t0, ok0, ok1, p);
+        if (q + 2 * kFusedG < q1) fused_load_a<COHERENT, MORTON>(fa, a0, a1, q + 2 * kFusedG, q1, p.K, t0, ok0, ok1, p);
         fused_mma(fb, sB, q + kFusedG, q1, lane, c);
       }
     }
@@ -808,7 +819,7 @@ __device__ __forceinline__ void fused_stage(const FusedStage& p, double* red, do
 // intermediates (two ping-pong buffers) stay in L2.
 // PROF: the diagnostic instance (QTT_FUSED_PROFILE) with %globaltimer stamps;
 // the production instance carries no profiling code.
-template <bool PROF>
+template <bool PROF, bool MORTON>
 __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const __grid_constant__ FusedArgs a) {
   __shared__ __align__(16) double red[kFusedWarps * 32 * 16];   // split-K partials, 32 KiB
   __shared__ __align__(8) uint64_t bar;
@@ -851,7 +862,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_small_kernel(const __g
       }
       unsigned long long* dp = prof ? prof + 2 * kFusedMaxStages + 2 + 4 * s : nullptr;
       unsigned long long* wpp = prof ? prof + kFusedProfBase + s * kFusedWarps * 4 : nullptr;
-      if (s == 0 && !a.pre_dim)   // x itself: written before this launch, read-only path
+      if (MORTON && s == 0)           // the natural-order grid, gathered by the A loads (own instance)
+        fused_stage<false, PROF, true>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp, wpp);
+      else if (s == 0 && !a.pre_dim)  // x itself: written before this launch, read-only path
         fused_stage<false, PROF>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp, wpp);
       else                        // written earlier in this launch: through L2
         fused_stage<true, PROF>(a.st[s], red, sB, &bar, nwait, prefetched, lane, dp, wpp);
@@ -1020,11 +1033,12 @@ bool fused_cooperative() {
 }
 
 cudaError_t fused_prepare() {
-  const cudaError_t e = cudaFuncSetAttribute(wide::fused_small_kernel<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedMaxBBytes));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(wide::fused_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              int(kFusedMaxBBytes));
+  for (auto f : {wide::fused_small_kernel<false, false>, wide::fused_small_kernel<true, false>,
+                 wide::fused_small_kernel<false, true>, wide::fused_small_kernel<true, true>}) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFusedMaxBBytes));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st, bool pdl) {
@@ -1048,8 +1062,11 @@ cudaError_t launch_fused(const FusedArgs& a, int grid, cudaStream_t st, bool pdl
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return a.prof ? cudaLaunchKernelEx(&cfg, wide::fused_small_kernel<true>, a)
-                : cudaLaunchKernelEx(&cfg, wide::fused_small_kernel<false>, a);
+  if (a.st[0].in_dim)   // fused grid apply gathering in stage 0: its own instance
+    return a.prof ? cudaLaunchKernelEx(&cfg, wide::fused_small_kernel<true, true>, a)
+                  : cudaLaunchKernelEx(&cfg, wide::fused_small_kernel<false, true>, a);
+  return a.prof ? cudaLaunchKernelEx(&cfg, wide::fused_small_kernel<true, false>, a)
+                : cudaLaunchKernelEx(&cfg, wide::fused_small_kernel<false, false>, a);
 }
 
 cudaError_t launch_shard_reduce(const double* recv, double* y, int parts, int64_t count, cudaStream_t st,
