@@ -410,7 +410,11 @@ double fused_stage_seconds(const int64_t* ranks, int k0, int k1, double rows, St
   sp->ksplit = ks;
   const double per_smsp = std::ceil(tiles * ks / (kSms * 4));   // warp tiles one sub-partition runs
   const double steps = std::ceil(double(sp->nchunks) / ks);
-  sp->est_seconds = per_smsp * steps * kStep + kLat + (ks > 1 ? kRed : 0.0) + kBar;
+  // + a tenth of the stage's executed flops at the FP64 peak: breaks the
+  // model's ties toward the cheaper super-cores (c1: [1-7] [8-12], 10.5
+  // MFLOP, measured 7.5 us against 7.8 us for [1-8] [9-12], 18.9 MFLOP)
+  const double flops = 2.0 * (rows / n_i) * double(K) * double(nout);
+  sp->est_seconds = per_smsp * steps * kStep + kLat + (ks > 1 ? kRed : 0.0) + kBar + 0.1 * flops / kFp64;
   return sp->est_seconds;
 }
 
