@@ -196,3 +196,28 @@ def test_forced_stage_split_switch():
     assert run("1-7,8-9") == default            # does not reach d = 24
     assert run("2-24") == default               # does not start at level 1
     assert run("garbage") == default
+
+
+def test_fused_unit_division_magic():
+    """The fused kernel divides a work-unit index u < 2^31 by its row-group
+    count with a multiply and a shift (qtt_runtime.cpp enqueue_fused,
+    qtt_wide_kernel.cu fused_cb): a power of two is a shift, otherwise
+    mul = floor(2^(31+l) / d) + 1 with l = ceil(log2 d) and
+    u / d = umulhi(u, mul) >> (l - 1).  Checked here against integer division
+    for every divisor up to 4096 on the units a kernel can see, and on
+    random indices up to 2^31 - 1."""
+    import random
+    rng = random.Random(0)
+    for d in range(1, 4097):
+        l = 0
+        while (1 << l) < d:
+            l += 1
+        if d & (d - 1) == 0:
+            div = lambda u: u >> l
+        else:
+            mul = ((1 << (31 + l)) // d) + 1
+            assert mul < (1 << 32)
+            div = lambda u: ((u * mul) >> 32) >> (l - 1)
+        us = list(range(0, 4 * d + 3)) + [rng.randrange(0, 1 << 31) for _ in range(64)] + [(1 << 31) - 1]
+        for u in us:
+            assert div(u) == u // d, (d, u)
