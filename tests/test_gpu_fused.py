@@ -297,3 +297,32 @@ def test_fused_concurrent_with_other_kernels(qtt):
         torch.cuda.synchronize()
     for y in outs:
         assert torch.equal(y, ref)
+
+
+_GRID_SCRIPT = r"""
+import hashlib, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1511_06029_b200 as q
+from qtt_workload import generate
+h = hashlib.sha256()
+for name, dim, nrhs in (("c1", 3, 1), ("c1", 2, 2), ("c1", 1, 1)):
+    cfg, cores, _ = generate(name)
+    x = np.random.default_rng(nrhs + dim).standard_normal((nrhs, cfg.N))
+    with q.QttOperator(cores) as op:
+        g = op.apply_grid(torch.from_numpy(x).cuda(), dim)
+        h.update(g.cpu().numpy().tobytes())
+print("digest", h.hexdigest())
+"""
+
+
+def test_fused_grid_gather_modes_bitwise():
+    """Fused grid apply: the Morton gather inside stage 0's A loads (default
+    for small grids) and the gather pre-pass + grid barrier
+    (QTT_FUSED_PREPASS=1) give bitwise-identical results."""
+    out = []
+    for extra in ({}, {"QTT_FUSED_PREPASS": "1"}):
+        r = subprocess.run([sys.executable, "-c", _GRID_SCRIPT, ROOT], env=dict(os.environ, **extra),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and "digest" in r.stdout, r.stdout + r.stderr
+        out.append(r.stdout.split("digest")[1].strip())
+    assert out[0] == out[1]
