@@ -132,6 +132,12 @@ struct LevelArgs {
   // debug builds (-DQTT_BOUNDS_CHECK): doubles addressable from `out` (0 = unchecked);
   // every epilogue store traps outside [out, out + out_limit)
   int64_t out_limit = 0;
+  // wide variant, plain epilogue: col_off[n] = (ii << log2_q) r_out + b for
+  // output column n = ii r_out + b (host-computed, L1-cached), and the tile ->
+  // (row tile, column block) split as a multiply-shift (ncb_mul = 0: divide)
+  const int64_t* col_off = nullptr;
+  uint32_t ncb_mul = 0;
+  int ncb_shr = 0;
   int ksplit = 1;
   int kcps = 0;                    // k-chunks per split
   double* partial = nullptr;       // [output tiles][ksplit][consumer warps][split_slot_doubles(NB)]

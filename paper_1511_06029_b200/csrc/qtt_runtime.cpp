@@ -240,10 +240,12 @@ size_t ws_bytes_for(const qtt_plan* h, int64_t nrhs) {
 }
 
 void free_plan(qtt_plan* h) {
-  for (auto& S : h->stages) {
-    if (S.d_bpack) cudaFree(S.d_bpack);
-    if (S.d_core) cudaFree(S.d_core);
-  }
+  for (auto* v : {&h->stages, &h->fstages})
+    for (auto& S : *v) {
+      if (S.d_bpack) cudaFree(S.d_bpack);
+      if (S.d_core) cudaFree(S.d_core);
+      if (S.d_coloff) cudaFree(S.d_coloff);
+    }
   for (double* p : h->d_raw)
     if (p) cudaFree(p);
   if (h->proj.d_bpack) cudaFree(h->proj.d_bpack);
@@ -331,6 +333,17 @@ qtt_status_t upload_stage(qtt_plan* h, Stage& S, const double* const* cores) {
     cudaError_t e = qtt::wide_prepare(sp.NB, h->smem_optin);
     if (e != cudaSuccess) return from_cuda(e);
     S.ctas_per_sm = 1;
+    {   // epilogue column offsets: column n = ii r_out + b -> (ii << log2_q) r_out + b
+      const int log2_q = h->d - (sp.k1 - sp.k0 + 1);
+      const int nout = sp.n_i * sp.r_out;
+      std::vector<int64_t> co(static_cast<size_t>(nout));
+      for (int n = 0; n < nout; ++n)
+        co[size_t(n)] = (int64_t(n / sp.r_out) << log2_q) * sp.r_out + n % sp.r_out;
+      e = cudaMalloc(&S.d_coloff, co.size() * sizeof(int64_t));
+      if (e != cudaSuccess) return from_cuda(e);
+      e = cudaMemcpy(S.d_coloff, co.data(), co.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return from_cuda(e);
+    }
     const std::vector<double> W = super_core(cores, h->ranks.data(), sp.k0, sp.k1);
     const std::vector<double> pk = pack_wide(W.data(), sp);
     e = cudaMalloc(&S.d_bpack, pk.size() * sizeof(double));
@@ -413,6 +426,24 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
       tiles *= ks;
     }
     a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms)));
+    if (!proj) {
+      static const bool no_coloff = std::getenv("QTT_WIDE_NO_COLOFF") != nullptr;   // A/B
+      a.col_off = no_coloff ? nullptr : S.d_coloff;
+      if (tiles < (int64_t(1) << 31)) {   // tile -> (row tile, column block) by multiply-shift
+        const uint32_t dv = uint32_t(sp.ncb);
+        int l = 0;
+        while ((uint32_t(1) << l) < dv) ++l;
+        if ((dv & (dv - 1)) == 0) {
+          a.ncb_mul = 0;
+          a.ncb_shr = l;
+        } else {
+          a.ncb_mul = uint32_t(((uint64_t(1) << (31 + l)) / dv) + 1);
+          a.ncb_shr = l - 1;
+        }
+      } else {
+        a.col_off = nullptr;              // the generic epilogue (64-bit tile indices)
+      }
+    }
     e = qtt::launch_wide(a, st);
   } else if (sp.variant == qtt::kSmall) {
     e = qtt::launch_small(a, st);

@@ -22,6 +22,7 @@ struct Stage {
   int ctas_per_sm = 1;
   double* d_bpack = nullptr;   // DMMA fragment-packed (super-)core
   double* d_core = nullptr;    // raw core (generic kernel, single level only)
+  int64_t* d_coloff = nullptr; // wide stages: output-column offsets of the epilogue (LevelArgs::col_off)
 };
 
 struct StageEvents {

@@ -200,6 +200,47 @@ __device__ __forceinline__ void runs_write(const double (&c)[4][4], int r, doubl
       }
 }
 
+// The wide stage's plain epilogue with host-computed column offsets
+// (LevelArgs::col_off): out + rowbase(m) r_out + col_off[n] -- one L1-cached
+// load per column pair and one 64-bit multiply per row instead of the
+// generic column walk (tile_store), so the epilogue the tile's warps run
+// together is short (it is DMMA-idle time).
+template <int NBC>
+__device__ __forceinline__ void tile_store_cols(const double (&c)[NBC][4], const LevelArgs& p, int64_t m_first,
+                                                int n_first, int lane) {
+  const int g = lane >> 2, t0 = lane & 3;
+  const bool vec = (p.r_out & 1) == 0;
+  int64_t co[NBC];
+#pragma unroll
+  for (int nb = 0; nb < NBC; ++nb) {
+    const int n = n_first + nb * 8 + 2 * t0;
+    co[nb] = n < p.nout ? __ldg(p.col_off + n) : int64_t(-1);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t m = m_first + g + 8 * h;
+    if (m >= p.M) continue;
+    double* rowp = p.out + (m + (((m >> p.log2_q) * (p.n_i - 1)) << p.log2_q)) * p.r_out;
+#pragma unroll
+    for (int nb = 0; nb < NBC; ++nb) {
+      if (co[nb] < 0) continue;
+      double* dst = rowp + co[nb];
+      QTT_CHECK_OUT(p, dst, vec ? 2 : 1);
+      if (vec) {
+        *reinterpret_cast<double2*>(dst) = make_double2(c[nb][2 * h], c[nb][2 * h + 1]);
+      } else {
+        dst[0] = c[nb][2 * h];
+        const int n1 = n_first + nb * 8 + 2 * t0 + 1;   // odd r_out: the pair may wrap to the next ii
+        if (n1 < p.nout) {
+          const int64_t c1 = __ldg(p.col_off + n1);
+          QTT_CHECK_OUT(p, rowp + c1, 1);
+          rowp[c1] = c[nb][2 * h + 1];
+        }
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -288,9 +329,19 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
         split_store<NBC>(c, p, to, int(t - to * p.ksplit), warp, cw, slot, lane);
         continue;
       }
-      const int64_t rt = to / p.ncb;
-      const int cb = int(to - rt * p.ncb);
+      int64_t rt;
+      int cb;
+      if (!(MODE & 2) && p.col_off) {   // tile < 2^31: multiply-shift instead of a 64-bit divide
+        const uint32_t t32 = uint32_t(to);
+        const uint32_t q = p.ncb_mul ? (__umulhi(t32, p.ncb_mul) >> p.ncb_shr) : (t32 >> p.ncb_shr);
+        rt = q;
+        cb = int(t32 - q * uint32_t(p.ncb));
+      } else {
+        rt = to / p.ncb;
+        cb = int(to - rt * p.ncb);
+      }
       if (MODE & 2) scatter_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
+      else if (p.col_off) tile_store_cols<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
       else tile_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
       if ((MODE & 1) && p.done) {   // publish this warp's part of the tile to the D2H copy stream
         __threadfence();
