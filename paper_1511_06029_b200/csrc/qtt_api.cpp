@@ -573,8 +573,10 @@ qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host
       if (e != cudaSuccess) return from_cuda(e);
       h->h_elems = elems;
     }
-    // pipelined copies: one RHS, at least two stages, enough rows to chunk
-    if (nrhs == 1 && h->stages.size() >= 2 && h->shard_bits == 0 && !h->timing &&
+    // pipelined copies: one RHS, at least two stages, enough rows to chunk --
+    // and not a latency-bound size the fused apply runs in one launch (the
+    // same plan as qtt_apply, so both give the same bits)
+    if (nrhs == 1 && h->stages.size() >= 2 && h->shard_bits == 0 && !h->timing && !use_fused(h, 1) &&
         (h->N >> (h->stages.front().plan.k1 - h->stages.front().plan.k0 + 1)) >= 8 * 64 &&
         (h->N >> (h->stages.back().plan.k1 - h->stages.back().plan.k0 + 1)) >= 8 * 64) {
       void* old_ws = h->ws;

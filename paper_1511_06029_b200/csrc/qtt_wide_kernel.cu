@@ -465,7 +465,8 @@ __device__ __forceinline__ void split_reduce_one(const LevelArgs& p, int64_t to,
   }
   const int64_t rt = to / p.ncb;
   const int cb = int(to - rt * p.ncb);
-  tile_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
+  if (p.col_off) tile_store_cols<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
+  else tile_store<NBC>(c, p, rt * kDmmaRowsPerSubtile + rg * 16, (cb * NB + nb0) * 8, lane);
   if (p.done) {
     __threadfence();
     __syncwarp();

@@ -326,3 +326,20 @@ def test_fused_grid_gather_modes_bitwise():
         assert r.returncode == 0 and "digest" in r.stdout, r.stdout + r.stderr
         out.append(r.stdout.split("digest")[1].strip())
     assert out[0] == out[1]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_fused_apply_host_same_bits(qtt, name):
+    """qtt_apply_host on a handle whose applies are fused runs the same plan
+    (H2D, the fused launch, D2H), so its result is bitwise that of qtt_apply."""
+    _, cores, x = generate(name)
+    with qtt.QttOperator(cores) as op:
+        assert op.stages(1)[0]["variant"] == "fused"
+        yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        xh = torch.from_numpy(x).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        for _ in range(3):
+            yh.zero_()
+            op.apply_host(xh.numpy(), out=yh.numpy())
+            np.testing.assert_array_equal(yh.numpy(), yd)
+        np.testing.assert_array_equal(op.apply_host(x), yd)
