@@ -168,7 +168,11 @@ qtt_status_t qtt_apply_ws(qtt_handle_t h, const double* x, double* y, int64_t nr
  * qtt_apply_host -- end-to-end convenience: x_host, y_host are HOST arrays
  * (pinned or pageable) of N*nrhs doubles.  Copies x to the device on
  * `stream`, applies, copies y back, and synchronizes `stream` before
- * returning.  Device staging buffers are cached in the handle.
+ * returning.  Device staging buffers are cached in the handle.  Results are
+ * bitwise those of qtt_apply on the same handle: large single-RHS applies
+ * overlap the copies with the first / last stage (chunked launches of the
+ * same stage kernels); latency-bound handles run H2D, their one-launch
+ * apply, D2H.
  */
 qtt_status_t qtt_apply_host(qtt_handle_t h, const double* x_host, double* y_host,
                             int64_t nrhs, qtt_stream_t stream);
