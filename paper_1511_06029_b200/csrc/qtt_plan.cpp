@@ -37,10 +37,12 @@ constexpr double kHbm = 6.45e12 * 0.90;
 constexpr double kLaunch = 3.0e-6;
 // measured (profiles/, c3-c5 stages): 8 consumer warps (NB <= 8) reach ~0.84
 // of nominal against 12 warps' ~0.955; a wide tile pays a fixed epilogue
-// against its k-chunks, ~nch / (nch + 0.3)
+// against its k-chunks, ~nch / (nch + 0.15) (c3's K = 64 stage [1-6]: 0.93,
+// K = 128 pairs: 0.97 of the resident rate; 0.3 made the planner keep c3's
+// r = 32 single level, 0.4% slower, profiles/r02zl_ab_c3*.json)
 double fp64_rate(int NB, double nchunks) {
   const double warps = dmma_col_groups(NB) >= 3 ? 1.0 : 0.88;
-  return kFp64 * warps * (nchunks / (nchunks + 0.3));
+  return kFp64 * warps * (nchunks / (nchunks + 0.15));
 }
 constexpr double kL2 = 7.0e12;                   // L2 -> SM bytes the wide kernel may pull
 constexpr double kTileLatency = 1.5e-6;          // one tile: TMA round trip + epilogue
