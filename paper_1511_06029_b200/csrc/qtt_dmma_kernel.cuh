@@ -201,9 +201,18 @@ __global__ void __launch_bounds__(dmma_threads(NB), 1)
 level_dmma_kernel(const LevelArgs p) {
   constexpr int CG = dmma_col_groups(NB);
   constexpr int CW = kDmmaRowGroups * CG;         // consumer warps
+#ifdef QTT_UNEVEN_CG
+  // experiment: unequal column groups, so the warps of a sub-partition reach
+  // their epilogues at different times
+  constexpr int NBW = (NB + CG - 1) / CG + ((CG >= 2 && NB >= 2 * CG) ? 1 : 0);
+  constexpr int NB_1 = CG == 1 ? 0 : CG == 2 ? NB - NBW : (NB - NBW + 1) / 2 + (((NB - NBW) % 2 == 0) ? 1 : 0);
+  constexpr int NB_2 = NB - NBW - NB_1;
+  static_assert(NB_1 >= 0 && NB_2 >= 0, "split");
+#else
   constexpr int NBW = (NB + CG - 1) / CG;         // n-blocks per column group
   constexpr int NB_1 = (NB - NBW) < NBW ? (NB - NBW) : NBW;
   constexpr int NB_2 = NB - NBW - NB_1;
+#endif
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
