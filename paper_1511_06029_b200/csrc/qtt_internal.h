@@ -68,7 +68,18 @@ constexpr int kMaxStageLevels = 10;  // most levels one merged stage may cover
 // column block, k-chunks of kWideBK; instances for NB in {4, 8, 12, 16}.
 constexpr int kWideKBC = 2;                  // k16 blocks per chunk
 constexpr int kWideBK = 16 * kWideKBC;       // 32
-constexpr int kWideStages = 4;
+// experiment knobs (A/B builds): ring depth, widest column block,
+// persistent CTAs per SM of the wide kernel
+#ifndef QTT_WIDE_STAGES
+#define QTT_WIDE_STAGES 4
+#endif
+#ifndef QTT_WIDE_NB_CAP
+#define QTT_WIDE_NB_CAP 16
+#endif
+#ifndef QTT_WIDE_CTAS
+#define QTT_WIDE_CTAS 1
+#endif
+constexpr int kWideStages = QTT_WIDE_STAGES;
 constexpr size_t kWideMaxCoreBytes = size_t(64) << 20;
 QTT_HD constexpr bool wide_instantiated(int NB) { return NB == 4 || NB == 8 || NB == 12 || NB == 16; }
 

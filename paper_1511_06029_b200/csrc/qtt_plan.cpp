@@ -180,8 +180,9 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
     // it beats 96-column blocks of whole ii blocks too: c4 levels 1-7 5.96 vs 6.04 ms)
     // For nout > 96 also try 96-column blocks: less padding when nout mod 128 is
     // small or just below 96 (r = 95: 2 x 96 = 192 computed columns instead of 256).
-    const int NBdef = nout <= 32 ? 4 : nout <= 64 ? 8 : nout <= 96 ? 12 : 16;
-    const bool try96 = nout > 96 && (nout + 95) / 96 * 96 < (nout + 127) / 128 * 128;
+    const int NBfit = nout <= 32 ? 4 : nout <= 64 ? 8 : nout <= 96 ? 12 : 16;
+    const int NBdef = NBfit < QTT_WIDE_NB_CAP ? NBfit : QTT_WIDE_NB_CAP;
+    const bool try96 = QTT_WIDE_NB_CAP >= 12 && nout > 96 && (nout + 95) / 96 * 96 < (nout + 127) / 128 * 128;
     for (const int NBw : {NBdef, try96 ? 12 : 0}) {
     if (NBw == 0) continue;
     const size_t smem = wide_smem_bytes(NBw);

@@ -425,7 +425,7 @@ cudaError_t launch_stage(qtt_plan* h, const Stage& S, bool proj, const double* i
       a.partial = split->partial;
       tiles *= ks;
     }
-    a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms)));
+    a.grid = int(std::min<int64_t>(tiles, int64_t(h->num_sms) * (sp.NB <= 8 ? QTT_WIDE_CTAS : 1)));
     if (!proj) {
       static const bool no_coloff = std::getenv("QTT_WIDE_NO_COLOFF") != nullptr;   // A/B
       a.col_off = no_coloff ? nullptr : S.d_coloff;

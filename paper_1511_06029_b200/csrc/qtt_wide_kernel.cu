@@ -355,7 +355,7 @@ __device__ __forceinline__ void consumer(const LevelArgs& p, uint64_t* full, uin
 // MODE flags: 1 host-copy hooks (qtt_apply_host), 2 fused shard exchange, 4 split-K;
 // instances 0, 1, 2, 4, 5
 template <int NB, int MODE>
-__global__ void __launch_bounds__(wide_threads(NB), 1)
+__global__ void __launch_bounds__(wide_threads(NB), NB <= 8 ? QTT_WIDE_CTAS : 1)
 wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   constexpr int CG = wide_col_groups(NB);
   constexpr int CW = kDmmaRowGroups * CG;
@@ -367,8 +367,16 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
   uint64_t* empty = full + kMaxStages;
   int64_t* tile_id = reinterpret_cast<int64_t*>(empty + kMaxStages);
   // the 128-byte swizzle needs 1024-byte aligned boxes
+#ifdef QTT_WIDE_GENERIC_RING
   unsigned char* ring = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem) + kBarBytes + 1023) & ~uintptr_t(1023));
+#else
+  // as an offset from the shared array, so the operand loads stay LDS (an
+  // integer round trip of the pointer made them generic LD.E.128, with
+  // 64-bit addresses and a spill in the NB = 16 instance)
+  const uint32_t smem_base = dmma::smem_u32(smem);
+  unsigned char* ring = smem + (((smem_base + kBarBytes + 1023u) & ~1023u) - smem_base);
+#endif
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
