@@ -172,9 +172,16 @@ __device__ __forceinline__ void consumer_loop(const LevelArgs& p, uint64_t* full
     const int b = n - i * p.RP;
     coff[nb] = (i >= p.n_i || b >= p.r_out) ? int64_t(-1) : ((int64_t(i) << p.log2_q) * p.r_out + b);
   }
-  for (int it = 0;; ++it) {
-    const int s = it % S;
-    const uint32_t ph = uint32_t(it / S) & 1u;
+  // ring stage and phase kept as counters: `it % S`, `it / S` with the runtime
+  // S cost a ~35-instruction reciprocal sequence in front of every tile's
+  // barrier wait (ncu source page), which the warps of a sub-partition run together
+  int s = 0;
+  uint32_t ph = 0;
+  for (;; ++s) {
+    if (s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
     mbar_wait(&full[s], ph);
     const int64_t t = tile_id[s];
     if (t < 0) break;
@@ -248,9 +255,13 @@ level_dmma_kernel(const LevelArgs p) {
     if (lane == 0) {
       const int64_t M = p.M;
       const int64_t nstage_tiles = (M + rows_per_stage - 1) / rows_per_stage;
-      for (int it = 0;; ++it) {
-        const int s = it % S;
-        const uint32_t ph = uint32_t(it / S) & 1u;
+      int s = 0;
+      uint32_t ph = 0;
+      for (;; ++s) {
+        if (s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
         mbar_wait(&empty[s], ph ^ 1u);
         const int64_t t = atomicAdd(p.tile_counter, 1);
         if (t >= nstage_tiles) {
