@@ -13,15 +13,19 @@
 // reading/writing the grid side in full 128-byte (dim 3) or 512-byte (dim 2)
 // rows and the QTT side as one contiguous 32 KiB run, through an XOR-swizzled
 // smem tile (bank-conflict free both ways), streaming loads/stores (.cs).
-// Pack, whose scattered side is the read side, moves two x-adjacent tiles per
-// CTA (consecutive in QTT order) so its grid reads are 256-byte (dim 3) rows;
-// consecutive CTAs take x-adjacent tiles.  Measured at 256^3: pack 79% of HBM
-// (70% with one tile), unpack 92%; one tile keeps static smem (a dynamic
-// 32 KiB tile cost unpack 15%, from the carveout the driver picked).
+// Pack, whose scattered side is the read side, reads 256-byte (dim 3) grid
+// rows: in 3-D a CTA moves the z_3 half of two x-adjacent tiles (32 x 16 x 8
+// points, 32 KiB of static smem, two 16 KiB QTT runs; morton_pack3_half_kernel),
+// in 2-D two x-adjacent tiles (64 KiB dynamic smem); consecutive CTAs take
+// x-adjacent units.  Measured at 256^3: pack 5.2 TB/s = 80% of HBM (5.1 with two
+// whole tiles per CTA, 70% with one tile and 128-byte rows), unpack 92%; one
+// tile keeps static smem (a dynamic 32 KiB tile cost unpack 15%, from the
+// carveout the driver picked).
 // Grids smaller than one tile use a per-element kernel.
 #include "qtt_internal.h"
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace qtt {
@@ -158,6 +162,61 @@ __global__ void __launch_bounds__(kThreads) morton_tile_kernel(const double* __r
   }
 }
 
+// 3-D pack, half-cube units: 32 (x) x 16 (y) x 8 (z) grid points = the z_3
+// half of two x-adjacent 16^3 tiles.  The grid reads are 256-byte rows (as with
+// two tiles per CTA), the QTT side is two contiguous 16 KiB runs (the half zh
+// of QTT blocks tq and tq + 1), and the unit is 32 KiB of STATIC shared memory,
+// so 7 CTAs fit an SM as in unpack (two whole tiles need 64 KiB: 3 CTAs).
+__global__ void __launch_bounds__(kThreads) morton_pack3_half_kernel(const double* __restrict__ in,
+                                                                     double* __restrict__ out, int levels,
+                                                                     int64_t N) {
+  constexpr int B = 4, R = 16, RW = 32;
+  __shared__ __align__(16) double tile[kTile];
+  const int64_t units_per_rhs = N >> kTileBits;            // (N / 4096 / 2 tile pairs) x 2 halves
+  const int64_t s = blockIdx.x / units_per_rhs;
+  const int64_t hb = blockIdx.x - s * units_per_rhs;
+  // consecutive CTAs: x-adjacent tile pairs, then the two z halves, then y, z
+  const int tb = levels - B;
+  const int64_t xm = (int64_t(1) << (tb - 1)) - 1, m = (int64_t(1) << tb) - 1;
+  const int64_t cx = (hb & xm) << (B + 1);
+  const int64_t r0 = hb >> (tb - 1);
+  const int zh = int(r0 & 1);
+  const int64_t r = r0 >> 1;
+  const int64_t cy = (r & m) << B, cz = (r >> tb) << B;
+  int64_t tq = 0;                                          // QTT index of the first tile
+  for (int l = 0; l < tb; ++l) {
+    tq |= ((cx >> (B + l)) & 1) << (3 * l);
+    tq |= ((cy >> (B + l)) & 1) << (3 * l + 1);
+    tq |= ((cz >> (B + l)) & 1) << (3 * l + 2);
+  }
+  const int64_t n = int64_t(1) << levels;
+  const int64_t gbase = s * N + ((cz + 8 * zh) * n + cy) * n + cx;
+  const int64_t qbase = s * N + (tq << kTileBits) + (int64_t(zh) << (kTileBits - 1));
+  double2* tile2 = reinterpret_cast<double2*>(tile);
+#pragma unroll
+  for (int e = 2 * threadIdx.x; e < kTile; e += 2 * kThreads) {
+    const int x = e & (RW - 1), row = e >> 5;              // row = z * 16 + y, z in 0..7
+    const int y = row & (R - 1), z = row >> B;
+    const double2* src = reinterpret_cast<const double2*>(in + gbase + (int64_t(z) * n + y) * n + x);
+    tile2[(row * RW + (x ^ swz<3>(row))) >> 1] = __ldcs(src);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 2 * threadIdx.x; u < kTile; u += 2 * kThreads) {
+    const int t = u >> (kTileBits - 1), w = u & ((kTile >> 1) - 1);   // tile of the pair, index in its half
+    int x = t * R, y = 0, z = 0;
+#pragma unroll
+    for (int l = 0; l < B; ++l) {
+      x |= ((w >> (3 * l)) & 1) << l;
+      y |= ((w >> (3 * l + 1)) & 1) << l;
+      if (l < B - 1) z |= ((w >> (3 * l + 2)) & 1) << l;
+    }
+    const int row = z * R + y;
+    __stcs(reinterpret_cast<double2*>(out + qbase + (int64_t(t) << kTileBits) + w),
+           tile2[(row * RW + (x ^ swz<3>(row))) >> 1]);
+  }
+}
+
 template <int DIM, bool PACK, int TX>
 cudaError_t launch_tile(const double* in, double* out, int levels, int64_t N, int64_t nrhs, cudaStream_t st) {
   const int64_t blocks = nrhs * ((N >> kTileBits) / TX);
@@ -187,6 +246,13 @@ cudaError_t launch_morton(const double* in, double* out, int dim, int levels, in
     // side is the write side, which one tile per CTA already streams at 92%
     const bool two = levels >= (kTileBits / dim) + 1;
     if (dim == 3) {
+      static const bool whole = std::getenv("QTT_MORTON_PACK_WHOLE") != nullptr;   // A/B: two whole tiles per CTA
+      if (pack && two && !whole) {
+        const int64_t blocks = nrhs * (N >> kTileBits);
+        if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
+        morton_pack3_half_kernel<<<int(blocks), kThreads, 0, st>>>(in, out, levels, N);
+        return cudaGetLastError();
+      }
       if (pack) return two ? launch_tile<3, true, 2>(in, out, levels, N, nrhs, st)
                            : launch_tile<3, true, 1>(in, out, levels, N, nrhs, st);
       return launch_tile<3, false, 1>(in, out, levels, N, nrhs, st);
