@@ -257,13 +257,17 @@ level_dmma_kernel(const LevelArgs p) {
       const int64_t nstage_tiles = (M + rows_per_stage - 1) / rows_per_stage;
       int s = 0;
       uint32_t ph = 0;
+      bool first = true;
       for (;; ++s) {
         if (s == S) {
           s = 0;
           ph ^= 1u;
         }
         mbar_wait(&empty[s], ph ^ 1u);
-        const int64_t t = atomicAdd(p.tile_counter, 1);
+        // the first tile is the CTA's own index (grid <= tiles): no L2 atomic, with every
+        // producer of the grid queueing on one address, in front of the first load
+        const int64_t t = first ? int64_t(blockIdx.x) : int64_t(gridDim.x) + atomicAdd(p.tile_counter, 1);
+        first = false;
         if (t >= nstage_tiles) {
           tile_id[s] = -1;
           mbar_arrive(&full[s]);

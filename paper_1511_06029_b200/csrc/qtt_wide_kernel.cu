@@ -397,8 +397,11 @@ wide_dmma_kernel(const LevelArgs p, const __grid_constant__ CUtensorMap tmA) {
       const int64_t ntiles = ((M + kDmmaRowsPerSubtile - 1) / kDmmaRowsPerSubtile) * p.ncb * ((MODE & 4) ? p.ksplit : 1);
       const uint32_t bbytes = b_chunk_bytes(NB);
       int it = 0;
+      bool first = true;
       for (;;) {
-        const int64_t t = atomicAdd(p.tile_counter, 1);
+        // the first tile is the CTA's own index (grid <= tiles): no L2 atomic in front of the first load
+        const int64_t t = first ? int64_t(blockIdx.x) : int64_t(gridDim.x) + atomicAdd(p.tile_counter, 1);
+        first = false;
         if (t >= ntiles) {
           const int s = it % kWideStages;
           mbar_wait(&empty[s], (uint32_t(it / kWideStages) & 1u) ^ 1u);
