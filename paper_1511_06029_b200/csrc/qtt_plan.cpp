@@ -34,7 +34,10 @@ namespace {
 // bandwidth as measured in MEASURED_PEAKS.json (~6.5 TB/s), launch ~3 us.
 constexpr double kFp64 = 37.2e12 * 0.955;     // DMMA rate of the resident kernel with 12 consumer warps
 constexpr double kHbm = 6.45e12 * 0.90;
-constexpr double kLaunch = 3.0e-6;
+#ifndef QTT_PLAN_KLAUNCH
+#define QTT_PLAN_KLAUNCH 3.0e-6
+#endif
+constexpr double kLaunch = QTT_PLAN_KLAUNCH;   // per-launch cost in the stage DP (build knob for calibration)
 // measured (profiles/, c3-c5 stages): 8 consumer warps (NB <= 8) reach ~0.84
 // of nominal against 12 warps' ~0.955; a wide tile pays a fixed epilogue
 // against its k-chunks, ~nch / (nch + 0.15) (c3's K = 64 stage [1-6]: 0.93,
