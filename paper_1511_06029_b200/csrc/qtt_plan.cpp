@@ -34,6 +34,10 @@ namespace {
 // bandwidth as measured in MEASURED_PEAKS.json (~6.5 TB/s), launch ~3 us.
 constexpr double kFp64 = 37.2e12 * 0.955;     // DMMA rate of the resident kernel with 12 consumer warps
 constexpr double kHbm = 6.45e12 * 0.90;
+// most warp tiles per SM a stage may have and still run on the small (L2-fed warp-tile) kernel
+#ifndef QTT_SMALL_MAX_WT_PER_SM
+#define QTT_SMALL_MAX_WT_PER_SM 24
+#endif
 #ifndef QTT_PLAN_KLAUNCH
 #define QTT_PLAN_KLAUNCH 3.0e-6
 #endif
@@ -230,7 +234,7 @@ static bool stage_shape(const int64_t* ranks, int k0, int k1, int64_t n, size_t 
   if (!no_small && wbytes <= double(kWideMaxCoreBytes) && sp->K % 2 == 0) {
     const int ncb = (nout + kSmallCols - 1) / kSmallCols;
     const double wt = std::ceil(M / kSmallRows) * ncb;        // warp tiles
-    if (wt <= kSms * 64) {
+    if (wt <= kSms * QTT_SMALL_MAX_WT_PER_SM) {
       const double nq = std::ceil(sp->K / double(kSmallK));
       const double flops = 2.0 * wt * kSmallRows * kSmallCols * nq * kSmallK;
       const double blocks = std::ceil(wt / kSmallWarps);
