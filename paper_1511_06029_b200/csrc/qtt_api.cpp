@@ -142,12 +142,13 @@ static qtt_status_t create_impl(qtt_handle_t* out, int d, const int64_t* ranks, 
         // The two models' residuals against 16 measured mid-size cases (d = 14..19,
         // r = 4..48; profiles/r02zzg_fused_decision.json): the fused launch runs
         // ~5 us under its estimate when small and ~30% over it when the estimate
-        // passes ~45 us; per-stage plans run ~1 us per launch over theirs.
+        // passes ~45 us; per-stage plans ran ~1 us per launch over theirs when the
+        // stage DP charged 3 us per launch.
         // (The 5 us only up to 4 RHS: at 8-16 RHS the fused launch already runs over
         // its estimate -- d = 13, r = 8 x 16 RHS 37.9 us against 27.5 estimated and 26.7
         // per-stage.)
         ef = ef - (p <= 4 ? 5.0e-6 : 0.0) + 0.6 * std::max(0.0, ef - 27.0e-6);
-        er += 1.0e-6 * double(rp.size());
+        er -= 1.0e-6 * double(rp.size());   // the stage DP charges 5 us per launch (it plans better with it); ~4 measured
         if (std::getenv("QTT_DEBUG"))
           std::fprintf(stderr, "qtt: fused plan (%zu stages) at %lld RHS: est %.2f us vs per-stage plan %.2f us\n",
                        fp.size(), (long long)p, ef * 1e6, er * 1e6);

@@ -39,7 +39,7 @@ constexpr double kHbm = 6.45e12 * 0.90;
 #define QTT_SMALL_MAX_WT_PER_SM 24
 #endif
 #ifndef QTT_PLAN_KLAUNCH
-#define QTT_PLAN_KLAUNCH 3.0e-6
+#define QTT_PLAN_KLAUNCH 5.0e-6
 #endif
 constexpr double kLaunch = QTT_PLAN_KLAUNCH;   // per-launch cost in the stage DP (build knob for calibration)
 // measured (profiles/, c3-c5 stages): 8 consumer warps (NB <= 8) reach ~0.84
